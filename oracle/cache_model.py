@@ -1,0 +1,72 @@
+"""Reference model of the attention-guided HBM chunk cache (TEST INFRASTRUCTURE).
+
+Follows PAPER.md §4.4 (lines 424-455) step by step, specialised to the
+B200 design of SURVEY §8(a) A4/A6/A9 (per-layer slot partitions):
+
+* every (layer, chunk) keeps I (cumulative importance) and F (access count),
+  including chunks not resident (the "in-memory table");
+* S_j = I_j * F_j  (Eq. 2);
+* before a load, the requested ids are checked against the cache;
+  misses take free slots (ascending slot index), then slots of evicted residents:
+  the lowest (S, j) residents that are not requested ("Both heaps will evict
+  low-scored ContiguousChunks"; ties by (S, l, j));
+* after the layer: I_j += A_j, F_j += 1 for the selected ids.
+
+Pure integer/slot bookkeeping plus the float compare of S; the GPU planner must
+reproduce this exactly when S values are exact (integers), and the tests use such.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+class CacheModel:
+    def __init__(self, num_layers: int, num_chunks: int, slots_per_layer: int):
+        self.L, self.m, self.P = num_layers, num_chunks, slots_per_layer
+        self.slot_of = np.full((num_layers, num_chunks), -1, dtype=np.int64)
+        self.owner = np.full((num_layers, slots_per_layer), -1, dtype=np.int64)
+        self.I = np.zeros((num_layers, num_chunks))
+        self.F = np.zeros((num_layers, num_chunks), dtype=np.int64)
+
+    def score(self, layer: int) -> np.ndarray:
+        """S_j = I_j x F_j  (Eq. 2)."""
+        return self.I[layer] * self.F[layer]
+
+    def plan(self, layer: int, ids, limit: int | None = None):
+        """Hit/miss check and slot assignment for `ids` at `layer`.
+
+        Returns (hits, loads) where loads is a list of (chunk, slot) in ascending
+        chunk order; at most `limit` misses are loaded (prefetch quota)."""
+        ids = [int(j) for j in sorted(ids)]
+        req = set(ids)
+        hits = [j for j in ids if self.slot_of[layer, j] >= 0]
+        misses = [j for j in ids if self.slot_of[layer, j] < 0]
+        if limit is not None:
+            misses = misses[:limit]
+        free = [s for s in range(self.P) if self.owner[layer, s] < 0]
+        need = len(misses) - len(free)
+        victims = []
+        if need > 0:
+            S = self.score(layer)
+            resident = [int(self.owner[layer, s]) for s in range(self.P)
+                        if self.owner[layer, s] >= 0 and int(self.owner[layer, s]) not in req]
+            resident.sort(key=lambda j: (S[j], j))
+            if need > len(resident):
+                raise RuntimeError("cache too small for the requested set")
+            victims = resident[:need]
+        slots = free[:len(misses)] + [int(self.slot_of[layer, j]) for j in victims]
+        for j in victims:
+            self.owner[layer, self.slot_of[layer, j]] = -1
+            self.slot_of[layer, j] = -1
+        loads = []
+        for j, s in zip(misses, slots):
+            self.slot_of[layer, j] = s
+            self.owner[layer, s] = j
+            loads.append((j, s))
+        return hits, loads, victims
+
+    def update(self, layer: int, ids, A) -> None:
+        """I_j += A_j, F_j += 1 for every selected chunk."""
+        for j in ids:
+            self.I[layer, int(j)] += float(A[int(j)])
+            self.F[layer, int(j)] += 1

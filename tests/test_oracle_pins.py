@@ -1,0 +1,325 @@
+"""Pins of oracle/ against what the paper and mathematics fix (no GPU).
+
+Each test names the pin type of SURVEY §8(c): worked example (tests/golden),
+closed form, invariant, metamorphic relation, library special case, brute force.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from oracle import brute
+from synth import CONFIGS, bf16_round, make_prefix, make_request
+
+
+def rand_case(seed=0, n=60, c=8, ns=4, hq=4, hkv=2, d=8, scale=1.0):
+    g = np.random.default_rng(seed)
+    Qs = g.standard_normal((ns, hq, d)) * scale
+    Kp = g.standard_normal((n, hkv, d))
+    Vp = g.standard_normal((n, hkv, d))
+    Ks = g.standard_normal((ns, hkv, d))
+    Vs = g.standard_normal((ns, hkv, d))
+    return Qs, Ks, Vs, Kp, Vp
+
+
+# ------------------------------------------------------------ worked examples
+def test_geometry_worked_examples(golden):
+    for e in golden["chunk_count"]:
+        assert O.chunk_count(e["n"], e["c"]) == e["m"]
+    for e in golden["chunk_range"]:
+        assert O.chunk_range(e["j"], e["n"], e["c"]) == tuple(e["range"])
+    with pytest.raises(ValueError):
+        O.chunk_count(0, 16)
+    with pytest.raises(ValueError):
+        O.chunk_range(7, 100, 16)
+
+
+@pytest.mark.parametrize("n,c", [(1, 1), (100, 16), (64, 64), (65, 64), (131072, 32), (37, 5)])
+def test_partition_property(n, c):
+    m = O.chunk_count(n, c)
+    cover = np.zeros(n, dtype=int)
+    for j in range(m):
+        s, e = O.chunk_range(j, n, c)
+        assert e > s
+        cover[s:e] += 1
+    assert (cover == 1).all()
+    assert m * c >= n > (m - 1) * c
+
+
+def test_chunk_scores_worked_examples(golden):
+    for e in golden["chunk_scores"]:
+        np.testing.assert_allclose(O.chunk_scores(e["a"], e["c"]), e["A"], rtol=0, atol=1e-15)
+
+
+def test_chunk_scores_conservation():
+    a = np.random.default_rng(1).random(1001)
+    for c in (1, 3, 16, 1001, 2000):
+        A = O.chunk_scores(a, c)
+        assert A.shape[0] == O.chunk_count(1001, c)
+        assert abs(A.sum() - a.sum()) <= 1e-12 * a.sum()
+
+
+def test_topk_worked_examples(golden):
+    for e in golden["select_topk"]:
+        assert O.select_topk(e["A"], e["k"]).tolist() == e["ids"]
+    for e in golden["coverage_ratio"]:
+        assert O.coverage_ratio(e["a"], e["b"]) == e["ratio"]
+
+
+def test_budget_floor_rule(golden):
+    for e in golden["budget_k_floor_rule"]:
+        assert O.budget_chunks(e["n"], e["c"], e["budget_bp"]) == e["k"]
+        cfg = CONFIGS[e["cfg"]]
+        assert O.budget_chunks(cfg.prefix_len, cfg.chunk_size, cfg.budget_bp) == e["k"]
+    assert O.budget_chunks(100, 16, 1) == 1          # max(1, .)
+    assert O.budget_chunks(100, 16, 10000) == 6      # floor(100/16) = 6 of m = 7
+    assert O.budget_chunks(96, 16, 10000) == 6       # = m
+
+
+# ------------------------------------------------------------ closed forms
+def test_token_scores_uniform_closed_form(golden):
+    # single query, all-equal logits (q = 0), n = 4 -> a = 1/4 each
+    Qs = np.zeros((1, 1, 4))
+    Kp = np.random.default_rng(0).standard_normal((4, 1, 4))
+    a, lam = O.token_scores(Qs, Kp, 1)
+    np.testing.assert_allclose(a, golden["token_scores"][0]["a"], atol=1e-15)
+    assert abs(lam[0, 0] - math.log(4)) < 1e-15
+
+
+def test_token_scores_saturation():
+    # one logit +50 vs 0 -> its a ~ 1; logits = q.k / sqrt(d), d = 1
+    Qs = np.ones((1, 1, 1))
+    Kp = np.array([0.0, 50.0, 0.0, 0.0]).reshape(4, 1, 1)
+    a, _ = O.token_scores(Qs, Kp, 1)
+    assert a[1] > 0.999999 and abs(a[1] - 1 / (1 + 3 * math.exp(-50))) < 1e-15
+
+
+def test_token_scores_conservation_and_rows():
+    Qs, Ks, Vs, Kp, Vp = rand_case(3, n=200, ns=5, hq=6, hkv=3, d=16, scale=3.0)
+    a, lam = O.token_scores(Qs, Kp, 2)
+    assert abs(a.sum() - 5 * 6) < 1e-12 * 30            # sum_i a_i = n_s * Hq
+    assert (a >= 0).all()
+    # FULLROW normalisation also counts suffix keys -> strictly less mass on the prefix
+    a2, lam2 = O.token_scores(Qs, Kp, 2, O.NORM_FULLROW, Ks)
+    assert a2.sum() < a.sum() and (lam2 > lam).all()
+
+
+def test_lambda_is_log_partition():
+    Qs, Ks, Vs, Kp, Vp = rand_case(4, n=30, ns=2, hq=2, hkv=1, d=4)
+    lam = O.row_lse(Qs, Kp, 2)
+    for h in range(2):
+        for r in range(2):
+            z = sum(math.exp(float(Qs[r, h] @ Kp[i, 0]) / 2.0) for i in range(30))
+            assert abs(lam[h, r] - math.log(z)) < 1e-12
+
+
+def test_uniform_keys_tie_break():
+    # all prefix keys equal -> every full chunk scores c*n_s*Hq/n, all tie -> S = {0..k-1}
+    n, c, ns, hq = 64, 8, 3, 4
+    g = np.random.default_rng(5)
+    Qs = g.standard_normal((ns, hq, 8))
+    Kp = np.tile(g.standard_normal((1, 2, 8)), (n, 1, 1))
+    a, _ = O.token_scores(Qs, Kp, 2)
+    A = O.chunk_scores(a, c)
+    np.testing.assert_allclose(A, c * ns * hq / n, rtol=1e-13)
+    assert O.select_topk(np.full(8, c * ns * hq / n), 3).tolist() == [0, 1, 2]
+
+
+def test_single_key_degenerate_closed_form():
+    # k = 1, c = 1, n_s = 1: the suffix key logit is >= 1e3 below the chosen token's
+    # -> O = v of the chosen prefix token (exact to fp64 underflow)
+    d = 4
+    Qs = np.ones((1, 1, d))
+    Kp = np.array([[[1.0] * d], [[1000.0] * d], [[-1.0] * d]])
+    Vp = np.arange(3 * d, dtype=float).reshape(3, 1, d)
+    Ks = np.full((1, 1, d), -1000.0)
+    Vs = np.full((1, 1, d), 7.0)
+    res = O.reprefill_layer(Qs, Ks, Vs, Kp, Vp, c=1, k=1, G=1)
+    assert res["ids"].tolist() == [1]
+    np.testing.assert_array_equal(res["out"][0, 0], Vp[1, 0])
+
+
+# ------------------------------------------------------------ metamorphic
+def test_shift_invariance():
+    Qs, Ks, Vs, Kp, Vp = rand_case(6, n=96, c=8, ns=4)
+    b = np.random.default_rng(7).standard_normal((1, 2, 8))
+    r0 = O.reprefill_layer(Qs, Ks, Vs, Kp, Vp, c=8, k=3, G=2)
+    r1 = O.reprefill_layer(Qs, Ks + b, Vs, Kp + b, Vp, c=8, k=3, G=2)
+    np.testing.assert_allclose(r1["A"], r0["A"], rtol=1e-10)
+    assert r1["ids"].tolist() == r0["ids"].tolist()
+    np.testing.assert_allclose(r1["out"], r0["out"], atol=1e-10)
+
+
+def test_value_independence_of_selection():
+    Qs, Ks, Vs, Kp, Vp = rand_case(8, n=96, c=8)
+    r0 = O.reprefill_layer(Qs, Ks, Vs, Kp, Vp, c=8, k=4, G=2)
+    r1 = O.reprefill_layer(Qs, Ks, -Vs * 3, Kp, Vp * 5 + 1, c=8, k=4, G=2)
+    np.testing.assert_array_equal(r1["A"], r0["A"])
+    assert r1["ids"].tolist() == r0["ids"].tolist()
+
+
+# ------------------------------------------------------------ top-k
+@pytest.mark.parametrize("seed", range(8))
+def test_topk_brute_force_subsets(seed):
+    g = np.random.default_rng(seed)
+    m = int(g.integers(2, 13))
+    A = g.integers(0, 5, m).astype(float) if seed % 2 else g.random(m)  # ties on odd seeds
+    for k in range(1, m + 1):
+        assert O.select_topk(A, k).tolist() == brute.best_subset(A.tolist(), k)
+
+
+def test_topk_nesting():
+    A = np.random.default_rng(9).integers(0, 20, 40).astype(float)
+    prev = set()
+    for k in range(1, 41):
+        cur = set(O.select_topk(A, k).tolist())
+        assert prev <= cur and len(cur) == k
+        prev = cur
+
+
+def test_c1_equals_token_level_topk():
+    # c = 1: chunk top-k == token-level top-k of a (H2O-style), via np.lexsort
+    Qs, Ks, Vs, Kp, Vp = rand_case(10, n=50, ns=3, scale=2.0)
+    a, _ = O.token_scores(Qs, Kp, 2)
+    A = O.chunk_scores(a, 1)
+    order = np.lexsort((np.arange(50), -a))
+    for k in (1, 5, 17, 50):
+        assert O.select_topk(A, k).tolist() == sorted(order[:k].tolist())
+
+
+# ------------------------------------------------------------ attention
+def _sdpa_dense(Qs, Ks, Vs, Kp, Vp, G):
+    """Dense causal attention over [prefix; suffix] via torch SDPA in fp64 (library routine)."""
+    ns, hq, d = Qs.shape
+    n = Kp.shape[0]
+    K = np.concatenate([Kp, Ks], 0)
+    V = np.concatenate([Vp, Vs], 0)
+    q = torch.tensor(Qs).permute(1, 0, 2)                              # [Hq, n_s, d]
+    k = torch.tensor(K).permute(1, 0, 2).repeat_interleave(G, dim=0)   # [Hq, n+n_s, d]
+    v = torch.tensor(V).permute(1, 0, 2).repeat_interleave(G, dim=0)
+    mask = torch.ones(ns, n + ns, dtype=torch.bool)
+    mask[:, n:] = torch.tril(torch.ones(ns, ns, dtype=torch.bool))
+    o = torch.nn.functional.scaled_dot_product_attention(q, k, v, attn_mask=mask)
+    return o.permute(1, 0, 2).numpy()
+
+
+@pytest.mark.parametrize("n,c", [(64, 8), (61, 8), (40, 1)])
+def test_budget_all_equals_dense_attention(n, c):
+    # k = m: the method is exactly dense causal attention (north_star pin)
+    Qs, Ks, Vs, Kp, Vp = rand_case(11, n=n, c=c, ns=5, hq=6, hkv=2, d=16, scale=2.0)
+    m = O.chunk_count(n, c)
+    res = O.reprefill_layer(Qs, Ks, Vs, Kp, Vp, c=c, k=m, G=3)
+    assert res["ids"].tolist() == list(range(m))
+    np.testing.assert_allclose(res["out"], _sdpa_dense(Qs, Ks, Vs, Kp, Vp, 3), atol=1e-12)
+
+
+def test_split_merge_identity():
+    Qs, Ks, Vs, Kp, Vp = rand_case(12, n=80, c=8, ns=4, scale=2.0)
+    toks = O.kept_token_index([0, 3, 5, 9], 80, 8)
+    full = O.attention(Qs, Ks, Vs, Kp, Vp, toks, 2)
+    p1 = O.attention(Qs, Ks, Vs, Kp, Vp, toks[:10], 2, include_suffix=False)
+    p2 = O.attention(Qs, Ks, Vs, Kp, Vp, toks[10:], 2, include_suffix=True)
+    p3 = O.attention(Qs, Ks, Vs, Kp, Vp, [], 2, include_suffix=False)  # empty part: weight 0
+    for parts in ([p1, p2], [p2, p1], [p1, p3, p2]):
+        Om, lm = O.lse_merge(parts)
+        np.testing.assert_allclose(Om, full[0], atol=1e-13)
+        np.testing.assert_allclose(lm, full[1], atol=1e-13)
+    # invariant to the order of kept chunks
+    perm = O.attention(Qs, Ks, Vs, Kp, Vp, toks[::-1], 2)
+    np.testing.assert_allclose(perm[0], full[0], atol=1e-13)
+
+
+@pytest.mark.parametrize("W", [2, 3, 4, 8])
+@pytest.mark.parametrize("norm", [O.NORM_PREFIX, O.NORM_FULLROW])
+def test_sharding_identity(W, norm):
+    Qs, Ks, Vs, Kp, Vp = rand_case(13, n=200, c=8, ns=4, hq=4, hkv=2, d=8, scale=2.5)
+    k = 6
+    ref = O.reprefill_layer(Qs, Ks, Vs, Kp, Vp, c=8, k=k, G=2, norm=norm)
+    sh = O.sharded_reprefill_layer(W, Qs, Ks, Vs, Kp, Vp, c=8, k=k, G=2, norm=norm)
+    assert sh["ids"].tolist() == ref["ids"].tolist()
+    np.testing.assert_allclose(sh["A"], ref["A"], rtol=1e-11)
+    np.testing.assert_allclose(sh["Lambda"], ref["Lambda"], rtol=1e-13)
+    np.testing.assert_allclose(sh["out"], ref["out"], atol=1e-12)
+
+
+# ------------------------------------------------------------ brute force
+@pytest.mark.parametrize("seed", range(4))
+def test_tiny_brute_force(seed):
+    g = np.random.default_rng(100 + seed)
+    n, c = int(g.integers(9, 64)), int(g.integers(1, 6))
+    ns, hkv, G, d = int(g.integers(1, 5)), int(g.integers(1, 3)), int(g.integers(1, 3)), int(g.integers(2, 9))
+    hq = hkv * G
+    Qs, Ks, Vs, Kp, Vp = (g.standard_normal(s) * 1.5 for s in
+                          [(ns, hq, d), (ns, hkv, d), (ns, hkv, d), (n, hkv, d), (n, hkv, d)])
+    a_b, A_b = brute.scores(Qs.tolist(), Kp.tolist(), c, G)
+    a, _ = O.token_scores(Qs, Kp, G)
+    np.testing.assert_allclose(a, a_b, rtol=1e-12)
+    np.testing.assert_allclose(O.chunk_scores(a, c), A_b, rtol=1e-12)
+    m = O.chunk_count(n, c)
+    k = int(g.integers(1, m + 1))
+    if m <= 16:
+        assert O.select_topk(A_b, k).tolist() == brute.best_subset(A_b, k)
+    sel = O.select_topk(A_b, k)
+    toks = O.kept_token_index(sel, n, c)
+    Ob = brute.attend(Qs.tolist(), Ks.tolist(), Vs.tolist(), Kp.tolist(), Vp.tolist(), toks.tolist(), G)
+    np.testing.assert_allclose(O.attention(Qs, Ks, Vs, Kp, Vp, toks, G)[0], Ob, atol=1e-12)
+
+
+# ------------------------------------------------------------ cache model
+def test_cache_touch_worked_examples(golden):
+    for e in golden["cache_touch"]:
+        cm = O.CacheModel(1, 4, 2)
+        for t in e["touches"]:
+            cm.update(0, [2], np.array([0, 0, t, 0]))
+        assert abs(cm.I[0, 2] - e["I"]) < 1e-15 and cm.F[0, 2] == e["F"]
+        assert abs(cm.score(0)[2] - e["S"]) < 1e-15
+
+
+def test_cache_heap_law_persistence_and_delta():
+    g = np.random.default_rng(3)
+    m, P, k = 40, 12, 5
+    cm = O.CacheModel(1, m, P)
+    seen_I = {}
+    for req in range(30):
+        A = g.integers(1, 10, m).astype(float)
+        ids = O.select_topk(A + g.random(m) * 0, k) if req % 3 else g.choice(m, k, replace=False)
+        resident_before = {int(j) for j in cm.owner[0] if j >= 0}
+        S_before = cm.score(0).copy()
+        hits, loads, victims = cm.plan(0, ids)
+        # delta law: loads are exactly the requested ids not resident
+        assert sorted(j for j, _ in loads) == sorted(set(int(j) for j in ids) - resident_before)
+        assert sorted(hits) == sorted(set(int(j) for j in ids) & resident_before)
+        # heap law: victims are the lowest-S evictable residents, in non-decreasing S
+        vs = [S_before[j] for j in victims]
+        assert vs == sorted(vs)
+        evictable = resident_before - set(int(j) for j in ids)
+        if victims:
+            assert max(vs) <= min(S_before[j] for j in evictable - set(victims)) if evictable - set(victims) else True
+        # capacity
+        assert (cm.owner[0] >= 0).sum() <= P
+        for j in victims:  # persistence: (I, F) survive eviction
+            seen_I[j] = (cm.I[0, j], cm.F[0, j])
+        cm.update(0, ids, A)
+    for j, (I, F) in seen_I.items():
+        assert cm.I[0, j] >= I and cm.F[0, j] >= F
+
+
+# ------------------------------------------------------------ synthetic inputs
+def test_synth_bf16_rounding_matches_torch():
+    x = np.random.default_rng(0).standard_normal(10000).astype(np.float32) * 7
+    ref = torch.tensor(x).to(torch.bfloat16).to(torch.float32).numpy()
+    np.testing.assert_array_equal(bf16_round(x), ref)
+
+
+def test_synth_deterministic_and_shaped():
+    cfg = CONFIGS["c1_0.5b"]
+    k1, v1 = make_prefix(cfg, 0)
+    k2, v2 = make_prefix(cfg, 0)
+    np.testing.assert_array_equal(k1, k2)
+    assert k1.shape == (2048, 2, 64) and v1.dtype == np.float32
+    q, ks, vs = make_request(cfg, 0, request=3)
+    assert q.shape == (32, 14, 64) and ks.shape == (32, 2, 64)
+    q2, _, _ = make_request(cfg, 0, request=4)
+    assert not np.array_equal(q, q2)
