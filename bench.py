@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Re-Prefill hot-path benchmark (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ckv|reference]
+
+Workload (config.workload): Qwen2.5-7B shape, 28 layers, 28 Q / 4 KV heads, d = 128,
+32K-token prefix, chunk 16, 128-token suffix, 10% budget (k = 204), bf16, inter-layer
+speculative prefetch on (quota k), HBM chunk cache of 2k + quota slots per layer,
+R = 4 distinct requests cycling over the shared prefix (synthetic, seed 42).
+A step = one request's Re-Prefill over all 28 layers (A1-A9 each layer).
+value = effective KV GB/s = (probe-K + kept K+V + suffix K+V bytes per layer) x layers
+        / step time; us_per_layer is reported beside it.
+Inputs larger than L2: each step streams 28 x 33.5 MB of probe keys (0.94 GB > 126 MB L2).
+N > 1: the prefix is sharded by position across ranks (strong scaling, NCCL exchanges).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CFG_NAME = "c3_7b"
+N_REQUESTS = 4
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def bytes_per_layer(cfg, k):
+    e = 2 if cfg.dtype == "bf16" else 4
+    probe = cfg.prefix_len * cfg.num_kv_heads * cfg.head_dim * e
+    kept = k * 2 * cfg.num_kv_heads * cfg.chunk_size * cfg.head_dim * e
+    suffix = 2 * cfg.suffix_len * cfg.num_kv_heads * cfg.head_dim * e
+    return probe + kept + suffix
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_layer_seconds(cfg, k, layer=0, request=0):
+    import oracle as O
+    from synth import make_prefix, make_request
+    kp, vp = make_prefix(cfg, layer)
+    qs, ks, vs = make_request(cfg, layer, request)
+    t = time.perf_counter()
+    O.reprefill_layer(qs, ks, vs, kp, vp, cfg.chunk_size, k, cfg.group)
+    return time.perf_counter() - t
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle on the host cores, each step one layer of the workload."""
+    from synth import CONFIGS
+    import oracle as O
+    if rank != 0:
+        return
+    cfg = CONFIGS[CFG_NAME]
+    k = O.budget_chunks(cfg.prefix_len, cfg.chunk_size, cfg.budget_bp)
+    for w in range(args.warmup):
+        oracle_layer_seconds(cfg, k, layer=w % cfg.num_layers)
+    ts = [oracle_layer_seconds(cfg, k, layer=s % cfg.num_layers) for s in range(args.steps)]
+    t = sum(ts) / len(ts)
+    bpl = bytes_per_layer(cfg, k)
+    value = bpl / t / 1e9
+    cores = cpu_cores()
+    line = {
+        "impl": "reference", "metric": "Re-Prefill effective KV GB/s (Qwen2.5-7B shape, 32K prefix)",
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "us_per_layer": t * 1e6, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seed 42)",
+        "config": {"workload": CFG_NAME, "step": "one layer (oracle, fp64 NumPy)", "prefix_len": cfg.prefix_len,
+                   "chunk": cfg.chunk_size, "suffix": cfg.suffix_len, "budget_chunks": k},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} single layers of {CFG_NAME}"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ckv(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_13631_b200 as ckv
+    from paper_2601_13631_b200.sharded import ShardedReprefill
+    from synth import CONFIGS, make_prefix, make_request
+
+    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[CFG_NAME]
+    k = ckv.ckv_budget_chunks(cfg.prefix_len, cfg.chunk_size, cfg.budget_bp)
+    quota = k if args.prefetch else 0
+    ctx = ckv.Context(cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.chunk_size,
+                      cfg.prefix_len, cfg.suffix_len, dtype=cfg.dtype, budget_bp=cfg.budget_bp,
+                      prefetch_chunks=quota, device=local_rank, shard_index=rank, num_shards=world)
+    dt = ctx.torch_dtype
+    for l in range(cfg.num_layers):
+        kp, vp = make_prefix(cfg, l)
+        ctx.store_prefix(l, torch.from_numpy(kp).to(dev, dt), torch.from_numpy(vp).to(dev, dt))
+    reqs_host = []
+    for r in range(N_REQUESTS):
+        per = []
+        for l in range(cfg.num_layers):
+            per.append([torch.from_numpy(x).to(dt).pin_memory() for x in make_request(cfg, l, r)])
+        reqs_host.append(per)
+    reqs = [[[t.to(dev) for t in lay] for lay in per] for per in reqs_host]
+    L = cfg.num_layers
+    outs = [torch.empty(cfg.suffix_len, cfg.num_q_heads, cfg.head_dim, dtype=dt, device=dev) for _ in range(L)]
+    ids = [torch.empty(k, dtype=torch.int32, device=dev) for _ in range(L)]
+    runner = ShardedReprefill(ctx) if world > 1 else None
+
+    def layer_call(l, q, ks, vs):
+        if runner is None:
+            ctx.reprefill_layer(l, q, ks, vs, out=outs[l], ids=ids[l])
+        else:
+            runner.reprefill_layer(l, q, ks, vs, out=outs[l], ids=ids[l])
+
+    def step(i):
+        per = reqs[i % N_REQUESTS]
+        for l in range(L):
+            layer_call(l, *per[l])
+
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, K):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(K):
+            fn(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    ctx.reset_stats()
+    launches0 = ctx.kernel_launches
+    with ClockSampler(local_rank) as clk:
+        ms = timed(step, args.steps)
+    launches = ctx.kernel_launches - launches0
+    stats = ctx.get_stats()
+    ms_step = ms / args.steps
+    bpl = bytes_per_layer(cfg, k)
+    value = bpl * L / (ms_step * 1e-3) / 1e9
+
+    # stage profile pass (CUDA events on the launching stream, inside the library)
+    ctx.profile(True)
+    ms_prof = timed(step, args.steps)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+
+    # end-to-end through the public API with host buffers: H2D of the step's inputs from
+    # pinned memory and D2H of its outputs inside the timed region
+    host_out = [torch.empty(outs[0].shape, dtype=dt).pin_memory() for _ in range(L)]
+    host_ids = [torch.empty(k, dtype=torch.int32).pin_memory() for _ in range(L)]
+    dev_in = [[torch.empty_like(t) for t in lay] for lay in reqs[0]]
+
+    def e2e_step(i):
+        per = reqs_host[i % N_REQUESTS]
+        for l in range(L):
+            for dst, src in zip(dev_in[l], per[l]):
+                dst.copy_(src, non_blocking=True)
+            layer_call(l, *dev_in[l])
+            host_out[l].copy_(outs[l], non_blocking=True)
+            host_ids[l].copy_(ids[l], non_blocking=True)
+
+    ms_e2e = timed(e2e_step, args.steps) / args.steps
+    h2d = sum(t.numel() * t.element_size() for lay in reqs_host[0] for t in lay)
+    d2h = L * (outs[0].numel() * outs[0].element_size() + k * 4)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = load_peaks()
+    score_ms, score_n = prof["score"]
+    score_avg = score_ms / max(score_n, 1)
+    flops = 2.0 * cfg.head_dim * cfg.num_q_heads * cfg.suffix_len * (cfg.prefix_len / world)
+    achieved = flops / (score_avg * 1e-3) / 1e12
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "score_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        traffic = tj.get("kind%d" % ctx.score_kernel_kind)
+    step_stage_ms = {n: v[0] / args.steps for n, v in prof.items()}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        t = oracle_layer_seconds(cfg, k)
+        cpu = {"value": bpl / t / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"1 layer (layer 0, request 0) of {CFG_NAME}, fp64 NumPy, {t:.2f} s"}
+    n_lay = max(stats["total_layers"], 1)
+    line = {
+        "metric": "Re-Prefill effective KV GB/s (Qwen2.5-7B shape, 32K prefix)",
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3 / L,
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seed 42, SURVEY §8(d) recipe)",
+        "config": {"workload": CFG_NAME, "layers": L, "prefix_len": cfg.prefix_len, "chunk": cfg.chunk_size,
+                   "suffix": cfg.suffix_len, "heads": f"{cfg.num_q_heads}/{cfg.num_kv_heads}",
+                   "head_dim": cfg.head_dim, "budget_chunks": k, "prefetch_quota": quota,
+                   "requests": N_REQUESTS, "parallelism": f"prefix-shard{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (0.94 GB of probe keys streamed per step)",
+                   "bytes_per_layer": bpl},
+        "roofline": {"kernel": "score_partial (A1)", "bound": "tensor", "achieved": achieved, "peak": peak,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": f"{peak_src} bf16_tflops_sustained", "score_kernel_kind":
+                         ["simt", "tcgen05"][ctx.score_kernel_kind], "avg_launch_ms": score_avg,
+                     "hbm_achieved_gbs": (cfg.prefix_len / world) * cfg.num_kv_heads * cfg.head_dim * 2
+                     / (score_avg * 1e-3) / 1e9},
+        "stage_ms_per_step": step_stage_ms, "profiled_ms_per_step": ms_prof / args.steps,
+        "cache": {"hit_rate": stats["total_hits"] / max(stats["total_hits"] + stats["total_misses"], 1),
+                  "misses_per_layer": stats["total_misses"] / n_lay,
+                  "spec_loads_per_layer": stats["total_spec_loads"] / n_lay,
+                  "spec_used_per_layer": stats["total_spec_used"] / n_lay,
+                  "link_bytes_per_layer": (stats["total_link_bytes_delta"] + stats["total_link_bytes_spec"]) / n_lay},
+        "e2e": {"value": bpl * L / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+        "context": "paper: 3.85x average Re-Prefill (TTFT) speedup over IMPRESS on 1x A800 + PCIe4 + NVMe "
+                   "(PAPER.md:29, 582) -- context only, not comparable",
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ckv", choices=["ckv", "reference"])
+    ap.add_argument("--no-prefetch", dest="prefetch", action="store_false")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ckv" else args.warmup
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ckv(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,734 @@
+// C-ABI and per-layer engine of libckv (include/ckv.h).
+//
+// Orchestrates, per layer, on the caller's stream S and one library-owned side stream P:
+//   S: A1 score -> A2 reduce -> A3 top-k -> [wait P's prefetch plan] A4 plan -> A5 delta
+//      gather -> [wait P's prefetch data] A7 attention -> A8 combine -> A9 update
+//   P: (after A3 of layer l) A4 plan of layer l+1 for ids_l (speculative, quota) -> A5
+//      gather  (inter-period speculative prefetch at p = 1)
+// No host synchronisation on the per-layer path: ids stay on the device, and the gather
+// reads the mapped pinned host store directly (device-initiated zero-copy).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ckv.h"
+#include "common.cuh"
+
+using namespace ckv;
+
+struct ckv_ctx {
+  ckv_config cfg{};
+  int L = 0, Hq = 0, Hkv = 0, G = 0, d = 0, c = 0, esz = 0, dtype = 0, fullrow = 0;
+  int64_t n = 0;
+  int m = 0;
+  int W = 1, shard = 0, j0 = 0, j1 = 0, m_loc = 0;
+  int64_t t0 = 0;
+  int n_loc = 0, n_pad = 0;
+  int k = 0, P = 0, quota = 0, max_ns = 0;
+  int64_t rec_elems = 0, rec_bytes = 0;
+  int nsplit_score_max = 1, nsplit_attn_max = 1;
+  int score_kind = 0;  // 0 SIMT, 1 tcgen05
+
+  void* probe = nullptr;
+  char* host_store = nullptr;
+  char* host_store_dev = nullptr;
+  char* pool = nullptr;
+  int32_t *slot_of = nullptr, *owner = nullptr, *pf_epoch = nullptr, *F = nullptr;
+  float* I = nullptr;
+  float *lam2 = nullptr, *lampart = nullptr, *Lam2 = nullptr, *A = nullptr;
+  int32_t* ids_buf[2] = {nullptr, nullptr};
+  int32_t* n_ids_buf[2] = {nullptr, nullptr};
+  int32_t *kept_slots = nullptr, *ids_glob = nullptr, *flag = nullptr;
+  int32_t *scratch_main = nullptr, *scratch_side = nullptr;
+  int32_t *gl_main = nullptr, *gl_side = nullptr, *nload_main = nullptr, *nload_side = nullptr;
+  int32_t* counts = nullptr;  // [L][2][4]
+  float *o_part = nullptr, *lse_part = nullptr;
+  int64_t* stats = nullptr;  // [16]
+  void* tmap_cache = nullptr;
+
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_ids = nullptr;
+  std::vector<cudaEvent_t> ev_pplan, ev_pf;
+  std::vector<int> pf_issued;
+  std::vector<char> stored;
+  int epoch = 0;
+  int last_layer = -1;
+  int64_t launches = 0;
+  // stage profiling (CUDA events on the launching stream; off by default)
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_marks;
+  size_t prof_used = 0;
+  cudaEvent_t prof_open[8] = {};
+  std::string err;
+};
+
+namespace {
+
+ckv_status fail(ckv_ctx* ctx, ckv_status s, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return s;
+}
+
+#define CK(expr)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (expr);                                                                         \
+    if (e_ != cudaSuccess) return fail(ctx, CKV_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                          \
+  } while (0)
+
+#define LK(expr)   \
+  do {             \
+    CK(expr);      \
+    ++ctx->launches; \
+  } while (0)
+
+cudaEvent_t prof_event(ckv_ctx* ctx) {
+  if (ctx->prof_used == ctx->prof_pool.size()) {
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    ctx->prof_pool.push_back(e);
+  }
+  return ctx->prof_pool[ctx->prof_used++];
+}
+void prof_begin(ckv_ctx* ctx, int stage, cudaStream_t st) {
+  if (!ctx->prof_on) return;
+  cudaEvent_t e = prof_event(ctx);
+  cudaEventRecord(e, st);
+  ctx->prof_open[stage] = e;
+}
+void prof_end(ckv_ctx* ctx, int stage, cudaStream_t st) {
+  if (!ctx->prof_on || !ctx->prof_open[stage]) return;
+  cudaEvent_t e = prof_event(ctx);
+  cudaEventRecord(e, st);
+  ctx->prof_marks.push_back({stage, {ctx->prof_open[stage], e}});
+  ctx->prof_open[stage] = nullptr;
+}
+#define PROF_BEGIN(s) prof_begin(ctx, (s), st)
+#define PROF_END(s) prof_end(ctx, (s), st)
+
+template <typename Tp>
+cudaError_t dalloc(Tp** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(Tp) + 16);
+}
+
+LayerGeom geom(const ckv_ctx* ctx, int ns) {
+  LayerGeom g;
+  g.Hq = ctx->Hq;
+  g.Hkv = ctx->Hkv;
+  g.G = ctx->G;
+  g.d = ctx->d;
+  g.c = ctx->c;
+  g.ns = ns;
+  g.R = ctx->G * ns;
+  g.m_loc = ctx->m_loc;
+  g.n_loc = ctx->n_loc;
+  g.n_pad = ctx->n_pad;
+  return g;
+}
+
+int simt_score_nsplit(const ckv_ctx* ctx, int ns) {
+  const int rowblocks = (ctx->G * ns + 63) / 64;
+  int s = (4 * 296 + rowblocks * ctx->Hkv - 1) / (rowblocks * ctx->Hkv);
+  s = s < 1 ? 1 : s;
+  return s > ctx->m_loc ? ctx->m_loc : s;
+}
+
+int attn_nsplit(const ckv_ctx* ctx, int ns, int n_kept_cap) {
+  const int rowblocks = (ctx->G * ns + 63) / 64;
+  int s = (2 * 296 + rowblocks * ctx->Hkv - 1) / (rowblocks * ctx->Hkv);
+  int maxs = n_kept_cap < 1 ? 1 : n_kept_cap;
+  s = s < 1 ? 1 : s;
+  s = s > maxs ? maxs : s;
+  return s > ctx->nsplit_attn_max ? ctx->nsplit_attn_max : s;
+}
+
+CacheLayer cache_layer(const ckv_ctx* ctx, int layer) {
+  CacheLayer cl;
+  cl.slot_of = ctx->slot_of + (size_t)layer * ctx->m_loc;
+  cl.owner = ctx->owner + (size_t)layer * ctx->P;
+  cl.pf_epoch = ctx->pf_epoch + (size_t)layer * ctx->P;
+  cl.I = ctx->I + (size_t)layer * ctx->m_loc;
+  cl.F = ctx->F + (size_t)layer * ctx->m_loc;
+  cl.m_loc = ctx->m_loc;
+  cl.P = ctx->P;
+  return cl;
+}
+
+const char* host_layer_dev(const ckv_ctx* ctx, int layer) {
+  return ctx->host_store_dev + (size_t)layer * ctx->m_loc * ctx->rec_bytes;
+}
+char* pool_layer(const ckv_ctx* ctx, int layer) { return ctx->pool + (size_t)layer * ctx->P * ctx->rec_bytes; }
+const void* probe_layer(const ckv_ctx* ctx, int layer) {
+  return static_cast<const char*>(ctx->probe) + (size_t)layer * ctx->Hkv * ctx->n_pad * ctx->d * ctx->esz;
+}
+
+// A1 (+ local part of A2): lam2, lampart, and Lam2 or the shard-local row LSE
+ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int ns, float* lam_local_out,
+                     int* nsplit_out, cudaStream_t st) {
+  LayerGeom g = geom(ctx, ns);
+  int nsplit = 0;
+  cudaError_t e = cudaErrorNotSupported;
+  PROF_BEGIN(0);
+  if (ctx->score_kind == 1) {
+    nsplit = score_tc_nsplit(g);
+    e = launch_score_tc(g, static_cast<const __nv_bfloat16*>(q),
+                        static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)), ctx->lam2, ctx->lampart, nsplit,
+                        ctx->tmap_cache, st);
+  }
+  if (e == cudaErrorNotSupported) {
+    nsplit = simt_score_nsplit(ctx, ns);
+    if (ctx->dtype == CKV_FP32)
+      e = launch_score_simt<float>(g, static_cast<const float*>(q), static_cast<const float*>(probe_layer(ctx, layer)),
+                                   ctx->lam2, ctx->lampart, nsplit, st);
+    else
+      e = launch_score_simt<__nv_bfloat16>(g, static_cast<const __nv_bfloat16*>(q),
+                                           static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)), ctx->lam2,
+                                           ctx->lampart, nsplit, st);
+  }
+  PROF_END(0);
+  CK(e);
+  ++ctx->launches;
+  *nsplit_out = nsplit;
+  // local row normaliser (-> Lam2 for W == 1, or the shard's lam_local)
+  PROF_BEGIN(1);
+  if (ctx->dtype == CKV_FP32)
+    LK(launch_row_lse<float>(g, ctx->lampart, nsplit, static_cast<const float*>(q), static_cast<const float*>(ks),
+                             lam_local_out ? 0 : ctx->fullrow, nullptr, 1, ctx->Lam2, lam_local_out, st));
+  else
+    LK(launch_row_lse<__nv_bfloat16>(g, ctx->lampart, nsplit, static_cast<const __nv_bfloat16*>(q),
+                                     static_cast<const __nv_bfloat16*>(ks), lam_local_out ? 0 : ctx->fullrow, nullptr,
+                                     1, ctx->Lam2, lam_local_out, st));
+  PROF_END(1);
+  return CKV_OK;
+}
+
+// A6: speculative plan + gather of layer `layer` for the given ids, on the side stream.
+ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, cudaStream_t st) {
+  if (ctx->quota <= 0 || layer >= ctx->L) return CKV_OK;
+  CK(cudaEventRecord(ctx->ev_ids, st));
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ids, 0));
+  PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)(layer * 2 + 1) * 4, ctx->stats};
+  LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 1, ctx->quota, ctx->epoch, ctx->rec_bytes, nullptr,
+                       ctx->scratch_side, po, ctx->side));
+  CK(cudaEventRecord(ctx->ev_pplan[layer], ctx->side));
+  LK(launch_gather(ctx->gl_side, ctx->nload_side, host_layer_dev(ctx, layer), pool_layer(ctx, layer), ctx->rec_bytes,
+                   ctx->side));
+  CK(cudaEventRecord(ctx->ev_pf[layer], ctx->side));
+  ctx->pf_issued[layer] = ctx->epoch;
+  return CKV_OK;
+}
+
+// A4 -> A5 -> A7 -> A8 -> A9 for the local selected ids.
+ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, const void* q,
+                      const void* ks, const void* vs, int ns, int include_suffix, void* out, float* o_f32,
+                      float* lse_nat, cudaStream_t st) {
+  const bool pf = ctx->pf_issued[layer] == ctx->epoch;
+  if (pf) CK(cudaStreamWaitEvent(st, ctx->ev_pplan[layer], 0));
+  PlanOut po{ctx->gl_main, ctx->nload_main, ctx->kept_slots, nullptr, ctx->counts + (size_t)(layer * 2) * 4,
+             ctx->stats};
+  PROF_BEGIN(3);
+  LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 0, 0, ctx->epoch, ctx->rec_bytes, nullptr,
+                       ctx->scratch_main, po, st));
+  PROF_END(3);
+  PROF_BEGIN(4);
+  LK(launch_gather(ctx->gl_main, ctx->nload_main, host_layer_dev(ctx, layer), pool_layer(ctx, layer), ctx->rec_bytes,
+                   st));
+  PROF_END(4);
+  if (pf) CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
+  LayerGeom g = geom(ctx, ns);
+  const int nsplit = attn_nsplit(ctx, ns, ctx->k);
+  PROF_BEGIN(5);
+  if (ctx->dtype == CKV_FP32) {
+    LK(launch_attn_simt<float>(g, static_cast<const float*>(q), static_cast<const float*>(ks),
+                               static_cast<const float*>(vs), reinterpret_cast<const float*>(pool_layer(ctx, layer)),
+                               ctx->rec_elems, ctx->kept_slots, ids, n_ids_dev, ctx->k, include_suffix, nsplit,
+                               ctx->o_part, ctx->lse_part, st));
+    LK(launch_attn_combine<float>(g, ctx->o_part, ctx->lse_part, nsplit, static_cast<float*>(out), o_f32, lse_nat,
+                                  st));
+  } else {
+    LK(launch_attn_simt<__nv_bfloat16>(g, static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(ks),
+                                       static_cast<const __nv_bfloat16*>(vs),
+                                       reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->rec_elems,
+                                       ctx->kept_slots, ids, n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part,
+                                       ctx->lse_part, st));
+    LK(launch_attn_combine<__nv_bfloat16>(g, ctx->o_part, ctx->lse_part, nsplit, static_cast<__nv_bfloat16*>(out),
+                                          o_f32, lse_nat, st));
+  }
+  PROF_END(5);
+  PROF_BEGIN(7);
+  LK(launch_cache_update(cache_layer(ctx, layer), ids, n_ids_dev, ctx->A, st));
+  PROF_END(7);
+  ctx->last_layer = layer;
+  return CKV_OK;
+}
+
+ckv_status check_layer_call(ckv_ctx* ctx, int layer, int ns) {
+  if (!ctx) return CKV_EINVAL;
+  if (layer < 0 || layer >= ctx->L) return fail(ctx, CKV_EINVAL, "layer %d out of range [0, %d)", layer, ctx->L);
+  if (ns < 1 || ns > ctx->max_ns) return fail(ctx, CKV_EINVAL, "n_suffix %d out of range [1, %d]", ns, ctx->max_ns);
+  if (!ctx->stored[layer]) return fail(ctx, CKV_ESTATE, "layer %d prefix not stored", layer);
+  return CKV_OK;
+}
+
+void free_all(ckv_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->cfg.device);
+  cudaDeviceSynchronize();
+  void* dev_ptrs[] = {ctx->probe, ctx->pool, ctx->slot_of, ctx->owner, ctx->pf_epoch, ctx->F, ctx->I, ctx->lam2,
+                      ctx->lampart, ctx->Lam2, ctx->A, ctx->ids_buf[0], ctx->ids_buf[1], ctx->n_ids_buf[0],
+                      ctx->n_ids_buf[1], ctx->kept_slots, ctx->ids_glob, ctx->flag, ctx->scratch_main,
+                      ctx->scratch_side, ctx->gl_main, ctx->gl_side, ctx->nload_main, ctx->nload_side, ctx->counts,
+                      ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache};
+  for (void* p : dev_ptrs)
+    if (p) cudaFree(p);
+  if (ctx->host_store) cudaFreeHost(ctx->host_store);
+  for (auto e : ctx->ev_pplan)
+    if (e) cudaEventDestroy(e);
+  for (auto e : ctx->ev_pf)
+    if (e) cudaEventDestroy(e);
+  if (ctx->ev_ids) cudaEventDestroy(ctx->ev_ids);
+  for (auto e : ctx->prof_pool)
+    if (e) cudaEventDestroy(e);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ckv_budget_chunks(int64_t n, int32_t c, int32_t budget_bp) {
+  if (n < 1 || c < 1 || budget_bp < 1 || budget_bp > 10000) return -1;
+  const int64_t m = (n + c - 1) / c;
+  int64_t k = ((int64_t)budget_bp * n) / ((int64_t)10000 * c);
+  if (k > m) k = m;
+  if (k < 1) k = 1;
+  return (int32_t)k;
+}
+
+ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
+  if (!cfg || !out) return CKV_EINVAL;
+  *out = nullptr;
+  ckv_ctx* ctx = new (std::nothrow) ckv_ctx();
+  if (!ctx) return CKV_ENOMEM;
+  ctx->cfg = *cfg;
+  const ckv_config& c = *cfg;
+  auto bad = [&](const char* msg) {
+    fprintf(stderr, "ckv_create: %s\n", msg);
+    delete ctx;
+    return CKV_EINVAL;
+  };
+  if (c.num_layers < 1 || c.num_q_heads < 1 || c.num_kv_heads < 1 || c.head_dim < 1) return bad("dims must be >= 1");
+  if (c.num_q_heads % c.num_kv_heads) return bad("num_q_heads % num_kv_heads != 0");
+  if (c.head_dim % 16 || c.head_dim > 128) return (delete ctx, CKV_EUNSUPPORTED);
+  if (c.dtype != CKV_BF16 && c.dtype != CKV_FP32) return bad("dtype");
+  if (c.chunk_size < 1 || c.prefix_len < 1 || c.max_suffix_len < 1) return bad("chunk_size/prefix_len/max_suffix_len");
+  if (c.num_shards < 1 || c.shard_index < 0 || c.shard_index >= c.num_shards) return bad("shard_index/num_shards");
+  if (c.score_norm != CKV_NORM_PREFIX && c.score_norm != CKV_NORM_FULLROW) return bad("score_norm");
+  ctx->L = c.num_layers;
+  ctx->Hq = c.num_q_heads;
+  ctx->Hkv = c.num_kv_heads;
+  ctx->G = c.num_q_heads / c.num_kv_heads;
+  ctx->d = c.head_dim;
+  ctx->c = c.chunk_size;
+  ctx->dtype = c.dtype;
+  ctx->esz = c.dtype == CKV_BF16 ? 2 : 4;
+  ctx->fullrow = c.score_norm == CKV_NORM_FULLROW;
+  ctx->n = c.prefix_len;
+  ctx->m = (int)((c.prefix_len + c.chunk_size - 1) / c.chunk_size);
+  ctx->W = c.num_shards;
+  ctx->shard = c.shard_index;
+  const int per = (ctx->m + ctx->W - 1) / ctx->W;
+  ctx->j0 = ctx->shard * per < ctx->m ? ctx->shard * per : ctx->m;
+  ctx->j1 = (ctx->shard + 1) * per < ctx->m ? (ctx->shard + 1) * per : ctx->m;
+  ctx->m_loc = ctx->j1 - ctx->j0;
+  ctx->t0 = (int64_t)ctx->j0 * ctx->c;
+  int64_t t1 = (int64_t)ctx->j1 * ctx->c < ctx->n ? (int64_t)ctx->j1 * ctx->c : ctx->n;
+  ctx->n_loc = (int)(t1 - ctx->t0);
+  ctx->n_pad = ((ctx->n_loc + 255) / 256 + 1) * 256;
+  if (ctx->m_loc < 1) return bad("shard owns no chunk (num_shards > m)");
+  ctx->k = c.budget_chunks > 0 ? c.budget_chunks : ckv_budget_chunks(c.prefix_len, c.chunk_size, c.budget_bp);
+  if (ctx->k < 1 || ctx->k > ctx->m) return bad("budget: k must be in [1, m]");
+  ctx->quota = c.prefetch_chunks < 0 ? 0 : (c.prefetch_chunks > ctx->k ? ctx->k : c.prefetch_chunks);
+  ctx->P = c.cache_slots > 0 ? c.cache_slots : 2 * ctx->k + ctx->quota;
+  if (ctx->P < ctx->k + ctx->quota) return bad("cache_slots < k + prefetch_chunks");
+  ctx->max_ns = c.max_suffix_len;
+  ctx->rec_elems = (int64_t)2 * ctx->Hkv * ctx->c * ctx->d;
+  ctx->rec_bytes = ctx->rec_elems * ctx->esz;
+
+  ckv_status st = CKV_OK;
+  auto cudafail = [&](cudaError_t e, const char* what) {
+    fprintf(stderr, "ckv_create: %s: %s\n", what, cudaGetErrorString(e));
+    free_all(ctx);
+    delete ctx;
+    return e == cudaErrorMemoryAllocation ? CKV_ENOMEM : CKV_ECUDA;
+  };
+#define CKC(expr)                                   \
+  do {                                              \
+    cudaError_t e_ = (expr);                        \
+    if (e_ != cudaSuccess) return cudafail(e_, #expr); \
+  } while (0)
+  CKC(cudaSetDevice(c.device));
+  const int R_max = ctx->G * ctx->max_ns;
+  ctx->nsplit_score_max = ctx->m_loc < 4096 ? ctx->m_loc : 4096;
+  ctx->nsplit_attn_max = 64;
+  const size_t probe_elems = (size_t)ctx->L * ctx->Hkv * ctx->n_pad * ctx->d;
+  CKC(cudaMalloc(&ctx->probe, probe_elems * ctx->esz));
+  CKC(cudaMemset(ctx->probe, 0, probe_elems * ctx->esz));
+  CKC(cudaHostAlloc(reinterpret_cast<void**>(&ctx->host_store), (size_t)ctx->L * ctx->m_loc * ctx->rec_bytes,
+                    cudaHostAllocMapped | cudaHostAllocPortable));
+  CKC(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->host_store_dev), ctx->host_store, 0));
+  CKC(cudaMalloc(reinterpret_cast<void**>(&ctx->pool), (size_t)ctx->L * ctx->P * ctx->rec_bytes));
+  CKC(dalloc(&ctx->slot_of, (size_t)ctx->L * ctx->m_loc));
+  CKC(dalloc(&ctx->owner, (size_t)ctx->L * ctx->P));
+  CKC(dalloc(&ctx->pf_epoch, (size_t)ctx->L * ctx->P));
+  CKC(dalloc(&ctx->F, (size_t)ctx->L * ctx->m_loc));
+  CKC(dalloc(&ctx->I, (size_t)ctx->L * ctx->m_loc));
+  CKC(cudaMemset(ctx->slot_of, 0xFF, sizeof(int32_t) * ctx->L * ctx->m_loc));
+  CKC(cudaMemset(ctx->owner, 0xFF, sizeof(int32_t) * ctx->L * ctx->P));
+  CKC(cudaMemset(ctx->pf_epoch, 0xFF, sizeof(int32_t) * ctx->L * ctx->P));
+  CKC(cudaMemset(ctx->F, 0, sizeof(int32_t) * ctx->L * ctx->m_loc));
+  CKC(cudaMemset(ctx->I, 0, sizeof(float) * ctx->L * ctx->m_loc));
+  CKC(dalloc(&ctx->lam2, (size_t)ctx->Hkv * ctx->m_loc * R_max));
+  CKC(dalloc(&ctx->lampart, (size_t)ctx->Hkv * ctx->nsplit_score_max * R_max));
+  CKC(dalloc(&ctx->Lam2, (size_t)ctx->Hkv * R_max));
+  CKC(dalloc(&ctx->A, (size_t)ctx->m_loc));
+  for (int i = 0; i < 2; ++i) {
+    CKC(dalloc(&ctx->ids_buf[i], (size_t)ctx->k));
+    CKC(dalloc(&ctx->n_ids_buf[i], 1));
+  }
+  CKC(dalloc(&ctx->kept_slots, (size_t)ctx->k));
+  CKC(dalloc(&ctx->ids_glob, (size_t)ctx->k));
+  CKC(dalloc(&ctx->flag, (size_t)ctx->m));
+  CKC(dalloc(&ctx->scratch_main, (size_t)ctx->k + 2 * ctx->P));
+  CKC(dalloc(&ctx->scratch_side, (size_t)ctx->k + 2 * ctx->P));
+  CKC(dalloc(&ctx->gl_main, (size_t)2 * ctx->k));
+  CKC(dalloc(&ctx->gl_side, (size_t)2 * ctx->k));
+  CKC(dalloc(&ctx->nload_main, 1));
+  CKC(dalloc(&ctx->nload_side, 1));
+  CKC(dalloc(&ctx->counts, (size_t)ctx->L * 8));
+  CKC(cudaMemset(ctx->counts, 0, sizeof(int32_t) * ctx->L * 8));
+  CKC(dalloc(&ctx->o_part, (size_t)ctx->nsplit_attn_max * ctx->Hkv * R_max * ctx->d));
+  CKC(dalloc(&ctx->lse_part, (size_t)ctx->nsplit_attn_max * ctx->Hkv * R_max));
+  CKC(dalloc(&ctx->stats, 16));
+  CKC(cudaMemset(ctx->stats, 0, sizeof(int64_t) * 16));
+  int lo = 0, hi = 0;
+  CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CKC(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi));
+  CKC(cudaEventCreateWithFlags(&ctx->ev_ids, cudaEventDisableTiming));
+  ctx->ev_pplan.assign(ctx->L, nullptr);
+  ctx->ev_pf.assign(ctx->L, nullptr);
+  for (int l = 0; l < ctx->L; ++l) {
+    CKC(cudaEventCreateWithFlags(&ctx->ev_pplan[l], cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_pf[l], cudaEventDisableTiming));
+  }
+  ctx->pf_issued.assign(ctx->L, -1);
+  ctx->stored.assign(ctx->L, 0);
+  ctx->score_kind = (ctx->dtype == CKV_BF16 && ctx->d == 128 && !(c.flags & CKV_FLAG_SIMT_SCORE)) ? 1 : 0;
+  if (ctx->score_kind == 1) {
+    LayerGeom g = geom(ctx, ctx->max_ns);
+    if (score_tc_nsplit(g) <= 0) ctx->score_kind = 0;
+  }
+  if (ctx->score_kind == 1) CKC(cudaMalloc(&ctx->tmap_cache, 4096));
+  CKC(cudaDeviceSynchronize());
+#undef CKC
+  (void)st;
+  *out = ctx;
+  return CKV_OK;
+}
+
+ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const void* v, int64_t n_tokens,
+                            void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!k || !v) return fail(ctx, CKV_EINVAL, "null k/v");
+  if (layer < 0 || layer >= ctx->L) return fail(ctx, CKV_EINVAL, "layer %d out of range", layer);
+  if (n_tokens != ctx->n) return fail(ctx, CKV_EINVAL, "n_tokens %lld != prefix_len %lld", (long long)n_tokens,
+                                      (long long)ctx->n);
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t bytes = (size_t)ctx->n * ctx->Hkv * ctx->d * ctx->esz;
+  auto is_dev = [](const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+  };
+  void *kd = const_cast<void*>(k), *vd = const_cast<void*>(v), *tmp = nullptr, *staging = nullptr;
+  if (!is_dev(k) || !is_dev(v)) {
+    CK(cudaMalloc(&tmp, 2 * bytes));
+    CK(cudaMemcpyAsync(tmp, k, bytes, cudaMemcpyDefault, st));
+    CK(cudaMemcpyAsync(static_cast<char*>(tmp) + bytes, v, bytes, cudaMemcpyDefault, st));
+    kd = tmp;
+    vd = static_cast<char*>(tmp) + bytes;
+  }
+  const size_t stage_bytes = (size_t)ctx->m_loc * ctx->rec_bytes;
+  CK(cudaMalloc(&staging, stage_bytes));
+  void* probe_l = const_cast<void*>(probe_layer(ctx, layer));
+  if (ctx->dtype == CKV_FP32) {
+    LK(launch_pack_probe<float>(static_cast<const float*>(kd), ctx->t0, ctx->n_loc, ctx->n_pad, ctx->Hkv, ctx->d,
+                                static_cast<float*>(probe_l), st));
+    LK(launch_pack_records<float>(static_cast<const float*>(kd), static_cast<const float*>(vd), ctx->t0, ctx->n_loc,
+                                  ctx->m_loc, ctx->c, ctx->Hkv, ctx->d, static_cast<float*>(staging), st));
+  } else {
+    LK(launch_pack_probe<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(kd), ctx->t0, ctx->n_loc, ctx->n_pad,
+                                        ctx->Hkv, ctx->d, static_cast<__nv_bfloat16*>(probe_l), st));
+    LK(launch_pack_records<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(kd), static_cast<const __nv_bfloat16*>(vd),
+                                          ctx->t0, ctx->n_loc, ctx->m_loc, ctx->c, ctx->Hkv, ctx->d,
+                                          static_cast<__nv_bfloat16*>(staging), st));
+  }
+  CK(cudaMemcpyAsync(ctx->host_store + (size_t)layer * stage_bytes, staging, stage_bytes, cudaMemcpyDeviceToHost, st));
+  CacheLayer cl = cache_layer(ctx, layer);
+  CK(cudaMemsetAsync(cl.slot_of, 0xFF, sizeof(int32_t) * ctx->m_loc, st));
+  CK(cudaMemsetAsync(cl.owner, 0xFF, sizeof(int32_t) * ctx->P, st));
+  CK(cudaMemsetAsync(cl.pf_epoch, 0xFF, sizeof(int32_t) * ctx->P, st));
+  CK(cudaMemsetAsync(cl.I, 0, sizeof(float) * ctx->m_loc, st));
+  CK(cudaMemsetAsync(cl.F, 0, sizeof(int32_t) * ctx->m_loc, st));
+  CK(cudaStreamSynchronize(st));
+  CK(cudaFree(staging));
+  if (tmp) CK(cudaFree(tmp));
+  ctx->stored[layer] = 1;
+  return CKV_OK;
+}
+
+ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const void* k_suf, const void* v_suf,
+                               int32_t n_suffix, void* out, int32_t* selected_ids, float* chunk_scores,
+                               void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  ckv_status s = check_layer_call(ctx, layer, n_suffix);
+  if (s != CKV_OK) return s;
+  if (ctx->W != 1) return fail(ctx, CKV_ESTATE, "ckv_reprefill_layer needs num_shards == 1; use ckv_shard_*");
+  if (!q || !k_suf || !v_suf || !out || !selected_ids) return fail(ctx, CKV_EINVAL, "null argument");
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (layer == 0) ++ctx->epoch;
+  int nsplit = 0;
+  if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
+  LayerGeom g = geom(ctx, n_suffix);
+  PROF_BEGIN(2);
+  LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->A, st));
+  PROF_END(2);
+  int32_t* ids = ctx->ids_buf[layer & 1];
+  int32_t* nids = ctx->n_ids_buf[layer & 1];
+  PROF_BEGIN(6);
+  LK(launch_topk_scores(ctx->A, ctx->m_loc, ctx->k, 0, ids, nullptr, 0, nids, st));
+  PROF_END(6);
+  if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st)) != CKV_OK) return s;
+  if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, st)) != CKV_OK)
+    return s;
+  CK(cudaMemcpyAsync(selected_ids, ids, sizeof(int32_t) * ctx->k, cudaMemcpyDeviceToDevice, st));
+  if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
+  return CKV_OK;
+}
+
+ckv_status ckv_shard_score(ckv_ctx* ctx, int32_t layer, const void* q, const void* k_suf, int32_t n_suffix,
+                           float* lam_local, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  ckv_status s = check_layer_call(ctx, layer, n_suffix);
+  if (s != CKV_OK) return s;
+  if (!q || !k_suf || !lam_local) return fail(ctx, CKV_EINVAL, "null argument");
+  CK(cudaSetDevice(ctx->cfg.device));
+  if (layer == 0) ++ctx->epoch;
+  int nsplit = 0;
+  return run_score(ctx, layer, q, k_suf, n_suffix, lam_local, &nsplit, static_cast<cudaStream_t>(stream));
+}
+
+ckv_status ckv_shard_select(ckv_ctx* ctx, int32_t layer, const void* q, const void* k_suf, int32_t n_suffix,
+                            const float* lam_all, uint64_t* cand, float* chunk_scores, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  ckv_status s = check_layer_call(ctx, layer, n_suffix);
+  if (s != CKV_OK) return s;
+  if (!q || !k_suf || !lam_all || !cand) return fail(ctx, CKV_EINVAL, "null argument");
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  LayerGeom g = geom(ctx, n_suffix);
+  // global Lambda = LSE over shards in rank order (+ causal suffix in FULLROW mode)
+  if (ctx->dtype == CKV_FP32)
+    LK(launch_row_lse<float>(g, nullptr, 0, static_cast<const float*>(q), static_cast<const float*>(k_suf),
+                             ctx->fullrow, lam_all, ctx->W, ctx->Lam2, nullptr, st));
+  else
+    LK(launch_row_lse<__nv_bfloat16>(g, nullptr, 0, static_cast<const __nv_bfloat16*>(q),
+                                     static_cast<const __nv_bfloat16*>(k_suf), ctx->fullrow, lam_all, ctx->W,
+                                     ctx->Lam2, nullptr, st));
+  LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->A, st));
+  LK(launch_topk_scores(ctx->A, ctx->m_loc, ctx->k, ctx->j0, nullptr, cand, ctx->k, nullptr, st));
+  if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
+  return CKV_OK;
+}
+
+ckv_status ckv_shard_attend(ckv_ctx* ctx, int32_t layer, const uint64_t* cand_all, const void* q, const void* k_suf,
+                            const void* v_suf, int32_t n_suffix, float* o_part, float* lse_part,
+                            int32_t* selected_ids, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  ckv_status s = check_layer_call(ctx, layer, n_suffix);
+  if (s != CKV_OK) return s;
+  if (!cand_all || !q || !k_suf || !v_suf || !o_part || !lse_part || !selected_ids)
+    return fail(ctx, CKV_EINVAL, "null argument");
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t* ids = ctx->ids_buf[layer & 1];
+  int32_t* nids = ctx->n_ids_buf[layer & 1];
+  LK(launch_topk_merge(cand_all, ctx->W * ctx->k, ctx->k, ctx->m, ctx->j0, ctx->j1, ctx->flag, ctx->ids_glob, ids,
+                       nids, st));
+  if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st)) != CKV_OK) return s;
+  if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, ctx->shard == ctx->W - 1, nullptr, o_part,
+                      lse_part, st)) != CKV_OK)
+    return s;
+  CK(cudaMemcpyAsync(selected_ids, ctx->ids_glob, sizeof(int32_t) * ctx->k, cudaMemcpyDeviceToDevice, st));
+  return CKV_OK;
+}
+
+ckv_status ckv_lse_merge_prepare(ckv_ctx* ctx, const float* o_part, const float* lse_part, const float* lse_max,
+                                 int32_t n_suffix, float* merge_buf, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!o_part || !lse_part || !lse_max || !merge_buf || n_suffix < 1 || n_suffix > ctx->max_ns)
+    return fail(ctx, CKV_EINVAL, "bad argument");
+  LK(launch_lse_merge_prepare(n_suffix * ctx->Hq, ctx->d, o_part, lse_part, lse_max, merge_buf,
+                              static_cast<cudaStream_t>(stream)));
+  return CKV_OK;
+}
+
+ckv_status ckv_lse_merge_finish(ckv_ctx* ctx, const float* merge_buf, int32_t n_suffix, void* out, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!merge_buf || !out || n_suffix < 1 || n_suffix > ctx->max_ns) return fail(ctx, CKV_EINVAL, "bad argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (ctx->dtype == CKV_FP32)
+    LK(launch_lse_merge_finish<float>(n_suffix * ctx->Hq, ctx->d, merge_buf, static_cast<float*>(out), st));
+  else
+    LK(launch_lse_merge_finish<__nv_bfloat16>(n_suffix * ctx->Hq, ctx->d, merge_buf,
+                                              static_cast<__nv_bfloat16*>(out), st));
+  return CKV_OK;
+}
+
+ckv_status ckv_reset_cache(ckv_ctx* ctx, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaMemsetAsync(ctx->slot_of, 0xFF, sizeof(int32_t) * ctx->L * ctx->m_loc, st));
+  CK(cudaMemsetAsync(ctx->owner, 0xFF, sizeof(int32_t) * ctx->L * ctx->P, st));
+  CK(cudaMemsetAsync(ctx->pf_epoch, 0xFF, sizeof(int32_t) * ctx->L * ctx->P, st));
+  return CKV_OK;
+}
+
+ckv_status ckv_get_stats(ckv_ctx* ctx, ckv_stats* out) {
+  if (!ctx || !out) return CKV_EINVAL;
+  ctx->err.clear();
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  int64_t s[16];
+  CK(cudaMemcpy(s, ctx->stats, sizeof s, cudaMemcpyDeviceToHost));
+  memset(out, 0, sizeof *out);
+  out->total_hits = s[0];
+  out->total_misses = s[1];
+  out->total_spec_loads = s[2];
+  out->total_spec_used = s[3];
+  out->total_link_bytes_delta = s[4];
+  out->total_link_bytes_spec = s[5];
+  out->total_layers = s[6];
+  if (ctx->last_layer >= 0) {
+    int32_t cnt[8];
+    CK(cudaMemcpy(cnt, ctx->counts + (size_t)ctx->last_layer * 8, sizeof cnt, cudaMemcpyDeviceToHost));
+    out->last_hits = cnt[0];
+    out->last_misses = cnt[1];
+    out->last_spec_used = cnt[3];
+    out->last_spec_loads = ctx->pf_issued[ctx->last_layer] == ctx->epoch ? cnt[4 + 1] : 0;
+  }
+  return CKV_OK;
+}
+
+ckv_status ckv_reset_stats(ckv_ctx* ctx) {
+  if (!ctx) return CKV_EINVAL;
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemset(ctx->stats, 0, sizeof(int64_t) * 16));
+  return CKV_OK;
+}
+
+ckv_status ckv_profile(ckv_ctx* ctx, int32_t enable) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->prof_on = enable != 0;
+  return CKV_OK;
+}
+
+ckv_status ckv_profile_read(ckv_ctx* ctx, double* ms, int64_t* count) {
+  if (!ctx || !ms || !count) return CKV_EINVAL;
+  ctx->err.clear();
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  for (int i = 0; i < CKV_NUM_STAGES; ++i) {
+    ms[i] = 0.0;
+    count[i] = 0;
+  }
+  for (auto& mk : ctx->prof_marks) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, mk.second.first, mk.second.second));
+    ms[mk.first] += t;
+    count[mk.first] += 1;
+  }
+  ctx->prof_marks.clear();
+  ctx->prof_used = 0;
+  return CKV_OK;
+}
+
+int64_t ckv_kernel_launches(const ckv_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int32_t ckv_num_chunks(const ckv_ctx* ctx) { return ctx ? ctx->m : -1; }
+int32_t ckv_num_local_chunks(const ckv_ctx* ctx) { return ctx ? ctx->m_loc : -1; }
+int32_t ckv_k(const ckv_ctx* ctx) { return ctx ? ctx->k : -1; }
+int32_t ckv_score_kernel_kind(const ckv_ctx* ctx) { return ctx ? ctx->score_kind : -1; }
+
+ckv_status ckv_test_topk(ckv_ctx* ctx, const float* A, int32_t m, int32_t k, int32_t* ids, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!A || !ids || m < 1 || k < 1 || k > m) return fail(ctx, CKV_EINVAL, "bad argument");
+  LK(launch_topk_scores(A, m, k, 0, ids, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream)));
+  return CKV_OK;
+}
+
+ckv_status ckv_test_cache_step(ckv_ctx* ctx, int32_t layer, const int32_t* ids, int32_t k, int32_t prefetch,
+                               const float* A, int32_t* loads, int32_t* victims, int32_t* counts, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (layer < 0 || layer >= ctx->L || !ids || !loads || !counts || k < 1 || k > ctx->k)
+    return fail(ctx, CKV_EINVAL, "bad argument");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  ++ctx->epoch;
+  PlanOut po{loads, ctx->nload_main, prefetch ? nullptr : ctx->kept_slots, victims, counts, nullptr};
+  LK(launch_cache_plan(cache_layer(ctx, layer), ids, nullptr, k, prefetch ? 1 : 0, ctx->quota, ctx->epoch,
+                       ctx->rec_bytes, nullptr, ctx->scratch_main, po, st));
+  if (A && !prefetch) {
+    CK(cudaMemcpyAsync(ctx->n_ids_buf[0], &k, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    LK(launch_cache_update(cache_layer(ctx, layer), ids, ctx->n_ids_buf[0], A, st));
+  }
+  return CKV_OK;
+}
+
+const char* ckv_last_error(const ckv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void ckv_destroy(ckv_ctx* ctx) {
+  if (!ctx) return;
+  free_all(ctx);
+  delete ctx;
+}
+
+}  // extern "C"

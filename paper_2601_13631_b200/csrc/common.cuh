@@ -1,0 +1,110 @@
+// Shared device helpers and launcher declarations of libckv (sm_100a).
+// Product code only: nothing here is shared with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace ckv {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f(float x);
+template <> __device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fast_log2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Geometry of one layer's work as seen by the kernels (local shard view).
+struct LayerGeom {
+  int Hq, Hkv, G, d, c;
+  int ns;          // suffix rows n_s of this call
+  int R;           // rows per KV head = G * ns (row rho = g * ns + r)
+  int m_loc;       // local chunks
+  int n_loc;       // local prefix tokens
+  int n_pad;       // probe-key row stride per KV head
+};
+
+// ---- launchers (defined in the k_*.cu files) ----
+// A1 SIMT: lam2[kvh][m_loc][R] = log2 sum_{i in chunk} 2^(l_i log2e), lampart[kvh][split][R]
+template <typename T>
+cudaError_t launch_score_simt(const LayerGeom& g, const T* q, const T* probe_layer, float* lam2,
+                              float* lampart, int nsplit, cudaStream_t st);
+// A1 tcgen05 (bf16 only, d == 128); returns cudaErrorNotSupported if the shape is outside it
+cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* probe_layer,
+                            float* lam2, float* lampart, int nsplit, void* tmap_cache, cudaStream_t st);
+int score_tc_nsplit(const LayerGeom& g);
+// A2: Lambda2[kvh][R] = LSE2 over splits (+ causal suffix if fullrow) ; also writes row LSE for shards
+template <typename T>
+cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit, const T* q, const T* k_suf,
+                           int fullrow, const float* lam_all, int W, float* Lam2, float* lam_local_out,
+                           cudaStream_t st);
+cudaError_t launch_chunk_sum(const LayerGeom& g, const float* lam2, const float* Lam2, float* A,
+                             cudaStream_t st);
+// A3
+cudaError_t launch_topk_scores(const float* A, int m, int k, int id_offset, int32_t* ids,
+                               uint64_t* cand_out, int n_cand_out, int32_t* n_out, cudaStream_t st);
+cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1,
+                              int32_t* flag_scratch, int32_t* ids_glob, int32_t* ids_local,
+                              int32_t* n_local, cudaStream_t st);
+// A4 / A5 / A9
+struct CacheLayer {
+  int32_t* slot_of;   // [m_loc]
+  int32_t* owner;     // [P]
+  int32_t* pf_epoch;  // [P]
+  float* I;           // [m_loc]
+  int32_t* F;         // [m_loc]
+  int m_loc, P;
+};
+struct PlanOut {
+  int32_t* gather_list;  // [2 * cap]: (chunk, slot)
+  int32_t* n_load;       // [1]
+  int32_t* kept_slots;   // [k] or null (prefetch mode)
+  int32_t* victims;      // [cap] or null
+  int32_t* counts;       // [4]: hits, loads, victims, spec_used  (or null)
+  int64_t* stats;        // device counters or null
+};
+cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
+                              int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t* scratch64,
+                              int32_t* scratch32, PlanOut out, cudaStream_t st);
+cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
+                          char* pool_layer, int64_t rec_bytes, cudaStream_t st);
+cudaError_t launch_cache_update(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev,
+                                const float* A, cudaStream_t st);
+// store
+template <typename T>
+cudaError_t launch_pack_probe(const T* k, int64_t t0, int n_loc, int n_pad, int Hkv, int d, T* probe_layer,
+                              cudaStream_t st);
+template <typename T>
+cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int n_loc, int m_loc, int c, int Hkv,
+                                int d, T* staging, cudaStream_t st);
+// A7 / A8
+template <typename T>
+cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, const T* v_suf,
+                             const T* pool_layer, int64_t rec_elems, const int32_t* kept_slots,
+                             const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap,
+                             int include_suffix, int nsplit, float* o_part, float* lse_part,
+                             cudaStream_t st);
+template <typename T>
+cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit,
+                                T* out, float* o_f32, float* lse_nat, cudaStream_t st);
+cudaError_t launch_lse_merge_prepare(int rows, int d, const float* o, const float* lse, const float* lse_max,
+                                     float* buf, cudaStream_t st);
+template <typename T>
+cudaError_t launch_lse_merge_finish(int rows, int d, const float* buf, T* out, cudaStream_t st);
+
+}  // namespace ckv

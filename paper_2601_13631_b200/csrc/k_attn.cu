@@ -1,0 +1,287 @@
+// A7 split-K exact attention (SIMT variant) and A8 LSE combine / cross-shard merge.
+//
+// Every suffix row attends, exactly, over the kept prefix chunks (all visible; padding
+// of a partial last chunk masked, Q6) plus the causal suffix keys t <= r (Q9):
+//   O = sum_k softmax_k(q.k / sqrt(d)) v_k      (Def. 1 at PAPER.md:159).
+// Rows are GQA-packed per KV head (rho = g * n_s + r).  The key list is split across
+// CTAs; each split writes a normalised partial O and its base-2 LSE, merged by
+//   O = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M).
+#include "common.cuh"
+
+namespace ckv {
+namespace {
+
+constexpr int RB = 64;
+constexpr int KB = 64;
+constexpr int NT = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(NT) attn_simt_kernel(LayerGeom g, const T* __restrict__ q, const T* __restrict__ ks,
+                                                       const T* __restrict__ vs, const T* __restrict__ pool,
+                                                       int64_t rec_elems, const int32_t* __restrict__ kept_slots,
+                                                       const int32_t* __restrict__ kept_ids,
+                                                       const int32_t* __restrict__ n_kept_dev, int k_cap,
+                                                       int include_suffix, int nsplit, float* __restrict__ o_part,
+                                                       float* __restrict__ lse_part) {
+  extern __shared__ float sm[];
+  const int d = g.d;
+  float* Qt = sm;               // [d][RB]
+  float* Kt = Qt + d * RB;      // [d][KB]
+  float* Vs = Kt + d * KB;      // [KB][d]
+  float* S = Vs + KB * d;       // [RB][KB+1]
+  float* row_m = S + RB * (KB + 1);
+  float* row_l = row_m + RB;
+  float* row_a = row_l + RB;
+  int* kmeta = reinterpret_cast<int*>(row_a + RB);  // [KB]: -2 invalid, -1 prefix, >=0 suffix token
+
+  const int kvh = blockIdx.z, sp = blockIdx.y, row0 = blockIdx.x * RB, tid = threadIdx.x;
+  const int n_kept = *n_kept_dev;
+  const int cps = (k_cap + nsplit - 1) / nsplit;
+  const int t0 = min(n_kept, sp * cps), t1 = min(n_kept, t0 + cps);
+  const int npre = (t1 - t0) * g.c;
+  const int nkeys = npre + ((include_suffix && sp == nsplit - 1) ? g.ns : 0);
+  const float scale = kLog2e * rsqrtf((float)d);
+
+  for (int e = tid; e < RB * d; e += NT) {
+    int rr = e / d, x = e % d, rho = row0 + rr;
+    float val = 0.f;
+    if (rho < g.R) {
+      int gq = rho / g.ns, r = rho % g.ns;
+      val = to_f(q[((size_t)r * g.Hq + kvh * g.G + gq) * d + x]);
+    }
+    Qt[x * RB + rr] = val;
+  }
+  if (tid < RB) {
+    row_m[tid] = -INFINITY;
+    row_l[tid] = 0.f;
+  }
+  const int ty = tid / 16, tx = tid % 16;
+  const int DPT = d / 16;
+  float acc[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  for (int kb = 0; kb < nkeys; kb += KB) {
+    __syncthreads();
+    if (tid < KB) {
+      const int p = kb + tid;
+      int meta = -2;
+      if (p < npre) {
+        const int t = t0 + p / g.c, off = p % g.c;
+        if ((int64_t)kept_ids[t] * g.c + off < g.n_loc) meta = -1;
+      } else if (p < nkeys) {
+        meta = p - npre;
+      }
+      kmeta[tid] = meta;
+    }
+    for (int e = tid; e < KB * d; e += NT) {
+      const int kk = e / d, x = e % d, p = kb + kk;
+      float kv = 0.f, vv = 0.f;
+      if (p < npre) {
+        const int t = t0 + p / g.c, off = p % g.c;
+        const T* rec = pool + (int64_t)kept_slots[t] * rec_elems;
+        kv = to_f(rec[((int64_t)kvh * g.c + off) * d + x]);
+        vv = to_f(rec[((int64_t)(g.Hkv + kvh) * g.c + off) * d + x]);
+      } else if (p < nkeys) {
+        const int ts = p - npre;
+        kv = to_f(ks[((int64_t)ts * g.Hkv + kvh) * d + x]);
+        vv = to_f(vs[((int64_t)ts * g.Hkv + kvh) * d + x]);
+      }
+      Kt[x * KB + kk] = kv;
+      Vs[kk * d + x] = vv;
+    }
+    __syncthreads();
+    {
+      float sacc[4][4] = {};
+      for (int x = 0; x < d; ++x) {
+        float4 a = *reinterpret_cast<const float4*>(&Qt[x * RB + ty * 4]);
+        float4 b = *reinterpret_cast<const float4*>(&Kt[x * KB + tx * 4]);
+        float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sacc[i][j] = fmaf(av[i], bv[j], sacc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int rho = row0 + ty * 4 + i;
+        const int r = rho % g.ns;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int meta = kmeta[tx * 4 + j];
+          const bool ok = (meta == -1) || (meta >= 0 && meta <= r);
+          S[(ty * 4 + i) * (KB + 1) + tx * 4 + j] = ok ? sacc[i][j] * scale : -INFINITY;
+        }
+      }
+    }
+    __syncthreads();
+    {  // online softmax: 4 threads per row, 16 keys each
+      const int rr = tid >> 2, part = tid & 3;
+      float* srow = S + rr * (KB + 1) + part * 16;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) mx = fmaxf(mx, srow[i]);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float m_old = row_m[rr];
+      const float m_new = fmaxf(m_old, mx);
+      float sum = 0.f;
+      if (m_new == -INFINITY) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) srow[i] = 0.f;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p = fast_exp2(srow[i] - m_new);
+          srow[i] = p;
+          sum += p;
+        }
+      }
+      sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+      sum += __shfl_xor_sync(0xffffffffu, sum, 2);
+      __syncwarp();
+      if (part == 0) {
+        const float alpha = (m_old == -INFINITY) ? 0.f : fast_exp2(m_old - m_new);
+        row_a[rr] = alpha;
+        row_l[rr] = row_l[rr] * alpha + sum;
+        row_m[rr] = m_new;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float a = row_a[ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] *= a;
+    }
+    for (int kk = 0; kk < KB; ++kk) {
+      float pv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pv[i] = S[(ty * 4 + i) * (KB + 1) + kk];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < DPT) {
+          const float v = Vs[kk * d + tx * DPT + j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i][j] = fmaf(pv[i], v, acc[i][j]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rr = ty * 4 + i, rho = row0 + rr;
+    if (rho >= g.R) continue;
+    const float l = row_l[rr];
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    float* dst = o_part + (((int64_t)sp * g.Hkv + kvh) * g.R + rho) * d;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < DPT) dst[tx * DPT + j] = acc[i][j] * inv;
+    if (tx == 0) lse_part[((int64_t)sp * g.Hkv + kvh) * g.R + rho] = (l > 0.f) ? row_m[rr] + fast_log2(l) : -INFINITY;
+  }
+}
+
+// Merge of split partials. Output row index (r, h); input row (kvh, rho = g*ns + r).
+template <typename T>
+__global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_part, const float* __restrict__ lse_part,
+                                    int nsplit, T* __restrict__ out, float* __restrict__ o_f32,
+                                    float* __restrict__ lse_nat) {
+  const int row = blockIdx.x;  // kvh * R + rho
+  const int kvh = row / g.R, rho = row % g.R;
+  const int gq = rho / g.ns, r = rho % g.ns, h = kvh * g.G + gq;
+  const int64_t nrow = (int64_t)g.Hkv * g.R;
+  float M = -INFINITY;
+  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, lse_part[s * nrow + row]);
+  float den = 0.f;
+  for (int s = 0; s < nsplit; ++s) {
+    const float l = lse_part[s * nrow + row];
+    den += (l == -INFINITY) ? 0.f : fast_exp2(l - M);
+  }
+  const int64_t obase = ((int64_t)r * g.Hq + h) * g.d;
+  for (int x = threadIdx.x; x < g.d; x += blockDim.x) {
+    float num = 0.f;
+    for (int s = 0; s < nsplit; ++s) {
+      const float l = lse_part[s * nrow + row];
+      if (l != -INFINITY) num += fast_exp2(l - M) * o_part[(s * nrow + row) * g.d + x];
+    }
+    const float o = den > 0.f ? num / den : 0.f;
+    if (out) out[obase + x] = from_f<T>(o);
+    if (o_f32) o_f32[obase + x] = o;
+  }
+  if (lse_nat && threadIdx.x == 0)
+    lse_nat[(int64_t)r * g.Hq + h] = den > 0.f ? (M + log2f(den)) * kLn2 : -INFINITY;
+}
+
+__global__ void lse_merge_prepare_kernel(int rows, int d, const float* __restrict__ o, const float* __restrict__ lse,
+                                         const float* __restrict__ lse_max, float* __restrict__ buf) {
+  const int i = blockIdx.x;
+  if (i >= rows) return;
+  const float l = lse[i], M = lse_max[i];
+  const float w = (l == -INFINITY) ? 0.f : __expf(l - M);
+  for (int x = threadIdx.x; x < d; x += blockDim.x) buf[(int64_t)i * (d + 1) + x] = o[(int64_t)i * d + x] * w;
+  if (threadIdx.x == 0) buf[(int64_t)i * (d + 1) + d] = w;
+}
+
+template <typename T>
+__global__ void lse_merge_finish_kernel(int rows, int d, const float* __restrict__ buf, T* __restrict__ out) {
+  const int i = blockIdx.x;
+  if (i >= rows) return;
+  const float den = buf[(int64_t)i * (d + 1) + d];
+  for (int x = threadIdx.x; x < d; x += blockDim.x)
+    out[(int64_t)i * d + x] = from_f<T>(den > 0.f ? buf[(int64_t)i * (d + 1) + x] / den : 0.f);
+}
+
+}  // namespace
+
+template <typename T>
+cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, const T* v_suf, const T* pool_layer,
+                             int64_t rec_elems, const int32_t* kept_slots, const int32_t* kept_ids,
+                             const int32_t* n_kept_dev, int k_cap, int include_suffix, int nsplit, float* o_part,
+                             float* lse_part, cudaStream_t st) {
+  if (g.d % 16 != 0 || g.d > 128) return cudaErrorNotSupported;
+  size_t smem = sizeof(float) * ((size_t)g.d * RB + (size_t)g.d * KB + (size_t)KB * g.d + RB * (KB + 1) + 3 * RB) +
+                sizeof(int) * KB;
+  auto kfn = attn_simt_kernel<T>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((g.R + RB - 1) / RB, nsplit, g.Hkv);
+  kfn<<<grid, NT, smem, st>>>(g, q, k_suf, v_suf, pool_layer, rec_elems, kept_slots, kept_ids, n_kept_dev, k_cap,
+                              include_suffix, nsplit, o_part, lse_part);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit, T* out,
+                                float* o_f32, float* lse_nat, cudaStream_t st) {
+  attn_combine_kernel<T><<<g.Hkv * g.R, 128, 0, st>>>(g, o_part, lse_part, nsplit, out, o_f32, lse_nat);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lse_merge_prepare(int rows, int d, const float* o, const float* lse, const float* lse_max,
+                                     float* buf, cudaStream_t st) {
+  lse_merge_prepare_kernel<<<rows, 128, 0, st>>>(rows, d, o, lse, lse_max, buf);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_lse_merge_finish(int rows, int d, const float* buf, T* out, cudaStream_t st) {
+  lse_merge_finish_kernel<T><<<rows, 128, 0, st>>>(rows, d, buf, out);
+  return cudaGetLastError();
+}
+
+#define CKV_INST(T)                                                                                                 \
+  template cudaError_t launch_attn_simt<T>(const LayerGeom&, const T*, const T*, const T*, const T*, int64_t,       \
+                                           const int32_t*, const int32_t*, const int32_t*, int, int, int, float*,   \
+                                           float*, cudaStream_t);                                                   \
+  template cudaError_t launch_attn_combine<T>(const LayerGeom&, const float*, const float*, int, T*, float*, float*, \
+                                              cudaStream_t);                                                        \
+  template cudaError_t launch_lse_merge_finish<T>(int, int, const float*, T*, cudaStream_t);
+CKV_INST(float)
+CKV_INST(__nv_bfloat16)
+#undef CKV_INST
+
+}  // namespace ckv

@@ -1,0 +1,266 @@
+// A4 cache plan, A5 whole-chunk gather, A9 cache-score update, and the store-prefix
+// layout kernels.
+//
+// HBM chunk cache (§4.4, 424-455): per (layer, chunk) the cumulative importance
+// I_j and access count F_j live in a table that survives eviction; the
+// cache score is S_j = I_j * F_j (Eq. 2).  Selected chunks are checked
+// against the cache before loading; misses take free slots first, then the
+// slots of the lowest-(S, j) residents that are neither requested nor pinned by an
+// in-flight prefetch ("Both heaps will evict low-scored ContiguousChunks").
+// Every transfer moves one whole chunk record (unit of storage = unit of transfer =
+// unit of eviction), so read amplification is 1.
+#include "common.cuh"
+#include "select.cuh"
+
+namespace ckv {
+namespace {
+
+constexpr int NT = 1024;
+
+__device__ __forceinline__ bool bsearch_ids(const int32_t* ids, int n, int j) {
+  int lo = 0, hi = n - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int v = ids[mid];
+    if (v == j) return true;
+    if (v < j) lo = mid + 1; else hi = mid - 1;
+  }
+  return false;
+}
+
+__global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int32_t* __restrict__ ids,
+                                                        const int32_t* __restrict__ n_ids_dev, int n_ids_host,
+                                                        int prefetch, int quota, int epoch, int64_t rec_bytes,
+                                                        int32_t* __restrict__ scratch, PlanOut out) {
+  __shared__ SelectSmem ss;
+  __shared__ int s_hits, s_spec_used;
+  const int n_ids = n_ids_dev ? *n_ids_dev : n_ids_host;
+  int32_t* miss = scratch;            // [n_ids]
+  int32_t* freel = scratch + n_ids;   // [P]
+  int32_t* vict = freel + cl.P;       // [P]
+  if (threadIdx.x == 0) { s_hits = 0; s_spec_used = 0; }
+  __syncthreads();
+
+  // 1. hit / miss, misses compacted in ascending chunk order
+  int n_miss = 0;
+  for (int b = 0; b < n_ids; b += NT) {
+    const int t = b + threadIdx.x;
+    bool is_miss = false;
+    if (t < n_ids) {
+      const int s = cl.slot_of[ids[t]];
+      is_miss = s < 0;
+      if (!is_miss) {
+        atomicAdd(&s_hits, 1);
+        if (!prefetch && cl.pf_epoch[s] == epoch) atomicAdd(&s_spec_used, 1);
+      }
+    }
+    int tot;
+    const int pos = block_excl_scan<NT>(is_miss ? 1 : 0, tot, ss);
+    if (is_miss) miss[n_miss + pos] = ids[t];
+    n_miss += tot;
+  }
+  if (prefetch) n_miss = min(n_miss, quota);
+  // 2. free slots, ascending
+  int n_free = 0;
+  for (int b = 0; b < cl.P; b += NT) {
+    const int s = b + threadIdx.x;
+    const bool f = s < cl.P && cl.owner[s] < 0;
+    int tot;
+    const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+    if (f) freel[n_free + pos] = s;
+    n_free += tot;
+  }
+  // 3. victims: the `need` lowest (S, j) evictable residents
+  const int need = n_miss - n_free;
+  int n_vict = 0;
+  if (need > 0) {
+    auto key = [&](int s) -> uint64_t {
+      const int j = cl.owner[s];
+      if (j < 0) return 0ull;
+      if (bsearch_ids(ids, n_ids, j)) return 0ull;
+      if (!prefetch && cl.pf_epoch[s] == epoch) return 0ull;
+      const float S = cl.I[j] * (float)cl.F[j];
+      return ~(((uint64_t)__float_as_uint(S) << 32) | (uint64_t)(uint32_t)j);
+    };
+    const uint64_t T = block_kth_largest<NT>(key, cl.P, need, ss);
+    for (int b = 0; b < cl.P; b += NT) {
+      const int s = b + threadIdx.x;
+      uint64_t kv = 0ull;
+      if (s < cl.P) kv = key(s);
+      const bool f = kv != 0ull && kv >= T;
+      int tot;
+      const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+      if (f) vict[n_vict + pos] = s;
+      n_vict += tot;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_vict; t += NT) {
+      const int s = vict[t];
+      const int j = cl.owner[s];
+      if (out.victims) out.victims[t] = j;
+      cl.slot_of[j] = -1;
+      cl.owner[s] = -1;
+    }
+  }
+  __syncthreads();
+  // 4. assign slots to misses: free slots, then victim slots (both ascending)
+  for (int t = threadIdx.x; t < n_miss; t += NT) {
+    const int s = (t < n_free) ? freel[t] : vict[t - n_free];
+    const int j = miss[t];
+    cl.slot_of[j] = s;
+    cl.owner[s] = j;
+    cl.pf_epoch[s] = prefetch ? epoch : -1;
+    out.gather_list[2 * t] = j;
+    out.gather_list[2 * t + 1] = s;
+  }
+  __syncthreads();
+  if (out.kept_slots)
+    for (int t = threadIdx.x; t < n_ids; t += NT) out.kept_slots[t] = cl.slot_of[ids[t]];
+  if (threadIdx.x == 0) {
+    *out.n_load = n_miss;
+    if (out.counts) {
+      out.counts[0] = s_hits;
+      out.counts[1] = n_miss;
+      out.counts[2] = n_vict;
+      out.counts[3] = s_spec_used;
+    }
+    if (out.stats) {
+      unsigned long long* st = reinterpret_cast<unsigned long long*>(out.stats);
+      if (prefetch) {
+        atomicAdd(st + 2, (unsigned long long)n_miss);
+        atomicAdd(st + 5, (unsigned long long)((int64_t)n_miss * rec_bytes));
+      } else {
+        atomicAdd(st + 0, (unsigned long long)s_hits);
+        atomicAdd(st + 1, (unsigned long long)n_miss);
+        atomicAdd(st + 3, (unsigned long long)s_spec_used);
+        atomicAdd(st + 4, (unsigned long long)((int64_t)n_miss * rec_bytes));
+        atomicAdd(st + 6, 1ull);
+      }
+    }
+  }
+}
+
+// Whole-record copy host store -> HBM slot: work items are 4 KiB segments of records so a
+// few misses still keep many 16-B loads in flight over the host link.
+constexpr int GATHER_SEG = 4096;
+constexpr int GATHER_THREADS = 256;
+constexpr int GATHER_BLOCKS = 64;
+
+__global__ void __launch_bounds__(GATHER_THREADS) gather_kernel(const int32_t* __restrict__ list,
+                                                                const int32_t* __restrict__ n_load,
+                                                                const char* __restrict__ host_layer,
+                                                                char* __restrict__ pool_layer, int64_t rec_bytes) {
+  const int n = *n_load;
+  if (n == 0) return;
+  const int nseg = (int)((rec_bytes + GATHER_SEG - 1) / GATHER_SEG);
+  const int total = n * nseg;
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * GATHER_THREADS + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * GATHER_THREADS) >> 5;
+  for (int it = warp; it < total; it += nwarps) {
+    const int e = it / nseg, sg = it % nseg;
+    const int j = list[2 * e], s = list[2 * e + 1];
+    const int64_t off = (int64_t)sg * GATHER_SEG;
+    const int cnt = (int)(min((int64_t)GATHER_SEG, rec_bytes - off) / 16);
+    const int4* src = reinterpret_cast<const int4*>(host_layer + (int64_t)j * rec_bytes + off);
+    int4* dst = reinterpret_cast<int4*>(pool_layer + (int64_t)s * rec_bytes + off);
+    int4 v[GATHER_SEG / 16 / 32];
+#pragma unroll
+    for (int u = 0; u < GATHER_SEG / 16 / 32; ++u) {
+      const int i = lane + 32 * u;
+      if (i < cnt) v[u] = __ldg(src + i);
+    }
+#pragma unroll
+    for (int u = 0; u < GATHER_SEG / 16 / 32; ++u) {
+      const int i = lane + 32 * u;
+      if (i < cnt) dst[i] = v[u];
+    }
+  }
+}
+
+__global__ void cache_update_kernel(CacheLayer cl, const int32_t* __restrict__ ids, const int32_t* n_ids_dev,
+                                    const float* __restrict__ A) {
+  const int n = *n_ids_dev;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int j = ids[t];
+    cl.I[j] += A[j];  // I_j = I_j + A_j
+    cl.F[j] += 1;     // F_j: access count
+  }
+}
+
+template <typename T>
+__global__ void pack_probe_kernel(const T* __restrict__ k, int64_t t0, int n_loc, int n_pad, int Hkv, int d,
+                                  T* __restrict__ probe) {
+  // probe[kvh][i][x] = k[t0 + i][kvh][x]
+  const int64_t total = (int64_t)Hkv * n_loc * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(e % d);
+    const int64_t r = e / d;
+    const int i = (int)(r % n_loc), kvh = (int)(r / n_loc);
+    probe[((int64_t)kvh * n_pad + i) * d + x] = k[((t0 + i) * Hkv + kvh) * d + x];
+  }
+}
+
+template <typename T>
+__global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t t0, int n_loc,
+                                    int m_loc, int c, int Hkv, int d, T* __restrict__ rec) {
+  // rec[j][kv][kvh][p][x], zero padding past n_loc
+  const int64_t per = (int64_t)2 * Hkv * c * d;
+  const int64_t total = (int64_t)m_loc * per;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e / per);
+    int64_t r = e % per;
+    const int x = (int)(r % d); r /= d;
+    const int p = (int)(r % c); r /= c;
+    const int kvh = (int)(r % Hkv);
+    const int kv = (int)(r / Hkv);
+    const int64_t i = (int64_t)j * c + p;
+    T val = from_f<T>(0.f);
+    if (i < n_loc) val = (kv == 0 ? k : v)[((t0 + i) * Hkv + kvh) * d + x];
+    rec[e] = val;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
+                              int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t*,
+                              int32_t* scratch32, PlanOut out, cudaStream_t st) {
+  cache_plan_kernel<<<1, NT, 0, st>>>(cl, ids, n_ids_dev, n_ids_host, prefetch, quota, epoch, rec_bytes, scratch32,
+                                      out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
+                          char* pool_layer, int64_t rec_bytes, cudaStream_t st) {
+  gather_kernel<<<GATHER_BLOCKS, GATHER_THREADS, 0, st>>>(gather_list, n_load, host_layer_dev, pool_layer, rec_bytes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cache_update(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, const float* A,
+                                cudaStream_t st) {
+  cache_update_kernel<<<8, 256, 0, st>>>(cl, ids, n_ids_dev, A);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_pack_probe(const T* k, int64_t t0, int n_loc, int n_pad, int Hkv, int d, T* probe_layer,
+                              cudaStream_t st) {
+  pack_probe_kernel<T><<<1184, 256, 0, st>>>(k, t0, n_loc, n_pad, Hkv, d, probe_layer);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int n_loc, int m_loc, int c, int Hkv, int d,
+                                T* staging, cudaStream_t st) {
+  pack_records_kernel<T><<<1184, 256, 0, st>>>(k, v, t0, n_loc, m_loc, c, Hkv, d, staging);
+  return cudaGetLastError();
+}
+template cudaError_t launch_pack_probe<float>(const float*, int64_t, int, int, int, int, float*, cudaStream_t);
+template cudaError_t launch_pack_probe<__nv_bfloat16>(const __nv_bfloat16*, int64_t, int, int, int, int,
+                                                      __nv_bfloat16*, cudaStream_t);
+template cudaError_t launch_pack_records<float>(const float*, const float*, int64_t, int, int, int, int, int, float*,
+                                                cudaStream_t);
+template cudaError_t launch_pack_records<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, int64_t, int,
+                                                        int, int, int, int, __nv_bfloat16*, cudaStream_t);
+
+}  // namespace ckv

@@ -1,0 +1,92 @@
+// A3 top-k (exact radix select, lowest-index tie-break, ascending ids) and the
+// candidate merge of the position-sharded path.
+//
+// Keys are 64-bit composites (float bits of A_j << 32) | (0xFFFFFFFF - j): A_j >= 0 so the
+// float bit pattern orders like the value, and the index part makes every key unique
+// (larger key = larger score, then lower index), so exactly k keys are >= the k-th
+// largest key T.  T is found by eight 8-bit MSB-first histogram passes in one CTA.
+#include "common.cuh"
+#include "select.cuh"
+
+namespace ckv {
+namespace {
+
+constexpr int NT = 1024;
+
+__global__ void __launch_bounds__(NT) topk_scores_kernel(const float* __restrict__ A, int m, int k, int id_offset,
+                                                         int32_t* __restrict__ ids, uint64_t* __restrict__ cand,
+                                                         int n_cand_out, int32_t* __restrict__ n_out) {
+  __shared__ SelectSmem ss;
+  auto key = [&](int j) -> uint64_t {
+    return ((uint64_t)__float_as_uint(A[j]) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j + id_offset));
+  };
+  const int kk = min(k, m);
+  const uint64_t T = block_kth_largest<NT>(key, m, kk, ss);
+  // ascending compaction
+  int base = 0;
+  for (int j0 = 0; j0 < m; j0 += NT) {
+    const int j = j0 + threadIdx.x;
+    const bool f = (j < m) && key(j) >= T;
+    int tot;
+    const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+    if (f) {
+      if (ids) ids[base + pos] = j + id_offset;
+      if (cand) cand[base + pos] = key(j);
+    }
+    base += tot;
+  }
+  if (cand)
+    for (int t = kk + threadIdx.x; t < n_cand_out; t += NT) cand[t] = 0ull;
+  if (n_out && threadIdx.x == 0) *n_out = base;
+}
+
+// Global top-k over the gathered candidates of all shards; ids_glob ascending (identical
+// on every rank), ids_local = the selected ids this shard owns, as local chunk indices.
+__global__ void __launch_bounds__(NT) topk_merge_kernel(const uint64_t* __restrict__ cand_all, int n_cand, int k,
+                                                        int m_glob, int j0, int j1, int32_t* __restrict__ flag,
+                                                        int32_t* __restrict__ ids_glob, int32_t* __restrict__ ids_local,
+                                                        int32_t* __restrict__ n_local) {
+  __shared__ SelectSmem ss;
+  for (int j = threadIdx.x; j < m_glob; j += NT) flag[j] = 0;
+  auto key = [&](int i) -> uint64_t { return cand_all[i]; };
+  const uint64_t T = block_kth_largest<NT>(key, n_cand, k, ss);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_cand; i += NT) {
+    const uint64_t kv = cand_all[i];
+    if (kv != 0ull && kv >= T) flag[0xFFFFFFFFu - (uint32_t)(kv & 0xFFFFFFFFull)] = 1;
+  }
+  __syncthreads();
+  int base = 0, lbase = 0;
+  for (int jb = 0; jb < m_glob; jb += NT) {
+    const int j = jb + threadIdx.x;
+    const bool f = (j < m_glob) && flag[j];
+    int tot;
+    const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+    if (f) ids_glob[base + pos] = j;
+    base += tot;
+    const bool fl = f && j >= j0 && j < j1;
+    int ltot;
+    const int lpos = block_excl_scan<NT>(fl ? 1 : 0, ltot, ss);
+    if (fl) ids_local[lbase + lpos] = j - j0;
+    lbase += ltot;
+  }
+  if (threadIdx.x == 0) *n_local = lbase;
+}
+
+}  // namespace
+
+cudaError_t launch_topk_scores(const float* A, int m, int k, int id_offset, int32_t* ids, uint64_t* cand_out,
+                               int n_cand_out, int32_t* n_out, cudaStream_t st) {
+  topk_scores_kernel<<<1, NT, 0, st>>>(A, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1,
+                              int32_t* flag_scratch, int32_t* ids_glob, int32_t* ids_local, int32_t* n_local,
+                              cudaStream_t st) {
+  topk_merge_kernel<<<1, NT, 0, st>>>(cand_all, n_cand, k, m_glob, j0, j1, flag_scratch, ids_glob, ids_local,
+                                      n_local);
+  return cudaGetLastError();
+}
+
+}  // namespace ckv

@@ -1,0 +1,95 @@
+// Single-CTA radix select and block scan used by top-k (A3) and the cache planner (A4).
+#pragma once
+#include "common.cuh"
+
+namespace ckv {
+
+struct SelectSmem {
+  int hist[256];
+  int warp_tot[32];
+  int state[2];
+};
+
+// Exclusive prefix sum of v over the block (threadIdx order); *tot = block total.
+// Every thread of the block must call it.
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int& tot, SelectSmem& ss) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();  // protect warp_tot from a previous call
+  if (lane == 31) ss.warp_tot[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    int w = (lane < NT / 32) ? ss.warp_tot[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < NT / 32) ss.warp_tot[lane] = wi - w;  // exclusive warp offsets
+    if (lane == 31) ss.state[0] = wi;
+  }
+  __syncthreads();
+  tot = ss.state[0];
+  return ss.warp_tot[wid] + incl - v;
+}
+
+// k-th largest (1-based) of n keys key(i); keys must be unique among those that can
+// reach the top k.  MSB-first 8-bit digits, 8 passes.  Every thread must call it.
+template <int NT, typename KeyFn>
+__device__ uint64_t block_kth_largest(KeyFn key, int n, int k, SelectSmem& ss) {
+  uint64_t prefix = 0, mask = 0;
+  int krem = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = threadIdx.x; b < 256; b += NT) ss.hist[b] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += NT) {
+      const uint64_t kv = key(i);
+      if ((kv & mask) == prefix) atomicAdd(&ss.hist[(kv >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int cnt[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[j] = ss.hist[255 - 8 * lane - j];
+        tot += cnt[j];
+      }
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int excl = incl - tot;
+      const unsigned bal = __ballot_sync(0xffffffffu, excl < krem && incl >= krem);
+      if (lane == __ffs(bal) - 1) {
+        int cum = excl;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (cum + cnt[j] >= krem) {
+            ss.state[0] = 255 - 8 * lane - j;
+            ss.state[1] = krem - cum;
+            break;
+          }
+          cum += cnt[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (uint64_t)ss.state[0] << shift;
+    mask |= (uint64_t)255u << shift;
+    krem = ss.state[1];
+    __syncthreads();
+  }
+  return prefix;
+}
+
+}  // namespace ckv

@@ -1,0 +1,222 @@
+"""GPU parity of libckv against the fp64 oracle (calls go through the C-ABI).
+
+Sizes: the BASELINE shapes (C1 full, C2 shape, C3 full size for two layers) plus
+ragged / degenerate cases (partial last chunk, c = 1, k = 1, k = m, odd n_s).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from paper_2601_13631_b200 import CKV_FLAG_SIMT_SCORE, CkvError, Context
+from synth import CONFIGS, ShapeConfig, make_prefix, make_request
+from tests.gpu_util import check_layer, make_ctx, run_layers, to_dev
+
+pytestmark = pytest.mark.gpu
+
+C1 = CONFIGS["c1_0.5b"]
+RAGGED_FP32 = ShapeConfig("ragged_fp32", 2, 6, 2, 64, 1003, 5, 7, 1000, "fp32")
+RAGGED_BF16 = ShapeConfig("ragged_bf16", 2, 28, 4, 128, 3001, 16, 9, 1000, "bf16")
+C2_SMALL = CONFIGS["c2_3b"].replace(num_layers=4)
+C3_2L = CONFIGS["c3_7b"].replace(num_layers=2)
+
+
+def _k(cfg):
+    return O.budget_chunks(cfg.prefix_len, cfg.chunk_size, cfg.budget_bp)
+
+
+def _check_all(ctx, cfg, prefix, results, k, norm=0):
+    diags = []
+    for r in results:
+        kp, vp = prefix[r["layer"]]
+        diags.append(check_layer(r["ids"], r["out"], r["A"], r["qs"], r["ks"], r["vs"], kp, vp, cfg, k, norm))
+    return diags
+
+
+@pytest.fixture(autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+def test_c1_fp32_full_config():
+    ctx, prefix = make_ctx(C1)
+    res = run_layers(ctx, C1, prefix, [0])
+    _check_all(ctx, C1, prefix, res, _k(C1))
+
+
+@pytest.mark.parametrize("cfg", [RAGGED_FP32, RAGGED_BF16], ids=lambda c: c.name)
+def test_ragged_partial_last_chunk(cfg):
+    k = 17
+    ctx, prefix = make_ctx(cfg, k=k, prefetch=k)
+    res = run_layers(ctx, cfg, prefix, range(cfg.num_layers))
+    _check_all(ctx, cfg, prefix, res, k)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_token_level_c1(dtype):
+    cfg = ShapeConfig("tok", 1, 4, 2, 64 if dtype == "fp32" else 128, 700, 1, 5, 1000, dtype)
+    ctx, prefix = make_ctx(cfg, k=37)
+    res = run_layers(ctx, cfg, prefix, [0])
+    _check_all(ctx, cfg, prefix, res, 37)
+
+
+@pytest.mark.parametrize("k", [1, "m"])
+def test_degenerate_budgets(k):
+    cfg = ShapeConfig("deg", 1, 8, 2, 128, 1040, 16, 12, 1000, "bf16")
+    kk = cfg.num_chunks if k == "m" else k
+    ctx, prefix = make_ctx(cfg, k=kk)
+    res = run_layers(ctx, cfg, prefix, [0])
+    _check_all(ctx, cfg, prefix, res, kk)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_fullrow_normalisation(dtype):
+    cfg = ShapeConfig("fr", 1, 8, 2, 64 if dtype == "fp32" else 128, 2048, 16, 24, 1000, dtype)
+    ctx, prefix = make_ctx(cfg, norm=1)
+    res = run_layers(ctx, cfg, prefix, [0])
+    _check_all(ctx, cfg, prefix, res, _k(cfg), norm=1)
+
+
+def test_c2_shape_layers_prefetch_and_cache_invariance():
+    cfg = C2_SMALL
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg, prefetch=k)
+    res = run_layers(ctx, cfg, prefix, range(cfg.num_layers))
+    _check_all(ctx, cfg, prefix, res, k)
+    st = ctx.get_stats()
+    assert st["total_spec_loads"] > 0 and st["total_spec_used"] > 0
+    # results never depend on the cache: warm (same request again), then cold
+    res2 = run_layers(ctx, cfg, prefix, range(cfg.num_layers))
+    ctx.reset_cache()
+    res3 = run_layers(ctx, cfg, prefix, range(cfg.num_layers))
+    for a, b, c in zip(res, res2, res3):
+        assert np.array_equal(a["ids"], b["ids"]) and np.array_equal(a["ids"], c["ids"])
+        assert np.array_equal(a["out"], b["out"]) and np.array_equal(a["out"], c["out"])
+
+
+def test_c3_full_size_two_layers():
+    cfg = C3_2L
+    k = _k(cfg)
+    assert k == 204
+    ctx, prefix = make_ctx(cfg, prefetch=k)
+    res = run_layers(ctx, cfg, prefix, range(2))
+    diags = _check_all(ctx, cfg, prefix, res, k)
+    print("C3 diagnostics", diags, "score kernel", ctx.score_kernel_kind)
+
+
+def test_score_kernels_agree_simt_vs_default():
+    cfg = RAGGED_BF16.replace(num_layers=1, prefix_len=4099)
+    k = 23
+    a, prefix = make_ctx(cfg, k=k)
+    b, _ = make_ctx(cfg, k=k, flags=CKV_FLAG_SIMT_SCORE)
+    ra = run_layers(a, cfg, prefix, [0])[0]
+    rb = run_layers(b, cfg, prefix, [0])[0]
+    np.testing.assert_allclose(ra["A"], rb["A"], rtol=2e-4)
+    check_layer(ra["ids"], ra["out"], ra["A"], ra["qs"], ra["ks"], ra["vs"], *prefix[0], cfg, k)
+
+
+# ---------------------------------------------------------------- top-k (bit exact)
+@pytest.mark.parametrize("m", [1, 7, 300, 2048, 32768])
+def test_topk_exact_with_ties(m):
+    ctx = Context(1, 1, 1, 64, 1, m, 1, dtype="fp32", budget_chunks=m)
+    g = np.random.default_rng(m)
+    for trial in range(4):
+        A = g.integers(0, 6, m).astype(np.float32) if trial % 2 else g.random(m).astype(np.float32)
+        if trial == 3:
+            A[:] = 0.0
+        Ad = torch.from_numpy(A).cuda()
+        for k in sorted({1, max(1, m // 10), max(1, m // 2), m}):
+            ids = ctx.test_topk(Ad, k).cpu().numpy()
+            assert ids.tolist() == O.select_topk(A.astype(np.float64), k).tolist()
+
+
+# ---------------------------------------------------------------- cache planner (A4/A9)
+def test_cache_plan_matches_model():
+    m, P, k = 64, 20, 8
+    ctx = Context(1, 1, 1, 64, 1, m, 1, dtype="fp32", budget_chunks=k, cache_slots=P)
+    ctx.store_prefix(0, torch.zeros(m, 1, 64, device="cuda"), torch.zeros(m, 1, 64, device="cuda"))
+    model = O.CacheModel(1, m, P)
+    g = np.random.default_rng(7)
+    for step in range(40):
+        A = g.integers(0, 50, m).astype(np.float32)  # integer scores: S exact in fp32 and fp64
+        ids = np.sort(g.choice(m // 2 if step % 3 else m, k, replace=False)).astype(np.int32)
+        hits_m, loads_m, vict_m = model.plan(0, ids)
+        model.update(0, ids, A.astype(np.float64))
+        loads, victims, counts = ctx.test_cache_step(0, torch.from_numpy(ids).cuda(), A=torch.from_numpy(A).cuda())
+        counts = counts.cpu().numpy()
+        loads = loads.cpu().numpy()[: 2 * counts[1]].reshape(-1, 2)
+        assert counts[0] == len(hits_m) and counts[1] == len(loads_m) and counts[2] == len(vict_m)
+        assert sorted(loads[:, 0].tolist()) == sorted(j for j, _ in loads_m)
+        assert sorted(victims.cpu().numpy()[: counts[2]].tolist()) == sorted(vict_m)
+        assert len(set(loads[:, 1].tolist())) == len(loads) and loads[:, 1].max(initial=0) < P
+
+
+# ---------------------------------------------------------------- sharded (logical, 1 GPU)
+@pytest.mark.parametrize("W", [2, 3, 4])
+def test_sharded_logical_on_one_gpu(W):
+    cfg = ShapeConfig("sh", 2, 8, 2, 128, 4000, 16, 10, 1000, "bf16")
+    k = _k(cfg)
+    ctxs = [make_ctx(cfg, shard=g, W=W, prefetch=k // 2)[0] for g in range(W)]
+    for l in range(cfg.num_layers):
+        kp, vp = make_prefix(cfg, l)
+        qs, ks, vs = make_request(cfg, l, 0)
+        q, k_, v_ = (to_dev(x, torch.bfloat16) for x in (qs, ks, vs))
+        ns = qs.shape[0]
+        lam = [torch.empty(cfg.num_q_heads * ns, device="cuda") for _ in range(W)]
+        for g_, c in enumerate(ctxs):
+            c.shard_score(l, q, k_, lam[g_])
+        lam_all = torch.cat(lam)                                   # allgather
+        cands = [torch.empty(k, dtype=torch.int64, device="cuda") for _ in range(W)]
+        for g_, c in enumerate(ctxs):
+            c.shard_select(l, q, k_, lam_all, cands[g_])
+        cand_all = torch.cat(cands)                                # allgather
+        o = [torch.empty(ns, cfg.num_q_heads, cfg.head_dim, device="cuda") for _ in range(W)]
+        lse = [torch.empty(ns * cfg.num_q_heads, device="cuda") for _ in range(W)]
+        ids = [torch.empty(k, dtype=torch.int32, device="cuda") for _ in range(W)]
+        for g_, c in enumerate(ctxs):
+            c.shard_attend(l, cand_all, q, k_, v_, o[g_], lse[g_], ids[g_])
+        M = torch.stack(lse).max(dim=0).values                     # allreduce(max)
+        bufs = []
+        for g_, c in enumerate(ctxs):
+            b = torch.empty(ns * cfg.num_q_heads * (cfg.head_dim + 1), device="cuda")
+            c.lse_merge_prepare(o[g_], lse[g_], M, ns, b)
+            bufs.append(b)
+        tot = torch.stack(bufs).sum(dim=0)                         # allreduce(sum)
+        out = torch.empty(ns, cfg.num_q_heads, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
+        ctxs[0].lse_merge_finish(tot, ns, out)
+        torch.cuda.synchronize()
+        for g_ in range(1, W):
+            assert torch.equal(ids[0], ids[g_])
+        check_layer(ids[0].cpu().numpy(), out.float().cpu().numpy(), None, qs, ks, vs, kp, vp, cfg, k)
+
+
+# ---------------------------------------------------------------- errors and accounting
+def test_errors_are_reported():
+    cfg = ShapeConfig("err", 2, 4, 2, 64, 256, 16, 8, 1000, "fp32")
+    ctx, prefix = make_ctx(cfg, layers=2, store=False)
+    q = torch.zeros(8, 4, 64, device="cuda")
+    kv = torch.zeros(8, 2, 64, device="cuda")
+    with pytest.raises(CkvError, match="ESTATE"):
+        ctx.reprefill_layer(0, q, kv, kv)
+    with pytest.raises(CkvError, match="EINVAL"):
+        ctx.reprefill_layer(5, q, kv, kv)
+    with pytest.raises(CkvError, match="EINVAL"):
+        ctx.store_prefix(0, torch.zeros(255, 2, 64, device="cuda"), torch.zeros(255, 2, 64, device="cuda"))
+    with pytest.raises(CkvError):
+        Context(1, 3, 2, 64, 16, 256, 8, dtype="fp32")  # Hq % Hkv != 0
+
+
+def test_delta_law_and_whole_chunk_transfers():
+    cfg = C2_SMALL.replace(num_layers=3, prefix_len=4096)
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg, prefetch=k)
+    rec = 2 * cfg.num_kv_heads * cfg.chunk_size * cfg.head_dim * 2
+    ctx.reset_stats()
+    for r in range(3):
+        run_layers(ctx, cfg, prefix, range(cfg.num_layers), request=r, with_A=False)
+    st = ctx.get_stats()
+    assert st["total_link_bytes_delta"] == st["total_misses"] * rec       # RA = 1, whole chunks
+    assert st["total_link_bytes_spec"] == st["total_spec_loads"] * rec
+    assert st["total_hits"] + st["total_misses"] == 3 * cfg.num_layers * k
+    assert st["total_layers"] == 3 * cfg.num_layers
