@@ -177,7 +177,8 @@ ckv_status ckv_reset_stats(ckv_ctx* ctx);
 int32_t ckv_num_chunks(const ckv_ctx* ctx);        /* m (global) */
 int32_t ckv_num_local_chunks(const ckv_ctx* ctx);  /* m_g of this shard */
 int32_t ckv_k(const ckv_ctx* ctx);                 /* k */
-int32_t ckv_score_kernel_kind(const ckv_ctx* ctx); /* 0 = SIMT, 1 = tcgen05 */
+int32_t ckv_score_kernel_kind(const ckv_ctx* ctx); /* A1 kernel: 0 = SIMT, 1 = tcgen05 */
+int32_t ckv_attn_kernel_kind(const ckv_ctx* ctx);  /* A7 kernel: 0 = SIMT, 1 = tcgen05 */
 
 /* Stage profiling: when enabled, CUDA events are recorded on the caller's stream
  * around each stage of every hot-path call.  ckv_profile_read synchronises, returns

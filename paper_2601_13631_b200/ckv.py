@@ -68,6 +68,7 @@ SIGNATURES = {
     "ckv_num_local_chunks": (_I32, [_P]),
     "ckv_k": (_I32, [_P]),
     "ckv_score_kernel_kind": (_I32, [_P]),
+    "ckv_attn_kernel_kind": (_I32, [_P]),
     "ckv_test_topk": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P]),
     "ckv_test_cache_step": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _P, _P, _P, _P, _P]),
     "ckv_profile": (ctypes.c_int, [_P, _I32]),
@@ -153,6 +154,10 @@ class Context:
     @property
     def score_kernel_kind(self) -> int:
         return self.lib.ckv_score_kernel_kind(self.h)
+
+    @property
+    def attn_kernel_kind(self) -> int:
+        return self.lib.ckv_attn_kernel_kind(self.h)
 
     # ---------------------------------------------------------------- C-ABI
     def store_prefix(self, layer, k, v, stream=None):

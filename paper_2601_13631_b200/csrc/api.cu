@@ -30,6 +30,7 @@ struct ckv_ctx {
   int64_t rec_elems = 0, rec_bytes = 0;
   int nsplit_score_max = 1, nsplit_attn_max = 1;
   int score_kind = 0;  // 0 SIMT, 1 tcgen05
+  int attn_kind = 0;   // 0 SIMT, 1 tcgen05
 
   void* probe = nullptr;
   char* host_store = nullptr;
@@ -246,7 +247,7 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
   PROF_END(4);
   if (pf) CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
   LayerGeom g = geom(ctx, ns);
-  const int nsplit = attn_nsplit(ctx, ns, ctx->k);
+  int nsplit = attn_nsplit(ctx, ns, ctx->k);
   PROF_BEGIN(5);
   if (ctx->dtype == CKV_FP32) {
     LK(launch_attn_simt<float>(g, static_cast<const float*>(q), static_cast<const float*>(ks),
@@ -256,11 +257,25 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
     LK(launch_attn_combine<float>(g, ctx->o_part, ctx->lse_part, nsplit, static_cast<float*>(out), o_f32, lse_nat,
                                   st));
   } else {
-    LK(launch_attn_simt<__nv_bfloat16>(g, static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(ks),
-                                       static_cast<const __nv_bfloat16*>(vs),
-                                       reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->rec_elems,
-                                       ctx->kept_slots, ids, n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part,
-                                       ctx->lse_part, st));
+    cudaError_t e = cudaErrorNotSupported;
+    if (ctx->attn_kind == 1) {
+      nsplit = attn_tc_nsplit(g, ctx->k, include_suffix);
+      e = launch_attn_tc(g, static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(ks),
+                         static_cast<const __nv_bfloat16*>(vs),
+                         reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->P, ctx->kept_slots, ids,
+                         n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->tmap_cache, st);
+      if (e == cudaSuccess) ctx->launches += 1;  // + the Q pack kernel
+    }
+    if (e == cudaErrorNotSupported) {
+      nsplit = attn_nsplit(ctx, ns, ctx->k);
+      e = launch_attn_simt<__nv_bfloat16>(g, static_cast<const __nv_bfloat16*>(q),
+                                          static_cast<const __nv_bfloat16*>(ks), static_cast<const __nv_bfloat16*>(vs),
+                                          reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)),
+                                          ctx->rec_elems, ctx->kept_slots, ids, n_ids_dev, ctx->k, include_suffix,
+                                          nsplit, ctx->o_part, ctx->lse_part, st);
+    }
+    CK(e);
+    ++ctx->launches;
     LK(launch_attn_combine<__nv_bfloat16>(g, ctx->o_part, ctx->lse_part, nsplit, static_cast<__nv_bfloat16*>(out),
                                           o_f32, lse_nat, st));
   }
@@ -380,6 +395,10 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   CKC(cudaSetDevice(c.device));
   const int R_max = ctx->G * ctx->max_ns;
   ctx->nsplit_score_max = ctx->m_loc < 4096 ? ctx->m_loc : 4096;
+  {
+    const int tc_splits = 4 * ((ctx->n_loc + 255) / 256);
+    if (ctx->nsplit_score_max < tc_splits) ctx->nsplit_score_max = tc_splits;
+  }
   ctx->nsplit_attn_max = 64;
   const size_t probe_elems = (size_t)ctx->L * ctx->Hkv * ctx->n_pad * ctx->d;
   CKC(cudaMalloc(&ctx->probe, probe_elems * ctx->esz));
@@ -438,7 +457,12 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
     LayerGeom g = geom(ctx, ctx->max_ns);
     if (score_tc_nsplit(g) <= 0) ctx->score_kind = 0;
   }
-  if (ctx->score_kind == 1) CKC(cudaMalloc(&ctx->tmap_cache, 4096));
+  {
+    LayerGeom g = geom(ctx, ctx->max_ns);
+    ctx->attn_kind = (ctx->dtype == CKV_BF16 && attn_tc_supported(g) && !(c.flags & CKV_FLAG_SIMT_ATTN)) ? 1 : 0;
+  }
+  if (ctx->score_kind == 1 || ctx->attn_kind == 1)
+    CKC(cudaMalloc(&ctx->tmap_cache, score_tc_qpack_elems(ctx->Hkv, R_max) * sizeof(__nv_bfloat16)));
   CKC(cudaDeviceSynchronize());
 #undef CKC
   (void)st;
@@ -695,6 +719,7 @@ int32_t ckv_num_chunks(const ckv_ctx* ctx) { return ctx ? ctx->m : -1; }
 int32_t ckv_num_local_chunks(const ckv_ctx* ctx) { return ctx ? ctx->m_loc : -1; }
 int32_t ckv_k(const ckv_ctx* ctx) { return ctx ? ctx->k : -1; }
 int32_t ckv_score_kernel_kind(const ckv_ctx* ctx) { return ctx ? ctx->score_kind : -1; }
+int32_t ckv_attn_kernel_kind(const ckv_ctx* ctx) { return ctx ? ctx->attn_kind : -1; }
 
 ckv_status ckv_test_topk(ckv_ctx* ctx, const float* A, int32_t m, int32_t k, int32_t* ids, void* stream) {
   if (!ctx) return CKV_EINVAL;

@@ -46,8 +46,9 @@ cudaError_t launch_score_simt(const LayerGeom& g, const T* q, const T* probe_lay
                               float* lampart, int nsplit, cudaStream_t st);
 // A1 tcgen05 (bf16 only, d == 128); returns cudaErrorNotSupported if the shape is outside it
 cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* probe_layer,
-                            float* lam2, float* lampart, int nsplit, void* tmap_cache, cudaStream_t st);
-int score_tc_nsplit(const LayerGeom& g);
+                            float* lam2, float* lampart, int nsplit, void* qpack_ws, cudaStream_t st);
+int score_tc_nsplit(const LayerGeom& g);   // 0 if the shape is outside the tcgen05 kernel
+size_t score_tc_qpack_elems(int Hkv, int R_max);
 // A2: Lambda2[kvh][R] = LSE2 over splits (+ causal suffix if fullrow) ; also writes row LSE for shards
 template <typename T>
 cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit, const T* q, const T* k_suf,
@@ -99,6 +100,13 @@ cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, con
                              const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap,
                              int include_suffix, int nsplit, float* o_part, float* lse_part,
                              cudaStream_t st);
+bool attn_tc_supported(const LayerGeom& g);
+int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix);
+cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* k_suf,
+                           const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, int P_slots,
+                           const int32_t* kept_slots, const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap,
+                           int include_suffix, int nsplit, float* o_part, float* lse_part, void* qpack_ws,
+                           cudaStream_t st);
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit,
                                 T* out, float* o_f32, float* lse_nat, cudaStream_t st);

@@ -1,0 +1,457 @@
+// A7 split-K exact attention on tcgen05 (bf16, d = 128), flash-attention style.
+//
+// Same contract as attn_simt_kernel (k_attn.cu): for every GQA-packed suffix row and every
+// key split, a normalised partial O and its base-2 LSE over the kept prefix chunks (all
+// visible, partial-chunk padding masked) and the causal suffix keys t <= r
+// (Q6, Q9).  A8 (attn_combine) merges the splits.
+//
+// Per work item (kv head, 128-row tile, key split), 1 CTA per SM, 320 threads:
+//   warp 0      TMA: Q tile (GQA-packed [Hkv][R_pad][128]); per 128-key tile the K and V
+//               blocks of 128/c kept chunks straight from their HBM cache slots (one 2-D box
+//               per chunk: [c tokens][64] x 2 halves, record layout [K|V][Hkv][c][d]), or the
+//               suffix tile through a 3-D map over k_suf / v_suf; missing chunks are fetched
+//               out of bounds (zero fill).  Two 64 KB K|V stages.
+//   warp 1      TMEM alloc + MMA issue: S = Q K^T (M 128, N 128, K 128; K-major / K-major) into one
+//               of two TMEM S buffers, then O += P V (P K-major from smem, V MN-major) into the TMEM
+//               O accumulator, software-pipelined one tile behind S.
+//   warps 2..9  softmax: one row per thread, two warps per TMEM lane quadrant (64 key columns
+//               and 64 O columns each); row max exchanged through shared memory; lazy O rescale
+//               (only when the running max grows by > 8 in log2 units) via tcgen05.ld/st;
+//               P = 2^(s - m) written as bf16 in the 128-byte-swizzled K-major layout.
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace ckv {
+namespace {
+
+constexpr int BM = 128, BN = 128, D = 128;
+constexpr int kSoftWarps = 8;
+constexpr int kThreads = 64 + 32 * kSoftWarps;
+constexpr uint32_t kQBytes = BM * D * 2;           // 32 KB
+constexpr uint32_t kKVBytes = 2 * BN * D * 2;      // K + V = 64 KB
+constexpr uint32_t kPBytes = BM * BN * 2;          // 32 KB
+constexpr size_t kSmem = kQBytes + 2 * kKVBytes + kPBytes + 4096 + 1024;
+constexpr float kRescaleThresh = 8.f;              // log2 units
+
+struct AttnParams {
+  LayerGeom g;
+  const int32_t* kept_slots;
+  const int32_t* kept_ids;
+  const int32_t* n_kept_dev;
+  int k_cap;
+  int include_suffix;
+  int nsplit;
+  int MT, R_pad;
+  int NTp_cap, NTs, T_cap;
+  int pool_rows;
+  int n_items;
+  float scale;
+  float* o_part;
+  float* lse_part;
+};
+
+struct Tiles {
+  int t0, t1;  // [t0, t1) in the tile index space of the item's KV head
+  int NTp;     // prefix tiles actually present
+};
+
+__device__ __forceinline__ Tiles item_tiles(const AttnParams& p, int sp, int n_kept) {
+  Tiles t;
+  t.t0 = (int)((int64_t)sp * p.T_cap / p.nsplit);
+  t.t1 = (int)((int64_t)(sp + 1) * p.T_cap / p.nsplit);
+  t.NTp = (n_kept * p.g.c + BN - 1) / BN;
+  return t;
+}
+// skip prefix tiles past the kept chunks; suffix tiles live at [NTp_cap, NTp_cap + NTs)
+__device__ __forceinline__ bool tile_present(const AttnParams& p, const Tiles& tl, int t) {
+  return (t < p.NTp_cap) ? (t < tl.NTp) : (p.include_suffix != 0);
+}
+
+// O += P V for the tile that was scored one step earlier (MMA thread).
+__device__ __forceinline__ void issue_pv(uint32_t tmem_O, uint32_t pa, uint8_t* kvbuf0, uint64_t* p_full,
+                                         uint64_t* p_empty, uint64_t* o_empty, uint64_t* kv_empty, uint32_t idesc_o,
+                                         int jj, int stage, int icount, int& pcount) {
+  ptx::mbar_wait(p_full, pcount & 1);
+  if (jj == 0) ptx::mbar_wait(o_empty, (icount & 1) ^ 1);
+  ptx::tc_fence_after();
+  const uint32_t va = ptx::smem_u32(kvbuf0 + stage * kKVBytes + kKVBytes / 2);
+#pragma unroll
+  for (int k = 0; k < BN / 16; ++k) {
+    const uint64_t adesc = ptx::umma_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32);
+    const uint64_t bdesc = ptx::umma_desc_sw128_mn(va + k * 16 * 128, kKVBytes / 4);
+    ptx::mma_bf16(tmem_O, adesc, bdesc, idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
+  }
+  ptx::mma_commit(p_empty);
+  ptx::mma_commit(&kv_empty[stage]);
+  ++pcount;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmPool,
+                   const __grid_constant__ CUtensorMap tmKs, const __grid_constant__ CUtensorMap tmVs, AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* qbuf = smem;
+  uint8_t* kvbuf0 = smem + kQBytes;
+  uint8_t* pbuf = kvbuf0 + 2 * kKVBytes;
+  float* red_m = reinterpret_cast<float*>(pbuf + kPBytes);  // [2][128]
+  float* red_l = red_m + 256;                                // [2][128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red_l + 256);
+  uint64_t* q_full = bars + 0;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;   // [2]
+  uint64_t* kv_empty = bars + 4;  // [2]
+  uint64_t* s_full = bars + 6;    // [2]
+  uint64_t* s_empty = bars + 8;   // [2]
+  uint64_t* p_full = bars + 10;
+  uint64_t* p_empty = bars + 11;
+  uint64_t* o_full = bars + 12;
+  uint64_t* o_empty = bars + 13;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_kept = *p.n_kept_dev;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&kv_empty[i], 1);
+      ptx::mbar_init(&s_full[i], 1);
+      ptx::mbar_init(&s_empty[i], kSoftWarps);
+    }
+    ptx::mbar_init(p_full, kSoftWarps);
+    ptx::mbar_init(p_empty, 1);
+    ptx::mbar_init(o_full, 1);
+    ptx::mbar_init(o_empty, kSoftWarps);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_O = tmem + 256;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmQ);
+      ptx::tma_prefetch_desc(&tmPool);
+      int icount = 0, kvcount = 0;
+      const int cpt = BN / p.g.c;  // chunks per key tile
+      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
+        const int sp = it % p.nsplit, mt = (it / p.nsplit) % p.MT, kvh = it / (p.nsplit * p.MT);
+        const Tiles tl = item_tiles(p, sp, n_kept);
+        ptx::mbar_wait(q_empty, (icount & 1) ^ 1);
+        ptx::mbar_expect_tx(q_full, kQBytes);
+        const int yq = kvh * p.R_pad + mt * BM;
+        ptx::tma_load_2d(qbuf, &tmQ, q_full, 0, yq);
+        ptx::tma_load_2d(qbuf + kQBytes / 2, &tmQ, q_full, 64, yq);
+        for (int t = tl.t0; t < tl.t1; ++t) {
+          if (!tile_present(p, tl, t)) continue;
+          const int st = kvcount & 1;
+          ptx::mbar_wait(&kv_empty[st], ((kvcount >> 1) & 1) ^ 1);
+          ptx::mbar_expect_tx(&kv_full[st], kKVBytes);
+          uint8_t* kb = kvbuf0 + st * kKVBytes;
+          uint8_t* vb = kb + kKVBytes / 2;
+          if (t < p.NTp_cap) {
+            for (int q = 0; q < cpt; ++q) {
+              const int ti = t * cpt + q;
+              int rk = p.pool_rows, rv = p.pool_rows;  // out of bounds -> zero fill
+              if (ti < n_kept) {
+                const int slot = p.kept_slots[ti];
+                rk = ((slot * 2 + 0) * p.g.Hkv + kvh) * p.g.c;
+                rv = ((slot * 2 + 1) * p.g.Hkv + kvh) * p.g.c;
+              }
+              const uint32_t off = q * p.g.c * 128;
+              ptx::tma_load_2d(kb + off, &tmPool, &kv_full[st], 0, rk);
+              ptx::tma_load_2d(kb + kKVBytes / 4 + off, &tmPool, &kv_full[st], 64, rk);
+              ptx::tma_load_2d(vb + off, &tmPool, &kv_full[st], 0, rv);
+              ptx::tma_load_2d(vb + kKVBytes / 4 + off, &tmPool, &kv_full[st], 64, rv);
+            }
+          } else {
+            const int ts0 = (t - p.NTp_cap) * BN;
+            ptx::tma_load_3d(kb, &tmKs, &kv_full[st], 0, kvh, ts0);
+            ptx::tma_load_3d(kb + kKVBytes / 4, &tmKs, &kv_full[st], 64, kvh, ts0);
+            ptx::tma_load_3d(vb, &tmVs, &kv_full[st], 0, kvh, ts0);
+            ptx::tma_load_3d(vb + kKVBytes / 4, &tmVs, &kv_full[st], 64, kvh, ts0);
+          }
+          ++kvcount;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);
+      constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(BM, D, true);
+      int icount = 0, kvcount = 0, scount = 0, pcount = 0;
+      const uint32_t qa = ptx::smem_u32(qbuf);
+      const uint32_t pa = ptx::smem_u32(pbuf);
+      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
+        const int sp = it % p.nsplit;
+        const Tiles tl = item_tiles(p, sp, n_kept);
+        ptx::mbar_wait(q_full, icount & 1);
+        int j = 0, prev_stage = 0;
+        for (int t = tl.t0; t < tl.t1; ++t) {
+          if (!tile_present(p, tl, t)) continue;
+          const int st = kvcount & 1;
+          ptx::mbar_wait(&kv_full[st], (kvcount >> 1) & 1);
+          const int sb = scount & 1;
+          ptx::mbar_wait(&s_empty[sb], ((scount >> 1) & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t ka = ptx::smem_u32(kvbuf0 + st * kKVBytes);
+#pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+            const uint32_t off_k = (k >> 2) * (kKVBytes / 4) + (k & 3) * 32;
+            ptx::mma_bf16(tmem + sb * BN, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k),
+                          idesc_s, k > 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&s_full[sb]);
+          ++scount;
+          if (j > 0) issue_pv(tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, idesc_o, j - 1, prev_stage, icount, pcount);
+          prev_stage = st;
+          ++kvcount;
+          ++j;
+        }
+        if (j > 0) issue_pv(tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, idesc_o, j - 1, prev_stage, icount, pcount);
+        ptx::mma_commit(q_empty);
+        ptx::mma_commit(o_full);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax / epilogue
+    const int e = warp - 2, quad = warp & 3, h = e >> 2;
+    const int rit = quad * 32 + lane;  // row in tile
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t bar_id = 1 + quad;  // named barrier shared by the two warps of a quadrant
+    int icount = 0, scount = 0, pcount = 0;
+    const float sc = p.scale;
+    int n_valid_prefix = 0;
+    if (n_kept > 0) {
+      const int last = p.kept_ids[n_kept - 1];
+      n_valid_prefix = (n_kept - 1) * p.g.c + min(p.g.c, p.g.n_loc - last * p.g.c);
+    }
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
+      const int sp = it % p.nsplit, mt = (it / p.nsplit) % p.MT, kvh = it / (p.nsplit * p.MT);
+      const Tiles tl = item_tiles(p, sp, n_kept);
+      const int rho = mt * BM + rit;
+      const bool row_ok = rho < p.g.R;
+      const int r = rho % p.g.ns;
+      float m_ref = -INFINITY, l = 0.f;
+      int j = 0;
+      for (int t = tl.t0; t < tl.t1; ++t) {
+        if (!tile_present(p, tl, t)) continue;
+        const int sb = scount & 1;
+        ptx::mbar_wait(&s_full[sb], (scount >> 1) & 1);
+        ptx::tc_fence_after();
+        float x[64];
+        ptx::tmem_ld32p(tmem + sb * BN + h * 64 + lane_off, x);
+        ptx::tmem_ld32p(tmem + sb * BN + h * 64 + 32 + lane_off, x + 32);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
+        ++scount;
+        // mask + scale (log2 units)
+        const int col0 = h * 64;
+        if (t < p.NTp_cap) {
+          const int kbase = t * BN + col0;
+          if (kbase + 64 > n_valid_prefix) {
+#pragma unroll
+            for (int i = 0; i < 64; ++i)
+              if (kbase + i >= n_valid_prefix) x[i] = -INFINITY;
+          }
+        } else {
+          const int tbase = (t - p.NTp_cap) * BN + col0;
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (tbase + i > r || tbase + i >= p.g.ns) x[i] = -INFINITY;
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          mx[i] = fmaxf(fmaxf(fmaxf(x[8 * i], x[8 * i + 1]), fmaxf(x[8 * i + 2], x[8 * i + 3])),
+                        fmaxf(fmaxf(x[8 * i + 4], x[8 * i + 5]), fmaxf(x[8 * i + 6], x[8 * i + 7])));
+        }
+        float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        red_m[h * 128 + rit] = tmax;
+        ptx::named_bar_sync(bar_id, 64);
+        tmax = fmaxf(red_m[rit], red_m[128 + rit]) * sc;
+        ptx::named_bar_sync(bar_id, 64);  // red_m reusable
+        const float m_new = fmaxf(m_ref, tmax);
+        const bool resc = (j > 0) && (m_ref != -INFINITY) && (m_new > m_ref + kRescaleThresh);
+        if (j == 0 || m_ref == -INFINITY) {
+          m_ref = m_new;
+        }
+        if (__any_sync(0xffffffffu, resc)) {
+          // O must hold PV(j-1) before it is rescaled
+          ptx::mbar_wait(p_empty, (pcount - 1) & 1);
+          ptx::tc_fence_after();
+          const float f = resc ? fast_exp2(m_ref - m_new) : 1.f;
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            float o[32];
+            const uint32_t ta = tmem_O + h * 64 + half * 32 + lane_off;
+            ptx::tmem_ld32(ta, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= f;
+            ptx::tmem_st32(ta, o);
+          }
+          l *= f;
+          if (resc) m_ref = m_new;
+        }
+        const float msub = (m_ref == -INFINITY) ? 0.f : m_ref;
+        float lsum = 0.f;
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float p0 = fast_exp2(fmaf(x[2 * i], sc, -msub));
+          const float p1 = fast_exp2(fmaf(x[2 * i + 1], sc, -msub));
+          lsum += p0 + p1;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        l += lsum;
+        // P buffer free (PV(j-1) done reading it)?
+        ptx::mbar_wait(p_empty, (pcount & 1) ^ 1);
+        uint8_t* prow = pbuf + h * (kPBytes / 2) + rit * 128;
+#pragma unroll
+        for (int c16 = 0; c16 < 8; ++c16) {
+          const int phys = c16 ^ (rit & 7);
+          *reinterpret_cast<uint4*>(prow + phys * 16) =
+              make_uint4(pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]);
+        }
+        ptx::fence_proxy_async_smem();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(p_full);
+        ++pcount;
+        ++j;
+      }
+      // final O of this item
+      ptx::mbar_wait(o_full, icount & 1);
+      ptx::tc_fence_after();
+      red_l[h * 128 + rit] = l;
+      ptx::named_bar_sync(bar_id, 64);
+      const float ltot = red_l[rit] + red_l[128 + rit];
+      ptx::named_bar_sync(bar_id, 64);
+      float o[64];
+      if (j > 0) {
+        ptx::tmem_ld32p(tmem_O + h * 64 + lane_off, o);
+        ptx::tmem_ld32p(tmem_O + h * 64 + 32 + lane_off, o + 32);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(o_empty);
+      if (row_ok) {
+        const float inv = (j > 0 && ltot > 0.f) ? 1.f / ltot : 0.f;
+        float* dst = p.o_part + (((size_t)sp * p.g.Hkv + kvh) * p.g.R + rho) * D + h * 64;
+#pragma unroll
+        for (int i = 0; i < 64; i += 4)
+          *reinterpret_cast<float4*>(dst + i) =
+              (j > 0) ? make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (h == 0)
+          p.lse_part[((size_t)sp * p.g.Hkv + kvh) * p.g.R + rho] =
+              (j > 0 && ltot > 0.f) ? m_ref + fast_log2(ltot) : -INFINITY;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem);
+  }
+}
+
+__global__ void pack_q_attn_kernel(LayerGeom g, int R_pad, const __nv_bfloat16* __restrict__ q,
+                                   __nv_bfloat16* __restrict__ qpack) {
+  const int64_t total = (int64_t)g.Hkv * R_pad * (D / 8);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int x8 = (int)(i % (D / 8));
+    const int64_t row = i / (D / 8);
+    const int kvh = (int)(row / R_pad), rho = (int)(row % R_pad);
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (rho < g.R) {
+      const int gq = rho / g.ns, r = rho % g.ns;
+      val = *reinterpret_cast<const uint4*>(q + ((int64_t)r * g.Hq + kvh * g.G + gq) * D + x8 * 8);
+    }
+    *reinterpret_cast<uint4*>(qpack + row * D + x8 * 8) = val;
+  }
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+bool attn_tc_supported(const LayerGeom& g) {
+  return g.d == D && g.c >= 8 && g.c <= BN && (BN % g.c) == 0;
+}
+
+int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix) {
+  const int MT = (g.R + BM - 1) / BM;
+  const int T_cap = (k_cap * g.c + BN - 1) / BN + (include_suffix ? (g.ns + BN - 1) / BN : 0);
+  int s = sm_count() / (g.Hkv * MT);
+  if (s < 1) s = 1;
+  if (s > T_cap) s = T_cap;
+  return s < 1 ? 1 : s;
+}
+
+cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* k_suf,
+                           const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, int P_slots,
+                           const int32_t* kept_slots, const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap,
+                           int include_suffix, int nsplit, float* o_part, float* lse_part, void* qpack_ws,
+                           cudaStream_t st) {
+  if (!attn_tc_supported(g) || !qpack_ws) return cudaErrorNotSupported;
+  AttnParams p;
+  p.g = g;
+  p.kept_slots = kept_slots;
+  p.kept_ids = kept_ids;
+  p.n_kept_dev = n_kept_dev;
+  p.k_cap = k_cap;
+  p.include_suffix = include_suffix;
+  p.nsplit = nsplit;
+  p.MT = (g.R + BM - 1) / BM;
+  p.R_pad = p.MT * BM;
+  p.NTp_cap = (k_cap * g.c + BN - 1) / BN;
+  p.NTs = (g.ns + BN - 1) / BN;
+  p.T_cap = p.NTp_cap + (include_suffix ? p.NTs : 0);
+  p.pool_rows = P_slots * 2 * g.Hkv * g.c;
+  p.n_items = g.Hkv * p.MT * nsplit;
+  p.scale = kLog2e / sqrtf((float)g.d);
+  p.o_part = o_part;
+  p.lse_part = lse_part;
+  auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
+  pack_q_attn_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  CUtensorMap tmQ, tmPool, tmKs, tmVs;
+  if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_2d(&tmPool, pool_layer, D, (uint64_t)p.pool_rows, (uint32_t)g.c)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_3d(&tmKs, k_suf, D, g.Hkv, g.ns, BN)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_3d(&tmVs, v_suf, D, g.Hkv, g.ns, BN)) return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = p.n_items < sm_count() ? p.n_items : sm_count();
+  attn_tc_kernel<<<grid, kThreads, kSmem, st>>>(tmQ, tmPool, tmKs, tmVs, p);
+  return cudaGetLastError();
+}
+
+}  // namespace ckv

@@ -20,23 +20,39 @@ __device__ __forceinline__ void lse2_acc(float& M, float& S, float v) {
   }
 }
 
+// Block = 8 warps x 32 rows: lane <-> row, warp w reduces splits w, w+8, ... (fixed order),
+// then warp 0 merges the 8 partials in order and adds the FULLROW suffix term.
 template <typename T>
-__global__ void row_lse_kernel(LayerGeom g, const float* __restrict__ lampart, int nsplit,
-                               const T* __restrict__ q, const T* __restrict__ ks, int fullrow,
-                               const float* __restrict__ lam_all, int W, float* __restrict__ Lam2,
-                               float* __restrict__ lam_local_out) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // = kvh * R + row = h * ns + r
-  if (idx >= g.Hkv * g.R) return;
-  const int kvh = idx / g.R, row = idx % g.R;
+__global__ void __launch_bounds__(256) row_lse_kernel(LayerGeom g, const float* __restrict__ lampart, int nsplit,
+                                                      const T* __restrict__ q, const T* __restrict__ ks, int fullrow,
+                                                      const float* __restrict__ lam_all, int W,
+                                                      float* __restrict__ Lam2, float* __restrict__ lam_local_out) {
+  __shared__ float sM[8][32], sS[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int idx = blockIdx.x * 32 + lane;  // = kvh * R + row = h * ns + r
+  const bool ok = idx < g.Hkv * g.R;
+  const int kvh = ok ? idx / g.R : 0, row = ok ? idx % g.R : 0;
   float M = -INFINITY, S = 0.f;
-  if (lam_all == nullptr) {
-    for (int sp = 0; sp < nsplit; ++sp) lse2_acc(M, S, lampart[((size_t)kvh * nsplit + sp) * g.R + row]);
-    float loc = (S > 0.f) ? M + fast_log2(S) : -INFINITY;
-    if (lam_local_out) lam_local_out[idx] = loc;
-  } else {
-    const int n = g.Hkv * g.R;
-    for (int w = 0; w < W; ++w) lse2_acc(M, S, lam_all[(size_t)w * n + idx]);
+  if (ok) {
+    if (lam_all == nullptr) {
+      const float* src = lampart + (size_t)kvh * nsplit * g.R + row;
+      for (int sp = warp; sp < nsplit; sp += 8) lse2_acc(M, S, src[(size_t)sp * g.R]);
+    } else {
+      const int n = g.Hkv * g.R;
+      for (int w = warp; w < W; w += 8) lse2_acc(M, S, lam_all[(size_t)w * n + idx]);
+    }
   }
+  sM[warp][lane] = M;
+  sS[warp][lane] = S;
+  __syncthreads();
+  if (warp != 0 || !ok) return;
+  M = -INFINITY;
+  S = 0.f;
+  for (int w = 0; w < 8; ++w) {
+    const float m = sM[w][lane], s = sS[w][lane];
+    if (s > 0.f) lse2_acc(M, S, m + fast_log2(s));
+  }
+  if (lam_all == nullptr && lam_local_out) lam_local_out[idx] = (S > 0.f) ? M + fast_log2(S) : -INFINITY;
   if (fullrow) {
     // causal suffix keys t <= r of the same KV head (Q1 FULLROW, Q9)
     const int gq = row / g.ns, r = row % g.ns, h = kvh * g.G + gq;
@@ -76,7 +92,7 @@ cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit,
                            int fullrow, const float* lam_all, int W, float* Lam2, float* lam_local_out,
                            cudaStream_t st) {
   const int n = g.Hkv * g.R;
-  row_lse_kernel<T><<<(n + 127) / 128, 128, 0, st>>>(g, lampart, nsplit, q, k_suf, fullrow, lam_all, W, Lam2,
+  row_lse_kernel<T><<<(n + 31) / 32, 256, 0, st>>>(g, lampart, nsplit, q, k_suf, fullrow, lam_all, W, Lam2,
                                                      lam_local_out);
   return cudaGetLastError();
 }

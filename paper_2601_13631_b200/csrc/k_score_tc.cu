@@ -1,9 +1,344 @@
-// A1 score-partial on tcgen05 (placeholder until the tensor-core kernel lands).
+// A1 score-partial on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), bf16, d = 128.
+//
+// Same contract as the SIMT kernel (k_score_simt.cu): for every (KV head, suffix row rho,
+// chunk j) it writes lam2 = log2 sum_{i in chunk j} 2^(l_i log2 e), l_i = q.k_i / sqrt(d)
+// (Q2-Q5), and per (row, 64-key quarter tile) a partial base-2 LSE.
+//
+// Layout / schedule (persistent, one CTA per SM, 576 threads):
+//   warp 0      TMA producer: K tiles [256 keys x 128] (64 KB, double-buffered, loaded once per
+//               (kv head, key tile) = K-stationary) and Q tiles [128 rows x 128] (32 KB, 2 stages)
+//               from a GQA-packed Q [Hkv][R_pad][128]; 128-byte swizzle.
+//   warp 1      TMEM allocator + single-thread MMA issuer: D[128 x 256] fp32 in TMEM
+//               (two accumulators = all 512 columns), 8 x tcgen05.mma kind::f16 (K = 16 each).
+//   warps 2..17 epilogue: tcgen05.ld 32 columns at a time, one suffix row per thread (TMEM lane),
+//               four warps per lane quadrant (64 columns each); per-chunk LSE in registers,
+//               coalesced lam2 stores ([kvh][chunk][row] layout).
+// Work units (kv head, key tile, row tile) are linearised with the row tile fastest and split
+// into contiguous ranges per CTA, so each K tile crosses HBM about once.
+#include <cstdio>
+
 #include "common.cuh"
+#include "tc_ptx.cuh"
+
 namespace ckv {
-int score_tc_nsplit(const LayerGeom&) { return 0; }
-cudaError_t launch_score_tc(const LayerGeom&, const __nv_bfloat16*, const __nv_bfloat16*, float*, float*, int, void*,
-                            cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace {
+
+constexpr int BM = 128, BN = 256, D = 128;
+constexpr int kEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 key columns each
+constexpr int kColSplit = kEpiWarps / 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr uint32_t kKBytes = BN * D * 2;  // 65536
+constexpr uint32_t kQBytes = BM * D * 2;  // 32768
+constexpr size_t kSmem = 2 * kKBytes + 2 * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
+
+struct TcParams {
+  LayerGeom g;
+  float* lam2;
+  float* lampart;
+  int nsplit;   // = 2 * NKT
+  int NKT;      // key tiles per kv head
+  int MT;       // row tiles per kv head
+  int R_pad;
+  int n_units;  // Hkv * NKT * MT
+  float scale;  // log2(e) / sqrt(d)
+};
+
+// In-place pairwise tree: after the call a[0..N/G) hold sums of consecutive groups of G.
+template <int N, int G>
+__device__ __forceinline__ void tree_sum(float* a) {
+  if constexpr (G > 1) {
+    tree_sum<N, G / 2>(a);
+#pragma unroll
+    for (int i = 0; i < N / G; ++i) a[i] = a[2 * i] + a[2 * i + 1];
+  }
 }
+
+template <int C>
+__device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32], int key0, int kvh, int rho,
+                                               bool row_ok, float& HM, float& HS, float& CM, float& CS) {
+  const float sc = p.scale;
+  if (key0 + 32 > p.g.n_loc) {  // only the shard's last key tile (warp-uniform)
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (key0 + j >= p.g.n_loc) v[j] = -INFINITY;
+  }
+  float m[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m[i] = fmaxf(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+  for (int n = 8; n >= 1; n >>= 1)
+#pragma unroll
+    for (int i = 0; i < n; ++i) m[i] = fmaxf(m[2 * i], m[2 * i + 1]);
+  const float gm = m[0];
+  const float gms = (gm == -INFINITY) ? 0.f : gm * sc;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = fast_exp2(fmaf(v[j], sc, -gms));
+  constexpr int CG = C < 32 ? C : 32;  // chunk piece inside this group
+  tree_sum<32, CG>(v);                 // v[0 .. 32/CG) = chunk (piece) sums
+  float cs[32 / CG];
+#pragma unroll
+  for (int i = 0; i < 32 / CG; ++i) cs[i] = v[i];
+  tree_sum<32 / CG, 32 / CG>(v);
+  const float gs = v[0];
+  if (gs > 0.f) {  // running LSE of this warp's 64-key quarter tile
+    if (HS == 0.f) {
+      HM = gms;
+      HS = gs;
+    } else {
+      const float nm = fmaxf(HM, gms);
+      HS = HS * fast_exp2(HM - nm) + gs * fast_exp2(gms - nm);
+      HM = nm;
+    }
+  }
+  float* lam = p.lam2 + (size_t)kvh * p.g.m_loc * p.g.R + rho;
+  if constexpr (C <= 32) {
+#pragma unroll
+    for (int i = 0; i < 32 / C; ++i) {
+      const int chunk = key0 / C + i;
+      if (row_ok && chunk < p.g.m_loc)
+        lam[(size_t)chunk * p.g.R] = (cs[i] > 0.f) ? gms + fast_log2(cs[i]) : -INFINITY;
+    }
+  } else {
+    if (gs > 0.f) {
+      if (CS == 0.f) {
+        CM = gms;
+        CS = gs;
+      } else {
+        const float nm = fmaxf(CM, gms);
+        CS = CS * fast_exp2(CM - nm) + gs * fast_exp2(gms - nm);
+        CM = nm;
+      }
+    }
+    if (((key0 + 32) % C) == 0) {
+      const int chunk = key0 / C;
+      if (row_ok && chunk < p.g.m_loc) lam[(size_t)chunk * p.g.R] = (CS > 0.f) ? CM + fast_log2(CS) : -INFINITY;
+      CM = -INFINITY;
+      CS = 0.f;
+    }
+  }
+}
+
+template <int C>
+__global__ void __launch_bounds__(kThreads, 1)
+    score_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ, TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* kbuf0 = smem;
+  uint8_t* qbuf0 = smem + 2 * kKBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kKBytes + 2 * kQBytes);
+  uint64_t* k_full = bars + 0;
+  uint64_t* k_empty = bars + 2;
+  uint64_t* q_full = bars + 4;
+  uint64_t* q_empty = bars + 6;
+  uint64_t* acc_full = bars + 8;
+  uint64_t* acc_empty = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
+  const int u1 = (int)((int64_t)(blockIdx.x + 1) * p.n_units / gridDim.x);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&q_full[i], 1);
+      ptx::mbar_init(&q_empty[i], 1);
+      ptx::mbar_init(&acc_full[i], 1);
+      ptx::mbar_init(&acc_empty[i], kEpiWarps);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmK);
+      ptx::tma_prefetch_desc(&tmQ);
+      int kcount = 0, qcount = 0, cur = -1;
+      for (int u = u0; u < u1; ++u) {
+        const int pr = u / p.MT, mt = u % p.MT;
+        const int kvh = pr / p.NKT, kt = pr % p.NKT;
+        if (pr != cur) {
+          const int kb = kcount & 1;
+          ptx::mbar_wait(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
+          ptx::mbar_expect_tx(&k_full[kb], kKBytes);
+          const int y = kvh * p.g.n_pad + kt * BN;
+          uint8_t* dst = kbuf0 + kb * kKBytes;
+          ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
+          ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
+          cur = pr;
+          ++kcount;
+        }
+        const int qs = qcount & 1;
+        ptx::mbar_wait(&q_empty[qs], ((qcount >> 1) & 1) ^ 1);
+        ptx::mbar_expect_tx(&q_full[qs], kQBytes);
+        const int yq = kvh * p.R_pad + mt * BM;
+        uint8_t* dq = qbuf0 + qs * kQBytes;
+        ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
+        ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
+        ++qcount;
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
+      int kcount = 0, qcount = 0, acount = 0, cur = -1, kb = 0;
+      for (int u = u0; u < u1; ++u) {
+        const int pr = u / p.MT;
+        if (pr != cur) {
+          kb = kcount & 1;
+          ptx::mbar_wait(&k_full[kb], (kcount >> 1) & 1);
+          ++kcount;
+          cur = pr;
+        }
+        const int qs = qcount & 1;
+        ptx::mbar_wait(&q_full[qs], (qcount >> 1) & 1);
+        const int ab = acount & 1;
+        ptx::mbar_wait(&acc_empty[ab], ((acount >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + ab * BN;
+        const uint32_t qa = ptx::smem_u32(qbuf0 + qs * kQBytes);
+        const uint32_t ka = ptx::smem_u32(kbuf0 + kb * kKBytes);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+          const uint32_t off_k = (k >> 2) * (kKBytes / 2) + (k & 3) * 32;
+          ptx::mma_bf16(d_tmem, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k), idesc,
+                        k > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(&q_empty[qs]);
+        ptx::mma_commit(&acc_full[ab]);
+        const bool last_of_pair = (u + 1 == u1) || ((u + 1) / p.MT != pr);
+        if (last_of_pair) ptx::mma_commit(&k_empty[kb]);
+        ++qcount;
+        ++acount;
+      }
+    }
+  } else {
+    const int e = warp - 2;
+    const int quad = warp & 3;
+    const int half = e >> 2;  // column quarter
+    const int row_in_tile = quad * 32 + lane;
+    int acount = 0;
+    for (int u = u0; u < u1; ++u) {
+      const int pr = u / p.MT, mt = u % p.MT;
+      const int kvh = pr / p.NKT, kt = pr % p.NKT;
+      const int ab = acount & 1;
+      ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
+      ptx::tc_fence_after();
+      const int rho = mt * BM + row_in_tile;
+      const bool row_ok = rho < p.g.R;
+      float HM = -INFINITY, HS = 0.f, CM = -INFINITY, CS = 0.f;
+#pragma unroll 1
+      for (int gi = 0; gi < BN / kColSplit / 32; ++gi) {
+        const int col0 = half * (BN / kColSplit) + gi * 32;
+        float v[32];
+        ptx::tmem_ld32(tmem_base + (uint32_t)(ab * BN + col0) + ((uint32_t)(quad * 32) << 16), v);
+        epilogue_group<C>(p, v, kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
+      }
+      if (row_ok)
+        p.lampart[((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho] =
+            (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
+      ++acount;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// GQA row packing: qpack[kvh][rho][x] = q[r][kvh*G + g][x], rho = g*ns + r, zero rows past R.
+__global__ void pack_q_kernel(LayerGeom g, int R_pad, const __nv_bfloat16* __restrict__ q,
+                              __nv_bfloat16* __restrict__ qpack) {
+  const int64_t total = (int64_t)g.Hkv * R_pad * (D / 8);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int x8 = (int)(i % (D / 8));
+    const int64_t row = i / (D / 8);
+    const int kvh = (int)(row / R_pad), rho = (int)(row % R_pad);
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (rho < g.R) {
+      const int gq = rho / g.ns, r = rho % g.ns;
+      val = *reinterpret_cast<const uint4*>(q + ((int64_t)r * g.Hq + kvh * g.G + gq) * D + x8 * 8);
+    }
+    *reinterpret_cast<uint4*>(qpack + row * D + x8 * 8) = val;
+  }
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int C>
+cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  score_tc_kernel<C><<<grid, kThreads, kSmem, st>>>(tmK, tmQ, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int score_tc_nsplit(const LayerGeom& g) {
+  if (g.d != D) return 0;
+  if (g.c < 1 || g.c > BN / kColSplit || ((BN / kColSplit) % g.c) != 0) return 0;
+  return kColSplit * ((g.n_loc + BN - 1) / BN);
+}
+
+size_t score_tc_qpack_elems(int Hkv, int R_max) { return (size_t)Hkv * ((R_max + BM - 1) / BM) * BM * D; }
+
+cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* probe_layer, float* lam2,
+                            float* lampart, int nsplit, void* qpack_ws, cudaStream_t st) {
+  if (score_tc_nsplit(g) == 0 || nsplit != score_tc_nsplit(g) || !qpack_ws) return cudaErrorNotSupported;
+  TcParams p;
+  p.g = g;
+  p.lam2 = lam2;
+  p.lampart = lampart;
+  p.nsplit = nsplit;
+  p.NKT = nsplit / kColSplit;
+  p.MT = (g.R + BM - 1) / BM;
+  p.R_pad = p.MT * BM;
+  p.n_units = g.Hkv * p.NKT * p.MT;
+  p.scale = kLog2e / sqrtf((float)g.d);
+  auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
+  pack_q_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  CUtensorMap tmK, tmQ;
+  if (!make_tmap_bf16_2d(&tmK, probe_layer, D, (uint64_t)g.Hkv * g.n_pad, BN)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) return cudaErrorInvalidValue;
+  const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
+  switch (g.c) {
+    case 1: return launch_c<1>(tmK, tmQ, p, grid, st);
+    case 2: return launch_c<2>(tmK, tmQ, p, grid, st);
+    case 4: return launch_c<4>(tmK, tmQ, p, grid, st);
+    case 8: return launch_c<8>(tmK, tmQ, p, grid, st);
+    case 16: return launch_c<16>(tmK, tmQ, p, grid, st);
+    case 32: return launch_c<32>(tmK, tmQ, p, grid, st);
+    case 64: return launch_c<64>(tmK, tmQ, p, grid, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
 }  // namespace ckv

@@ -116,6 +116,20 @@ def test_score_kernels_agree_simt_vs_default():
     check_layer(ra["ids"], ra["out"], ra["A"], ra["qs"], ra["ks"], ra["vs"], *prefix[0], cfg, k)
 
 
+@pytest.mark.parametrize("c,ns,k", [(16, 130, 21), (8, 1, 5), (32, 40, 9), (64, 200, 3), (16, 256, 64)])
+def test_tensor_core_paths_vs_oracle_shapes(c, ns, k):
+    """tcgen05 score + attention across chunk sizes, 1..2 suffix tiles, k not a multiple of 128/c."""
+    from paper_2601_13631_b200 import CKV_FLAG_SIMT_ATTN
+    cfg = ShapeConfig("tcshape", 1, 8, 2, 128, 5003, c, ns, 1000, "bf16")
+    a, prefix = make_ctx(cfg, k=k)
+    b, _ = make_ctx(cfg, k=k, flags=CKV_FLAG_SIMT_ATTN | CKV_FLAG_SIMT_SCORE)
+    assert a.attn_kernel_kind == 1 and b.attn_kernel_kind == 0
+    ra = run_layers(a, cfg, prefix, [0])[0]
+    rb = run_layers(b, cfg, prefix, [0])[0]
+    check_layer(ra["ids"], ra["out"], ra["A"], ra["qs"], ra["ks"], ra["vs"], *prefix[0], cfg, k)
+    check_layer(rb["ids"], rb["out"], rb["A"], rb["qs"], rb["ks"], rb["vs"], *prefix[0], cfg, k)
+
+
 # ---------------------------------------------------------------- top-k (bit exact)
 @pytest.mark.parametrize("m", [1, 7, 300, 2048, 32768])
 def test_topk_exact_with_ties(m):
