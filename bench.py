@@ -219,17 +219,41 @@ def run_ckv(args, rank, world):
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    ctx.reset_stats()
+    # host cost of enqueueing one eager step (launch-bound check)
+    t0 = time.perf_counter()
+    step(0)
+    host_ms = (time.perf_counter() - t0) * 1e3
+    torch.cuda.synchronize()
     launches0 = ctx.kernel_launches
-    with ClockSampler(local_rank) as clk:
-        ms = timed(step, args.steps)
+    ms_eager = timed(step, args.steps) / args.steps
     launches = ctx.kernel_launches - launches0
+
+    # one CUDA graph per request input set: the 28-layer step replays without host launches
+    graphs = None
+    if args.graph and world == 1:
+        graphs = []
+        for r in range(N_REQUESTS):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(r)
+            graphs.append(g)
+        for g in graphs:
+            g.replay()
+        torch.cuda.synchronize()
+
+    def graph_step(i):
+        graphs[i % N_REQUESTS].replay()
+
+    main_step = graph_step if graphs else step
+    ctx.reset_stats()
+    with ClockSampler(local_rank) as clk:
+        ms = timed(main_step, args.steps)
     stats = ctx.get_stats()
     ms_step = ms / args.steps
     bpl = bytes_per_layer(cfg, k)
     value = bpl * L / (ms_step * 1e-3) / 1e9
 
-    # stage profile pass (CUDA events on the launching stream, inside the library)
+    # stage profile pass (eager; CUDA events on the launching stream, inside the library)
     ctx.profile(True)
     ms_prof = timed(step, args.steps)
     prof = ctx.profile_read()
@@ -239,14 +263,19 @@ def run_ckv(args, rank, world):
     # pinned memory and D2H of its outputs inside the timed region
     host_out = [torch.empty(outs[0].shape, dtype=dt).pin_memory() for _ in range(L)]
     host_ids = [torch.empty(k, dtype=torch.int32).pin_memory() for _ in range(L)]
-    dev_in = [[torch.empty_like(t) for t in lay] for lay in reqs[0]]
 
     def e2e_step(i):
-        per = reqs_host[i % N_REQUESTS]
+        r = i % N_REQUESTS
+        per_h, per_d = reqs_host[r], reqs[r]
         for l in range(L):
-            for dst, src in zip(dev_in[l], per[l]):
+            for dst, src in zip(per_d[l], per_h[l]):
                 dst.copy_(src, non_blocking=True)
-            layer_call(l, *dev_in[l])
+        if graphs:
+            graphs[r].replay()
+        else:
+            for l in range(L):
+                layer_call(l, *per_d[l])
+        for l in range(L):
             host_out[l].copy_(outs[l], non_blocking=True)
             host_ids[l].copy_(ids[l], non_blocking=True)
 
@@ -283,6 +312,7 @@ def run_ckv(args, rank, world):
         "metric": "Re-Prefill effective KV GB/s (Qwen2.5-7B shape, 32K prefix)",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3 / L,
+        "eager": {"ms_per_step": ms_eager, "host_enqueue_ms_per_step": host_ms, "cuda_graph": bool(graphs)},
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seed 42, SURVEY §8(d) recipe)",
         "config": {"workload": CFG_NAME, "layers": L, "prefix_len": cfg.prefix_len, "chunk": cfg.chunk_size,
@@ -305,7 +335,7 @@ def run_ckv(args, rank, world):
                   "link_bytes_per_layer": (stats["total_link_bytes_delta"] + stats["total_link_bytes_spec"]) / n_lay},
         "e2e": {"value": bpl * L / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
+        "gpu_launches": launches,  # kernels per K steps (counted on the eager pass; the graphs hold the same)
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
         "context": "paper: 3.85x average Re-Prefill (TTFT) speedup over IMPRESS on 1x A800 + PCIe4 + NVMe "
@@ -325,6 +355,7 @@ def main():
     ap.add_argument("--impl", default="ckv", choices=["ckv", "reference"])
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ckv" else args.warmup
     rank = int(os.environ.get("RANK", 0))

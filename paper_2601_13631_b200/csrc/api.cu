@@ -47,6 +47,7 @@ struct ckv_ctx {
   int32_t* counts = nullptr;  // [L][2][4]
   float *o_part = nullptr, *lse_part = nullptr;
   int64_t* stats = nullptr;  // [16]
+  int32_t* epoch_dev = nullptr;  // request counter on the device (graph-safe)
   void* tmap_cache = nullptr;
 
   cudaStream_t side = nullptr;
@@ -218,7 +219,8 @@ ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int
   if (ctx->quota <= 0 || layer >= ctx->L) return CKV_OK;
   CK(cudaEventRecord(ctx->ev_ids, st));
   CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ids, 0));
-  PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)(layer * 2 + 1) * 4, ctx->stats};
+  PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)(layer * 2 + 1) * 4, ctx->stats,
+             nullptr, ctx->epoch_dev};
   LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 1, ctx->quota, ctx->epoch, ctx->rec_bytes, nullptr,
                        ctx->scratch_side, po, ctx->side));
   CK(cudaEventRecord(ctx->ev_pplan[layer], ctx->side));
@@ -236,7 +238,7 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
   const bool pf = ctx->pf_issued[layer] == ctx->epoch;
   if (pf) CK(cudaStreamWaitEvent(st, ctx->ev_pplan[layer], 0));
   PlanOut po{ctx->gl_main, ctx->nload_main, ctx->kept_slots, nullptr, ctx->counts + (size_t)(layer * 2) * 4,
-             ctx->stats};
+             ctx->stats, ctx->A, ctx->epoch_dev};
   PROF_BEGIN(3);
   LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 0, 0, ctx->epoch, ctx->rec_bytes, nullptr,
                        ctx->scratch_main, po, st));
@@ -280,9 +282,6 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
                                           o_f32, lse_nat, st));
   }
   PROF_END(5);
-  PROF_BEGIN(7);
-  LK(launch_cache_update(cache_layer(ctx, layer), ids, n_ids_dev, ctx->A, st));
-  PROF_END(7);
   ctx->last_layer = layer;
   return CKV_OK;
 }
@@ -303,7 +302,7 @@ void free_all(ckv_ctx* ctx) {
                       ctx->lampart, ctx->Lam2, ctx->A, ctx->ids_buf[0], ctx->ids_buf[1], ctx->n_ids_buf[0],
                       ctx->n_ids_buf[1], ctx->kept_slots, ctx->ids_glob, ctx->flag, ctx->scratch_main,
                       ctx->scratch_side, ctx->gl_main, ctx->gl_side, ctx->nload_main, ctx->nload_side, ctx->counts,
-                      ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache};
+                      ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache, ctx->epoch_dev};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (ctx->host_store) cudaFreeHost(ctx->host_store);
@@ -439,6 +438,8 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   CKC(dalloc(&ctx->o_part, (size_t)ctx->nsplit_attn_max * ctx->Hkv * R_max * ctx->d));
   CKC(dalloc(&ctx->lse_part, (size_t)ctx->nsplit_attn_max * ctx->Hkv * R_max));
   CKC(dalloc(&ctx->stats, 16));
+  CKC(dalloc(&ctx->epoch_dev, 1));
+  CKC(cudaMemset(ctx->epoch_dev, 0, sizeof(int32_t)));
   CKC(cudaMemset(ctx->stats, 0, sizeof(int64_t) * 16));
   int lo = 0, hi = 0;
   CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -537,7 +538,10 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
   if (!q || !k_suf || !v_suf || !out || !selected_ids) return fail(ctx, CKV_EINVAL, "null argument");
   CK(cudaSetDevice(ctx->cfg.device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (layer == 0) ++ctx->epoch;
+  if (layer == 0) {
+    ++ctx->epoch;
+    LK(launch_epoch_inc(ctx->epoch_dev, st));
+  }
   int nsplit = 0;
   if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
   LayerGeom g = geom(ctx, n_suffix);
@@ -565,7 +569,10 @@ ckv_status ckv_shard_score(ckv_ctx* ctx, int32_t layer, const void* q, const voi
   if (s != CKV_OK) return s;
   if (!q || !k_suf || !lam_local) return fail(ctx, CKV_EINVAL, "null argument");
   CK(cudaSetDevice(ctx->cfg.device));
-  if (layer == 0) ++ctx->epoch;
+  if (layer == 0) {
+    ++ctx->epoch;
+    LK(launch_epoch_inc(ctx->epoch_dev, static_cast<cudaStream_t>(stream)));
+  }
   int nsplit = 0;
   return run_score(ctx, layer, q, k_suf, n_suffix, lam_local, &nsplit, static_cast<cudaStream_t>(stream));
 }
@@ -668,6 +675,7 @@ ckv_status ckv_get_stats(ckv_ctx* ctx, ckv_stats* out) {
   out->total_link_bytes_delta = s[4];
   out->total_link_bytes_spec = s[5];
   out->total_layers = s[6];
+  if (s[15]) return fail(ctx, CKV_ESTATE, "HBM chunk cache overflow detected by the planner (P < k + quota?)");
   if (ctx->last_layer >= 0) {
     int32_t cnt[8];
     CK(cudaMemcpy(cnt, ctx->counts + (size_t)ctx->last_layer * 8, sizeof cnt, cudaMemcpyDeviceToHost));
@@ -737,7 +745,7 @@ ckv_status ckv_test_cache_step(ckv_ctx* ctx, int32_t layer, const int32_t* ids, 
     return fail(ctx, CKV_EINVAL, "bad argument");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   ++ctx->epoch;
-  PlanOut po{loads, ctx->nload_main, prefetch ? nullptr : ctx->kept_slots, victims, counts, nullptr};
+  PlanOut po{loads, ctx->nload_main, prefetch ? nullptr : ctx->kept_slots, victims, counts, nullptr, nullptr, nullptr};
   LK(launch_cache_plan(cache_layer(ctx, layer), ids, nullptr, k, prefetch ? 1 : 0, ctx->quota, ctx->epoch,
                        ctx->rec_bytes, nullptr, ctx->scratch_main, po, st));
   if (A && !prefetch) {

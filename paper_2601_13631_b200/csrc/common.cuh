@@ -78,10 +78,13 @@ struct PlanOut {
   int32_t* victims;      // [cap] or null
   int32_t* counts;       // [4]: hits, loads, victims, spec_used  (or null)
   int64_t* stats;        // device counters or null
+  const float* upd_A;    // if set (demand plans): fused A9 update I += A, F += 1 after planning
+  const int32_t* epoch_dev;  // if set: request epoch read from device memory (graph-safe)
 };
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t* scratch64,
                               int32_t* scratch32, PlanOut out, cudaStream_t st);
+cudaError_t launch_epoch_inc(int32_t* epoch_dev, cudaStream_t st);
 cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
                           char* pool_layer, int64_t rec_bytes, cudaStream_t st);
 cudaError_t launch_cache_update(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev,

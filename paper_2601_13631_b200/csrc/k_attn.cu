@@ -246,8 +246,12 @@ cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, con
   size_t smem = sizeof(float) * ((size_t)g.d * RB + (size_t)g.d * KB + (size_t)KB * g.d + RB * (KB + 1) + 3 * RB) +
                 sizeof(int) * KB;
   auto kfn = attn_simt_kernel<T>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static int attr_done = 0;  // per template instance; set before any graph capture
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024 * 4);
+    if (e != cudaSuccess) return e;
+    attr_done = 1;
+  }
   dim3 grid((g.R + RB - 1) / RB, nsplit, g.Hkv);
   kfn<<<grid, NT, smem, st>>>(g, q, k_suf, v_suf, pool_layer, rec_elems, kept_slots, kept_ids, n_kept_dev, k_cap,
                               include_suffix, nsplit, o_part, lse_part);

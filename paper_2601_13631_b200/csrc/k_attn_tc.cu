@@ -135,33 +135,41 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_O = tmem + 256;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (whole warp:
+    // lanes fetch the tile's slot ids in parallel, lane 0 issues the copies)
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmQ);
       ptx::tma_prefetch_desc(&tmPool);
-      int icount = 0, kvcount = 0;
-      const int cpt = BN / p.g.c;  // chunks per key tile
-      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
-        const int sp = it % p.nsplit, mt = (it / p.nsplit) % p.MT, kvh = it / (p.nsplit * p.MT);
-        const Tiles tl = item_tiles(p, sp, n_kept);
+    }
+    int icount = 0, kvcount = 0;
+    const int cpt = BN / p.g.c;  // chunks per key tile (<= 16)
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
+      const int sp = it % p.nsplit, mt = (it / p.nsplit) % p.MT, kvh = it / (p.nsplit * p.MT);
+      const Tiles tl = item_tiles(p, sp, n_kept);
+      if (lane == 0) {
         ptx::mbar_wait(q_empty, (icount & 1) ^ 1);
         ptx::mbar_expect_tx(q_full, kQBytes);
         const int yq = kvh * p.R_pad + mt * BM;
         ptx::tma_load_2d(qbuf, &tmQ, q_full, 0, yq);
         ptx::tma_load_2d(qbuf + kQBytes / 2, &tmQ, q_full, 64, yq);
-        for (int t = tl.t0; t < tl.t1; ++t) {
-          if (!tile_present(p, tl, t)) continue;
-          const int st = kvcount & 1;
+      }
+      for (int t = tl.t0; t < tl.t1; ++t) {
+        if (!tile_present(p, tl, t)) continue;
+        int my_slot = -1;
+        if (t < p.NTp_cap && lane < cpt && t * cpt + lane < n_kept) my_slot = p.kept_slots[t * cpt + lane];
+        const int st = kvcount & 1;
+        uint8_t* kb = kvbuf0 + st * kKVBytes;
+        uint8_t* vb = kb + kKVBytes / 2;
+        if (lane == 0) {
           ptx::mbar_wait(&kv_empty[st], ((kvcount >> 1) & 1) ^ 1);
           ptx::mbar_expect_tx(&kv_full[st], kKVBytes);
-          uint8_t* kb = kvbuf0 + st * kKVBytes;
-          uint8_t* vb = kb + kKVBytes / 2;
-          if (t < p.NTp_cap) {
-            for (int q = 0; q < cpt; ++q) {
-              const int ti = t * cpt + q;
+        }
+        if (t < p.NTp_cap) {
+          for (int q = 0; q < cpt; ++q) {
+            const int slot = __shfl_sync(0xffffffffu, my_slot, q);
+            if (lane == 0) {
               int rk = p.pool_rows, rv = p.pool_rows;  // out of bounds -> zero fill
-              if (ti < n_kept) {
-                const int slot = p.kept_slots[ti];
+              if (slot >= 0) {
                 rk = ((slot * 2 + 0) * p.g.Hkv + kvh) * p.g.c;
                 rv = ((slot * 2 + 1) * p.g.Hkv + kvh) * p.g.c;
               }
@@ -171,15 +179,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::tma_load_2d(vb + off, &tmPool, &kv_full[st], 0, rv);
               ptx::tma_load_2d(vb + kKVBytes / 4 + off, &tmPool, &kv_full[st], 64, rv);
             }
-          } else {
-            const int ts0 = (t - p.NTp_cap) * BN;
-            ptx::tma_load_3d(kb, &tmKs, &kv_full[st], 0, kvh, ts0);
-            ptx::tma_load_3d(kb + kKVBytes / 4, &tmKs, &kv_full[st], 64, kvh, ts0);
-            ptx::tma_load_3d(vb, &tmVs, &kv_full[st], 0, kvh, ts0);
-            ptx::tma_load_3d(vb + kKVBytes / 4, &tmVs, &kv_full[st], 64, kvh, ts0);
           }
-          ++kvcount;
+        } else if (lane == 0) {
+          const int ts0 = (t - p.NTp_cap) * BN;
+          ptx::tma_load_3d(kb, &tmKs, &kv_full[st], 0, kvh, ts0);
+          ptx::tma_load_3d(kb + kKVBytes / 4, &tmKs, &kv_full[st], 64, kvh, ts0);
+          ptx::tma_load_3d(vb, &tmVs, &kv_full[st], 0, kvh, ts0);
+          ptx::tma_load_3d(vb + kKVBytes / 4, &tmVs, &kv_full[st], 64, kvh, ts0);
         }
+        __syncwarp();
+        ++kvcount;
       }
     }
   } else if (warp == 1) {

@@ -35,6 +35,7 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
   __shared__ SelectSmem ss;
   __shared__ int s_hits, s_spec_used;
   const int n_ids = n_ids_dev ? *n_ids_dev : n_ids_host;
+  if (out.epoch_dev) epoch = *out.epoch_dev;
   int32_t* miss = scratch;            // [n_ids]
   int32_t* freel = scratch + n_ids;   // [P]
   int32_t* vict = freel + cl.P;       // [P]
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
     n_free += tot;
   }
   // 3. victims: the `need` lowest (S, j) evictable residents
-  const int need = n_miss - n_free;
+  int need = n_miss - n_free;
   int n_vict = 0;
   if (need > 0) {
     auto key = [&](int s) -> uint64_t {
@@ -82,7 +83,20 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
       const float S = cl.I[j] * (float)cl.F[j];
       return ~(((uint64_t)__float_as_uint(S) << 32) | (uint64_t)(uint32_t)j);
     };
-    const uint64_t T = block_kth_largest<NT>(key, cl.P, need, ss);
+    // capacity guard (cannot trigger when P >= k + quota; kept as a loud failure, not a crash)
+    int n_evictable = 0;
+    for (int b = 0; b < cl.P; b += NT) {
+      const int s = b + threadIdx.x;
+      int tot;
+      block_excl_scan<NT>((s < cl.P && key(s) != 0ull) ? 1 : 0, tot, ss);
+      n_evictable += tot;
+    }
+    if (need > n_evictable) {
+      if (threadIdx.x == 0 && out.stats) out.stats[15] = 1;
+      need = n_evictable;
+      n_miss = n_free + need;
+    }
+    const uint64_t T = need > 0 ? block_kth_largest<NT>(key, cl.P, need, ss) : ~0ull;
     for (int b = 0; b < cl.P; b += NT) {
       const int s = b + threadIdx.x;
       uint64_t kv = 0ull;
@@ -116,6 +130,12 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
   __syncthreads();
   if (out.kept_slots)
     for (int t = threadIdx.x; t < n_ids; t += NT) out.kept_slots[t] = cl.slot_of[ids[t]];
+  if (out.upd_A)  // A9: after the victims were chosen with the old S
+    for (int t = threadIdx.x; t < n_ids; t += NT) {
+      const int j = ids[t];
+      cl.I[j] += out.upd_A[j];
+      cl.F[j] += 1;
+    }
   if (threadIdx.x == 0) {
     *out.n_load = n_miss;
     if (out.counts) {
@@ -221,7 +241,14 @@ __global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict
   }
 }
 
+__global__ void epoch_inc_kernel(int32_t* e) { *e += 1; }
+
 }  // namespace
+
+cudaError_t launch_epoch_inc(int32_t* epoch_dev, cudaStream_t st) {
+  epoch_inc_kernel<<<1, 1, 0, st>>>(epoch_dev);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t*,

@@ -117,8 +117,12 @@ cudaError_t launch_score_simt(const LayerGeom& g, const T* q, const T* probe_lay
   if (g.d % 4 != 0 || g.d > 128) return cudaErrorNotSupported;
   size_t smem = sizeof(float) * ((size_t)g.d * RB + (size_t)g.d * KB + (size_t)RB * (KB + 1));
   auto kfn = score_simt_kernel<T>;
-  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  static int attr_done = 0;  // per template instance; set before any graph capture
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, 48 * 1024 * 4);
+    if (e != cudaSuccess) return e;
+    attr_done = 1;
+  }
   dim3 grid((g.R + RB - 1) / RB, nsplit, g.Hkv);
   kfn<<<grid, NT, smem, st>>>(g, q, probe_layer, lam2, lampart, nsplit);
   return cudaGetLastError();

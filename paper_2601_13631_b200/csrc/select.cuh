@@ -7,7 +7,7 @@ namespace ckv {
 struct SelectSmem {
   int hist[256];
   int warp_tot[32];
-  int state[2];
+  int state[3];
 };
 
 // Exclusive prefix sum of v over the block (threadIdx order); *tot = block total.
@@ -77,6 +77,7 @@ __device__ uint64_t block_kth_largest(KeyFn key, int n, int k, SelectSmem& ss) {
           if (cum + cnt[j] >= krem) {
             ss.state[0] = 255 - 8 * lane - j;
             ss.state[1] = krem - cum;
+            ss.state[2] = (cnt[j] == krem - cum);  // the whole bin is taken: threshold found
             break;
           }
           cum += cnt[j];
@@ -87,7 +88,10 @@ __device__ uint64_t block_kth_largest(KeyFn key, int n, int k, SelectSmem& ss) {
     prefix |= (uint64_t)ss.state[0] << shift;
     mask |= (uint64_t)255u << shift;
     krem = ss.state[1];
+    const bool done = ss.state[2] != 0;
     __syncthreads();
+    // every key of the chosen bin is selected: keys >= prefix (low digits 0) are exactly k
+    if (done) break;
   }
   return prefix;
 }

@@ -8,7 +8,7 @@ from tests.gpu_util import make_ctx, run_layers, check_layer
 cfg = CONFIGS["c3_7b"].replace(num_layers=1, prefix_len=4096, suffix_len=32)
 k = O.budget_chunks(cfg.prefix_len, cfg.chunk_size, cfg.budget_bp)
 ctx, prefix = make_ctx(cfg)
-print("score kernel kind", ctx.score_kernel_kind, flush=True)
+print("score kernel kind", ctx.score_kernel_kind, "attn kind", ctx.attn_kernel_kind, flush=True)
 t = time.time()
 r = run_layers(ctx, cfg, prefix, [0])[0]
 print("ran in", time.time() - t, flush=True)

@@ -130,6 +130,44 @@ def test_tensor_core_paths_vs_oracle_shapes(c, ns, k):
     check_layer(rb["ids"], rb["out"], rb["A"], rb["qs"], rb["ks"], rb["vs"], *prefix[0], cfg, k)
 
 
+def test_cuda_graph_replay_matches_eager():
+    """A whole multi-layer request captured in a CUDA graph (side-stream prefetch included)
+    replays to the same ids and outputs as eager calls, across requests and cache states."""
+    cfg = C2_SMALL.replace(num_layers=3, prefix_len=4096)
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg, prefetch=k)
+    reqs = []
+    for r in range(3):
+        reqs.append([[to_dev(x, torch.bfloat16) for x in make_request(cfg, l, r)] for l in range(cfg.num_layers)])
+    outs = [torch.empty(cfg.suffix_len, cfg.num_q_heads, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
+            for _ in range(cfg.num_layers)]
+    ids = [torch.empty(k, dtype=torch.int32, device="cuda") for _ in range(cfg.num_layers)]
+
+    def step(r):
+        for l in range(cfg.num_layers):
+            ctx.reprefill_layer(l, *reqs[r][l], out=outs[l], ids=ids[l])
+
+    eager = []
+    for r in range(3):
+        step(r)
+        torch.cuda.synchronize()
+        eager.append(([o.clone() for o in outs], [i.clone() for i in ids]))
+    graphs = []
+    for r in range(3):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step(r)
+        graphs.append(g)
+    for rep in range(3):
+        for r in (2, 0, 1):
+            graphs[r].replay()
+            torch.cuda.synchronize()
+            for l in range(cfg.num_layers):
+                assert torch.equal(ids[l], eager[r][1][l])
+                assert torch.equal(outs[l], eager[r][0][l])
+    ctx.get_stats()  # raises if the planner ever saw a cache overflow
+
+
 # ---------------------------------------------------------------- top-k (bit exact)
 @pytest.mark.parametrize("m", [1, 7, 300, 2048, 32768])
 def test_topk_exact_with_ties(m):
