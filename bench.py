@@ -6,7 +6,7 @@
 Workload (config.workload): Qwen2.5-7B shape, 28 layers, 28 Q / 4 KV heads, d = 128,
 32K-token prefix, chunk 16, 128-token suffix, 10% budget (k = 204), bf16, inter-layer
 speculative prefetch on (quota k), HBM chunk cache of 2k + quota slots per layer,
-R = 4 distinct requests cycling over the shared prefix (synthetic, seed 42).
+R = 8 distinct requests cycling over the shared prefix (synthetic, seed 42).
 A step = one request's Re-Prefill over all 28 layers (A1-A9 each layer).
 value = effective KV GB/s = (probe-K + kept K+V + suffix K+V bytes per layer) x layers
         / step time; us_per_layer is reported beside it.
@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 CFG_NAME = "c3_7b"
-N_REQUESTS = 4
+N_REQUESTS = 8
 
 
 def load_peaks():
@@ -64,10 +64,13 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:  # sampler running before timing
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -77,6 +80,10 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        n = len(self.lines)
+        t0 = time.time()
+        while len(self.lines) < n + 2 and time.time() - t0 < 1.0:  # one sample past the region
+            time.sleep(0.01)
         if self.proc:
             self.proc.terminate()
             try:

@@ -94,9 +94,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* qbuf = smem;
   uint8_t* kvbuf0 = smem + kQBytes;
   uint8_t* pbuf = kvbuf0 + 2 * kKVBytes;
-  float* red_m = reinterpret_cast<float*>(pbuf + kPBytes);  // [2][128]
-  float* red_l = red_m + 256;                                // [2][128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(red_l + 256);
+  __shared__ float red_m[256], red_l[256];  // [2 warps of a quadrant][128 rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + kPBytes);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
   uint64_t* kv_full = bars + 2;   // [2]
@@ -152,6 +151,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int yq = kvh * p.R_pad + mt * BM;
         ptx::tma_load_2d(qbuf, &tmQ, q_full, 0, yq);
         ptx::tma_load_2d(qbuf + kQBytes / 2, &tmQ, q_full, 64, yq);
+      }
+      {  // warm L2 with every kept chunk of this item at once: the per-tile TMA loads then
+         // see L2 latency instead of a serial chain of HBM round trips
+        const int c_beg = min(tl.t0, p.NTp_cap) * cpt, c_end = min(min(tl.t1, p.NTp_cap) * cpt, n_kept);
+        for (int ti = c_beg + lane; ti < c_end; ti += 32) {
+          const int slot = p.kept_slots[ti];
+          const int rk = ((slot * 2 + 0) * p.g.Hkv + kvh) * p.g.c;
+          const int rv = ((slot * 2 + 1) * p.g.Hkv + kvh) * p.g.c;
+          ptx::prefetch_tma_2d_l2(&tmPool, 0, rk);
+          ptx::prefetch_tma_2d_l2(&tmPool, 64, rk);
+          ptx::prefetch_tma_2d_l2(&tmPool, 0, rv);
+          ptx::prefetch_tma_2d_l2(&tmPool, 64, rv);
+        }
+        __syncwarp();
       }
       for (int t = tl.t0; t < tl.t1; ++t) {
         if (!tile_present(p, tl, t)) continue;
@@ -257,49 +270,67 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sb = scount & 1;
         ptx::mbar_wait(&s_full[sb], (scount >> 1) & 1);
         ptx::tc_fence_after();
-        float x[64];
-        ptx::tmem_ld32p(tmem + sb * BN + h * 64 + lane_off, x);
-        ptx::tmem_ld32p(tmem + sb * BN + h * 64 + 32 + lane_off, x + 32);
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
-        ++scount;
-        // mask + scale (log2 units)
-        const int col0 = h * 64;
-        if (t < p.NTp_cap) {
-          const int kbase = t * BN + col0;
-          if (kbase + 64 > n_valid_prefix) {
+        // S columns of this warp: pass 1 = masked max, pass 2 = P (re-read from TMEM, so only
+        // 32 logits are live at a time)
+        const uint32_t s_addr = tmem + sb * BN + h * 64 + lane_off;
+        const bool pre = t < p.NTp_cap;
+        const int base = (pre ? t * BN : (t - p.NTp_cap) * BN) + h * 64;
+        const int lim = pre ? n_valid_prefix : min(r + 1, p.g.ns);  // key valid iff index < lim
+        float tmax = -INFINITY;
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          float x[32];
+          ptx::tmem_ld32p(s_addr + hh * 32, x);
+          const int b0 = base + hh * 32;
+          if (b0 + 32 > lim) {
 #pragma unroll
-            for (int i = 0; i < 64; ++i)
-              if (kbase + i >= n_valid_prefix) x[i] = -INFINITY;
+            for (int i = 0; i < 32; ++i)
+              if (b0 + i >= lim) x[i] = -INFINITY;
           }
-        } else {
-          const int tbase = (t - p.NTp_cap) * BN + col0;
 #pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (tbase + i > r || tbase + i >= p.g.ns) x[i] = -INFINITY;
-        }
-        float mx[8];
+          for (int n = 16; n >= 1; n >>= 1)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          mx[i] = fmaxf(fmaxf(fmaxf(x[8 * i], x[8 * i + 1]), fmaxf(x[8 * i + 2], x[8 * i + 3])),
-                        fmaxf(fmaxf(x[8 * i + 4], x[8 * i + 5]), fmaxf(x[8 * i + 6], x[8 * i + 7])));
+            for (int i = 0; i < n; ++i) x[i] = fmaxf(x[i], x[i + n]);
+          tmax = fmaxf(tmax, x[0]);
         }
-        float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
         red_m[h * 128 + rit] = tmax;
         ptx::named_bar_sync(bar_id, 64);
         tmax = fmaxf(red_m[rit], red_m[128 + rit]) * sc;
         ptx::named_bar_sync(bar_id, 64);  // red_m reusable
         const float m_new = fmaxf(m_ref, tmax);
         const bool resc = (j > 0) && (m_ref != -INFINITY) && (m_new > m_ref + kRescaleThresh);
-        if (j == 0 || m_ref == -INFINITY) {
-          m_ref = m_new;
+        const float f = resc ? fast_exp2(m_ref - m_new) : 1.f;
+        if (j == 0 || m_ref == -INFINITY || resc) m_ref = m_new;
+        const float msub = (m_ref == -INFINITY) ? 0.f : m_ref;
+        float lsum = 0.f;
+        uint32_t pk[32];
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          float x[32];
+          ptx::tmem_ld32p(s_addr + hh * 32, x);
+          const int b0 = base + hh * 32;
+          if (b0 + 32 > lim) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (b0 + i >= lim) x[i] = -INFINITY;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = fast_exp2(fmaf(x[2 * i], sc, -msub));
+            const float p1 = fast_exp2(fmaf(x[2 * i + 1], sc, -msub));
+            lsum += p0 + p1;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+            pk[hh * 16 + i] = *reinterpret_cast<uint32_t*>(&b2);
+          }
         }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
+        ++scount;
         if (__any_sync(0xffffffffu, resc)) {
-          // O must hold PV(j-1) before it is rescaled
+          // lazy rescale: O must hold PV(j-1) before it is multiplied by 2^(m_old - m_new)
           ptx::mbar_wait(p_empty, (pcount - 1) & 1);
           ptx::tc_fence_after();
-          const float f = resc ? fast_exp2(m_ref - m_new) : 1.f;
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
             float o[32];
@@ -309,29 +340,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) o[i] *= f;
             ptx::tmem_st32(ta, o);
           }
-          l *= f;
-          if (resc) m_ref = m_new;
         }
-        const float msub = (m_ref == -INFINITY) ? 0.f : m_ref;
-        float lsum = 0.f;
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float p0 = fast_exp2(fmaf(x[2 * i], sc, -msub));
-          const float p1 = fast_exp2(fmaf(x[2 * i + 1], sc, -msub));
-          lsum += p0 + p1;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
-        }
-        l += lsum;
+        l = l * f + lsum;
         // P buffer free (PV(j-1) done reading it)?
         ptx::mbar_wait(p_empty, (pcount & 1) ^ 1);
-        uint8_t* prow = pbuf + h * (kPBytes / 2) + rit * 128;
+        const uint32_t prow = ptx::smem_u32(pbuf) + h * (kPBytes / 2) + rit * 128;
 #pragma unroll
         for (int c16 = 0; c16 < 8; ++c16) {
-          const int phys = c16 ^ (rit & 7);
-          *reinterpret_cast<uint4*>(prow + phys * 16) =
-              make_uint4(pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]);
+          const uint32_t phys = (uint32_t)(c16 ^ (rit & 7));
+          ptx::st_shared_v4(prow + phys * 16, pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]);
         }
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();

@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU round: quick tcgen05 check, GPU tests, smoke, bench, ncu launch list + full capture.
+# One GPU round: quick tcgen05 check, GPU tests, smoke, bench; optional ncu launch list + full captures.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 120 python scripts/quick_tc.py > gpurun_out/quick.log 2>&1 || { echo "quick failed"; tail -20 gpurun_out/quick.log; exit 1; }
@@ -7,10 +7,12 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1
 timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1
 if [ "$1" == "ncu" ]; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 1200 -c 400 --csv \
-     --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:score_tc -s 40 -c 1 \
-     -o gpurun_out/score_tc python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 1300 -c 400 --csv \
+     --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu --no-graph > gpurun_out/ncu_launch.log 2>&1
+  for K in score_tc attn_tc; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 40 -c 1 \
+       -o gpurun_out/$K python bench.py --steps 1 --warmup 3 --no-cpu --no-graph > gpurun_out/ncu_$K.log 2>&1
+  done
 fi
-tail -3 gpurun_out/quick.log gpurun_out/pytest_gpu.log gpurun_out/smoke.log
+tail -n 3 gpurun_out/quick.log gpurun_out/pytest_gpu.log gpurun_out/smoke.log
 tail -c 600 gpurun_out/bench.log
