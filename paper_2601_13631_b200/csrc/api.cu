@@ -30,6 +30,7 @@ struct ckv_ctx {
   int64_t rec_elems = 0, rec_bytes = 0;
   int nsplit_score_max = 1, nsplit_attn_max = 1;
   int score_kind = 0;  // 0 SIMT, 1 tcgen05
+  int rec_swz = 0;     // chunk-record layout (rec_elem)
   int attn_kind = 0;   // 0 SIMT, 1 tcgen05
 
   void* probe = nullptr;
@@ -135,6 +136,7 @@ LayerGeom geom(const ckv_ctx* ctx, int ns) {
   g.m_loc = ctx->m_loc;
   g.n_loc = ctx->n_loc;
   g.n_pad = ctx->n_pad;
+  g.rec_swz = ctx->rec_swz;
   return g;
 }
 
@@ -378,6 +380,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   ctx->max_ns = c.max_suffix_len;
   ctx->rec_elems = (int64_t)2 * ctx->Hkv * ctx->c * ctx->d;
   ctx->rec_bytes = ctx->rec_elems * ctx->esz;
+  ctx->rec_swz = (ctx->dtype == CKV_BF16 && ctx->d == 128) ? 1 : 0;
 
   ckv_status st = CKV_OK;
   auto cudafail = [&](cudaError_t e, const char* what) {
@@ -505,12 +508,12 @@ ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const vo
     LK(launch_pack_probe<float>(static_cast<const float*>(kd), ctx->t0, ctx->n_loc, ctx->n_pad, ctx->Hkv, ctx->d,
                                 static_cast<float*>(probe_l), st));
     LK(launch_pack_records<float>(static_cast<const float*>(kd), static_cast<const float*>(vd), ctx->t0, ctx->n_loc,
-                                  ctx->m_loc, ctx->c, ctx->Hkv, ctx->d, static_cast<float*>(staging), st));
+                                  ctx->m_loc, ctx->c, ctx->Hkv, ctx->d, ctx->rec_swz, static_cast<float*>(staging), st));
   } else {
     LK(launch_pack_probe<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(kd), ctx->t0, ctx->n_loc, ctx->n_pad,
                                         ctx->Hkv, ctx->d, static_cast<__nv_bfloat16*>(probe_l), st));
     LK(launch_pack_records<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(kd), static_cast<const __nv_bfloat16*>(vd),
-                                          ctx->t0, ctx->n_loc, ctx->m_loc, ctx->c, ctx->Hkv, ctx->d,
+                                          ctx->t0, ctx->n_loc, ctx->m_loc, ctx->c, ctx->Hkv, ctx->d, ctx->rec_swz,
                                           static_cast<__nv_bfloat16*>(staging), st));
   }
   CK(cudaMemcpyAsync(ctx->host_store + (size_t)layer * stage_bytes, staging, stage_bytes, cudaMemcpyDeviceToHost, st));

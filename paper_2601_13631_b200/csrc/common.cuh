@@ -37,7 +37,20 @@ struct LayerGeom {
   int m_loc;       // local chunks
   int n_loc;       // local prefix tokens
   int n_pad;       // probe-key row stride per KV head
+  int rec_swz;     // chunk-record layout: 0 plain, 1 swizzled (see rec_elem)
 };
+
+// Element offset inside one chunk record (one HBM slot / one host-store record).
+//  plain    [K|V][Hkv][c][d]
+//  swizzled (bf16, d = 128): [Hkv][K|V][half][c][64] with each 128-byte row's 16-byte units
+//           XOR-swizzled by (row & 7) -- the exact shared-memory image the tcgen05 attention
+//           consumes, so one (chunk, kv head) K+V block is a single contiguous bulk copy.
+__host__ __device__ __forceinline__ int64_t rec_elem(int swz, int kv, int kvh, int p, int x, int Hkv, int c, int d) {
+  if (!swz) return (((int64_t)kv * Hkv + kvh) * c + p) * d + x;
+  const int half = x >> 6, xi = x & 63;
+  const int u = (xi >> 3) ^ (p & 7);
+  return ((((int64_t)kvh * 2 + kv) * 2 + half) * c + p) * 64 + u * 8 + (xi & 7);
+}
 
 // ---- launchers (defined in the k_*.cu files) ----
 // A1 SIMT: lam2[kvh][m_loc][R] = log2 sum_{i in chunk} 2^(l_i log2e), lampart[kvh][split][R]
@@ -95,7 +108,7 @@ cudaError_t launch_pack_probe(const T* k, int64_t t0, int n_loc, int n_pad, int 
                               cudaStream_t st);
 template <typename T>
 cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int n_loc, int m_loc, int c, int Hkv,
-                                int d, T* staging, cudaStream_t st);
+                                int d, int swz, T* staging, cudaStream_t st);
 // A7 / A8
 template <typename T>
 cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, const T* v_suf,

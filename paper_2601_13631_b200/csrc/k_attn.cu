@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(NT) attn_simt_kernel(LayerGeom g, const T* __r
       if (p < npre) {
         const int t = t0 + p / g.c, off = p % g.c;
         const T* rec = pool + (int64_t)kept_slots[t] * rec_elems;
-        kv = to_f(rec[((int64_t)kvh * g.c + off) * d + x]);
-        vv = to_f(rec[((int64_t)(g.Hkv + kvh) * g.c + off) * d + x]);
+        kv = to_f(rec[rec_elem(g.rec_swz, 0, kvh, off, x, g.Hkv, g.c, d)]);
+        vv = to_f(rec[rec_elem(g.rec_swz, 1, kvh, off, x, g.Hkv, g.c, d)]);
       } else if (p < nkeys) {
         const int ts = p - npre;
         kv = to_f(ks[((int64_t)ts * g.Hkv + kvh) * d + x]);

@@ -18,6 +18,9 @@
 //               and 64 O columns each); row max exchanged through shared memory; lazy O rescale
 //               (only when the running max grows by > 8 in log2 units) via tcgen05.ld/st;
 //               P = 2^(s - m) written as bf16 in the 128-byte-swizzled K-major layout.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -43,12 +46,23 @@ struct AttnParams {
   int nsplit;
   int MT, R_pad;
   int NTp_cap, NTs, T_cap;
-  int pool_rows;
+  const char* pool;      // this layer's slot pool (swizzled records, rec_elem)
+  int64_t rec_bytes;
+  uint32_t chunk_bytes;  // one (chunk, kv head) K+V block = 4 * c * 128 bytes
   int n_items;
   float scale;
   float* o_part;
   float* lse_part;
+  unsigned long long* trace;  // debug: per-event %globaltimer of CTA 0 (CKV_ATTN_TRACE=1), else null
 };
+
+__device__ __forceinline__ void trace_ev(const AttnParams& p, int ev, int i) {
+  if (p.trace && blockIdx.x == 0 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[ev * 64 + i] = t;
+  }
+}
 
 struct Tiles {
   int t0, t1;  // [t0, t1) in the tile index space of the item's KV head
@@ -67,19 +81,38 @@ __device__ __forceinline__ bool tile_present(const AttnParams& p, const Tiles& t
   return (t < p.NTp_cap) ? (t < tl.NTp) : (p.include_suffix != 0);
 }
 
-// O += P V for the tile that was scored one step earlier (MMA thread).
-__device__ __forceinline__ void issue_pv(uint32_t tmem_O, uint32_t pa, uint8_t* kvbuf0, uint64_t* p_full,
-                                         uint64_t* p_empty, uint64_t* o_empty, uint64_t* kv_empty, uint32_t idesc_o,
-                                         int jj, int stage, int icount, int& pcount) {
+// O += P V for the tile that was scored one step earlier (MMA thread).  Prefix tiles hold
+// `nv` chunk blocks [K h0|K h1|V h0|V h1] of c rows each; suffix tiles hold [K h0|K h1|V h0|V h1]
+// of 128 rows each.  V is the MN-major B operand (d contiguous), P the K-major A operand.
+__device__ __forceinline__ void issue_pv(const AttnParams& p, uint32_t tmem_O, uint32_t pa, uint8_t* kvbuf0,
+                                         uint64_t* p_full, uint64_t* p_empty, uint64_t* o_empty, uint64_t* kv_empty,
+                                         uint32_t idesc_o, int jj, int stage, bool prefix, int nv, int icount,
+                                         int& pcount) {
   ptx::mbar_wait(p_full, pcount & 1);
   if (jj == 0) ptx::mbar_wait(o_empty, (icount & 1) ^ 1);
   ptx::tc_fence_after();
-  const uint32_t va = ptx::smem_u32(kvbuf0 + stage * kKVBytes + kKVBytes / 2);
+  const uint32_t sa = ptx::smem_u32(kvbuf0 + stage * kKVBytes);
+  uint32_t acc = jj > 0 ? 1u : 0u;
+  if (prefix) {
+    const int c = p.g.c;
+    for (int q = 0; q < nv; ++q) {
+      const uint32_t vbase = sa + q * p.chunk_bytes + 2 * c * 128;
+      for (int s16 = 0; s16 < c / 16; ++s16) {
+        const int kk = q * c + s16 * 16;  // key index inside the tile
+        const uint64_t adesc = ptx::umma_desc_sw128(pa + (kk >> 6) * (kPBytes / 2) + ((kk & 63) >> 4) * 32);
+        const uint64_t bdesc = ptx::umma_desc_sw128_mn(vbase + s16 * 16 * 128, c * 128);
+        ptx::mma_bf16(tmem_O, adesc, bdesc, idesc_o, acc);
+        acc = 1u;
+      }
+    }
+  } else {
 #pragma unroll
-  for (int k = 0; k < BN / 16; ++k) {
-    const uint64_t adesc = ptx::umma_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32);
-    const uint64_t bdesc = ptx::umma_desc_sw128_mn(va + k * 16 * 128, kKVBytes / 4);
-    ptx::mma_bf16(tmem_O, adesc, bdesc, idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
+    for (int k = 0; k < BN / 16; ++k) {
+      const uint64_t adesc = ptx::umma_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32);
+      const uint64_t bdesc = ptx::umma_desc_sw128_mn(sa + kKVBytes / 2 + k * 16 * 128, kKVBytes / 4);
+      ptx::mma_bf16(tmem_O, adesc, bdesc, idesc_o, acc);
+      acc = 1u;
+    }
   }
   ptx::mma_commit(p_empty);
   ptx::mma_commit(&kv_empty[stage]);
@@ -87,8 +120,8 @@ __device__ __forceinline__ void issue_pv(uint32_t tmem_O, uint32_t pa, uint8_t* 
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmPool,
-                   const __grid_constant__ CUtensorMap tmKs, const __grid_constant__ CUtensorMap tmVs, AttnParams p) {
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKs,
+                   const __grid_constant__ CUtensorMap tmVs, AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* qbuf = smem;
@@ -110,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_kept = *p.n_kept_dev;
+  if (threadIdx.x == 0) trace_ev(p, 5, 0);
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(q_full, 1);
@@ -138,7 +172,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // lanes fetch the tile's slot ids in parallel, lane 0 issues the copies)
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmQ);
-      ptx::tma_prefetch_desc(&tmPool);
     }
     int icount = 0, kvcount = 0;
     const int cpt = BN / p.g.c;  // chunks per key tile (<= 16)
@@ -152,49 +185,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_load_2d(qbuf, &tmQ, q_full, 0, yq);
         ptx::tma_load_2d(qbuf + kQBytes / 2, &tmQ, q_full, 64, yq);
       }
-      {  // warm L2 with every kept chunk of this item at once: the per-tile TMA loads then
-         // see L2 latency instead of a serial chain of HBM round trips
-        const int c_beg = min(tl.t0, p.NTp_cap) * cpt, c_end = min(min(tl.t1, p.NTp_cap) * cpt, n_kept);
-        for (int ti = c_beg + lane; ti < c_end; ti += 32) {
-          const int slot = p.kept_slots[ti];
-          const int rk = ((slot * 2 + 0) * p.g.Hkv + kvh) * p.g.c;
-          const int rv = ((slot * 2 + 1) * p.g.Hkv + kvh) * p.g.c;
-          ptx::prefetch_tma_2d_l2(&tmPool, 0, rk);
-          ptx::prefetch_tma_2d_l2(&tmPool, 64, rk);
-          ptx::prefetch_tma_2d_l2(&tmPool, 0, rv);
-          ptx::prefetch_tma_2d_l2(&tmPool, 64, rv);
-        }
-        __syncwarp();
-      }
       for (int t = tl.t0; t < tl.t1; ++t) {
         if (!tile_present(p, tl, t)) continue;
         int my_slot = -1;
         if (t < p.NTp_cap && lane < cpt && t * cpt + lane < n_kept) my_slot = p.kept_slots[t * cpt + lane];
         const int st = kvcount & 1;
         uint8_t* kb = kvbuf0 + st * kKVBytes;
-        uint8_t* vb = kb + kKVBytes / 2;
+        const bool prefix = t < p.NTp_cap;
+        const int nv = prefix ? min(cpt, n_kept - t * cpt) : 0;
         if (lane == 0) {
           ptx::mbar_wait(&kv_empty[st], ((kvcount >> 1) & 1) ^ 1);
-          ptx::mbar_expect_tx(&kv_full[st], kKVBytes);
+          ptx::mbar_expect_tx(&kv_full[st], prefix ? nv * p.chunk_bytes : kKVBytes);
+          trace_ev(p, 0, kvcount);
         }
-        if (t < p.NTp_cap) {
-          for (int q = 0; q < cpt; ++q) {
+        if (prefix) {
+          // one contiguous bulk copy per kept chunk: its (kv head) K+V block, already in the
+          // swizzled shared-memory image (rec_elem)
+          for (int q = 0; q < nv; ++q) {
             const int slot = __shfl_sync(0xffffffffu, my_slot, q);
-            if (lane == 0) {
-              int rk = p.pool_rows, rv = p.pool_rows;  // out of bounds -> zero fill
-              if (slot >= 0) {
-                rk = ((slot * 2 + 0) * p.g.Hkv + kvh) * p.g.c;
-                rv = ((slot * 2 + 1) * p.g.Hkv + kvh) * p.g.c;
-              }
-              const uint32_t off = q * p.g.c * 128;
-              ptx::tma_load_2d(kb + off, &tmPool, &kv_full[st], 0, rk);
-              ptx::tma_load_2d(kb + kKVBytes / 4 + off, &tmPool, &kv_full[st], 64, rk);
-              ptx::tma_load_2d(vb + off, &tmPool, &kv_full[st], 0, rv);
-              ptx::tma_load_2d(vb + kKVBytes / 4 + off, &tmPool, &kv_full[st], 64, rv);
-            }
+            if (lane == 0)
+              ptx::bulk_g2s(kb + q * p.chunk_bytes, p.pool + slot * p.rec_bytes + (int64_t)kvh * p.chunk_bytes,
+                            p.chunk_bytes, &kv_full[st]);
           }
         } else if (lane == 0) {
           const int ts0 = (t - p.NTp_cap) * BN;
+          uint8_t* vb = kb + kKVBytes / 2;
           ptx::tma_load_3d(kb, &tmKs, &kv_full[st], 0, kvh, ts0);
           ptx::tma_load_3d(kb + kKVBytes / 4, &tmKs, &kv_full[st], 64, kvh, ts0);
           ptx::tma_load_3d(vb, &tmVs, &kv_full[st], 0, kvh, ts0);
@@ -209,6 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);
       constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(BM, D, true);
+      const uint32_t idesc_sc = ptx::idesc_bf16_f32(BM, p.g.c, false);
+      const int cpt = BN / p.g.c;
       int icount = 0, kvcount = 0, scount = 0, pcount = 0;
       const uint32_t qa = ptx::smem_u32(qbuf);
       const uint32_t pa = ptx::smem_u32(pbuf);
@@ -216,30 +233,55 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sp = it % p.nsplit;
         const Tiles tl = item_tiles(p, sp, n_kept);
         ptx::mbar_wait(q_full, icount & 1);
-        int j = 0, prev_stage = 0;
+        int j = 0, prev_stage = 0, prev_nv = 0;
+        bool prev_prefix = false;
         for (int t = tl.t0; t < tl.t1; ++t) {
           if (!tile_present(p, tl, t)) continue;
           const int st = kvcount & 1;
           ptx::mbar_wait(&kv_full[st], (kvcount >> 1) & 1);
+          trace_ev(p, 1, kvcount);
           const int sb = scount & 1;
           ptx::mbar_wait(&s_empty[sb], ((scount >> 1) & 1) ^ 1);
           ptx::tc_fence_after();
           const uint32_t ka = ptx::smem_u32(kvbuf0 + st * kKVBytes);
+          const bool prefix = t < p.NTp_cap;
+          const int nv = prefix ? min(cpt, n_kept - t * cpt) : 0;
+          if (prefix) {
+            // one N = c MMA chain per chunk block (keys of different chunks are not uniformly strided)
+            for (int q = 0; q < nv; ++q) {
+              const uint32_t kbase = ka + q * p.chunk_bytes;
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
-            const uint32_t off_k = (k >> 2) * (kKVBytes / 4) + (k & 3) * 32;
-            ptx::mma_bf16(tmem + sb * BN, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k),
-                          idesc_s, k > 0 ? 1u : 0u);
+              for (int k = 0; k < D / 16; ++k) {
+                const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+                const uint32_t off_k = (k >> 2) * (p.g.c * 128) + (k & 3) * 32;
+                ptx::mma_bf16(tmem + sb * BN + q * p.g.c, ptx::umma_desc_sw128(qa + off_q),
+                              ptx::umma_desc_sw128(kbase + off_k), idesc_sc, k > 0 ? 1u : 0u);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k) {
+              const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+              const uint32_t off_k = (k >> 2) * (kKVBytes / 4) + (k & 3) * 32;
+              ptx::mma_bf16(tmem + sb * BN, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k),
+                            idesc_s, k > 0 ? 1u : 0u);
+            }
           }
           ptx::mma_commit(&s_full[sb]);
+          trace_ev(p, 2, scount);
           ++scount;
-          if (j > 0) issue_pv(tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, idesc_o, j - 1, prev_stage, icount, pcount);
+          if (j > 0)
+            issue_pv(p, tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, idesc_o, j - 1, prev_stage,
+                     prev_prefix, prev_nv, icount, pcount);
           prev_stage = st;
+          prev_prefix = prefix;
+          prev_nv = nv;
           ++kvcount;
           ++j;
         }
-        if (j > 0) issue_pv(tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, idesc_o, j - 1, prev_stage, icount, pcount);
+        if (j > 0)
+          issue_pv(p, tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, idesc_o, j - 1, prev_stage, prev_prefix,
+                   prev_nv, icount, pcount);
         ptx::mma_commit(q_empty);
         ptx::mma_commit(o_full);
       }
@@ -269,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!tile_present(p, tl, t)) continue;
         const int sb = scount & 1;
         ptx::mbar_wait(&s_full[sb], (scount >> 1) & 1);
+        if (warp == 2 && lane == 0) trace_ev(p, 3, scount);
         ptx::tc_fence_after();
         // S columns of this warp: pass 1 = masked max, pass 2 = P (re-read from TMEM, so only
         // 32 logits are live at a time)
@@ -354,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(p_full);
+        if (warp == 2 && lane == 0) trace_ev(p, 4, pcount);
         ++pcount;
         ++j;
       }
@@ -424,7 +468,8 @@ int sm_count() {
 }  // namespace
 
 bool attn_tc_supported(const LayerGeom& g) {
-  return g.d == D && g.c >= 8 && g.c <= BN && (BN % g.c) == 0;
+  // chunk blocks feed N = c MMAs (M = 128 needs N % 16 == 0) and must tile 128 keys
+  return g.d == D && g.rec_swz == 1 && g.c >= 16 && g.c <= BN && (BN % g.c) == 0;
 }
 
 int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix) {
@@ -455,7 +500,10 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   p.NTp_cap = (k_cap * g.c + BN - 1) / BN;
   p.NTs = (g.ns + BN - 1) / BN;
   p.T_cap = p.NTp_cap + (include_suffix ? p.NTs : 0);
-  p.pool_rows = P_slots * 2 * g.Hkv * g.c;
+  p.pool = reinterpret_cast<const char*>(pool_layer);
+  p.rec_bytes = (int64_t)2 * g.Hkv * g.c * D * 2;
+  p.chunk_bytes = 4u * g.c * 128u;
+  (void)P_slots;
   p.n_items = g.Hkv * p.MT * nsplit;
   p.scale = kLog2e / sqrtf((float)g.d);
   p.o_part = o_part;
@@ -464,9 +512,8 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   pack_q_attn_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  CUtensorMap tmQ, tmPool, tmKs, tmVs;
+  CUtensorMap tmQ, tmKs, tmVs;
   if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_2d(&tmPool, pool_layer, D, (uint64_t)p.pool_rows, (uint32_t)g.c)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_3d(&tmKs, k_suf, D, g.Hkv, g.ns, BN)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_3d(&tmVs, v_suf, D, g.Hkv, g.ns, BN)) return cudaErrorInvalidValue;
   static bool attr = false;
@@ -476,7 +523,28 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
     attr = true;
   }
   const int grid = p.n_items < sm_count() ? p.n_items : sm_count();
-  attn_tc_kernel<<<grid, kThreads, kSmem, st>>>(tmQ, tmPool, tmKs, tmVs, p);
+  static int trace_mode = -1;
+  static unsigned long long* trace_buf = nullptr;
+  if (trace_mode < 0) {
+    const char* ev = getenv("CKV_ATTN_TRACE");
+    trace_mode = (ev && ev[0] == '1') ? 1 : 0;
+    if (trace_mode) cudaMalloc(&trace_buf, 6 * 64 * sizeof(unsigned long long));
+  }
+  p.trace = trace_buf;
+  if (trace_buf) cudaMemsetAsync(trace_buf, 0, 6 * 64 * sizeof(unsigned long long), st);
+  attn_tc_kernel<<<grid, kThreads, kSmem, st>>>(tmQ, tmKs, tmVs, p);
+  if (trace_buf) {  // debug only: synchronous dump of CTA 0's event times (ns since kernel start)
+    unsigned long long h[6 * 64];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost);
+    const unsigned long long t0 = h[5 * 64];
+    const char* nm[5] = {"tma_issue", "kv_full", "s_commit", "s_full@sm", "p_full@sm"};
+    for (int e = 0; e < 5; ++e) {
+      fprintf(stderr, "[attn trace] %-10s", nm[e]);
+      for (int i = 0; i < 12; ++i) fprintf(stderr, " %7.2f", h[e * 64 + i] ? (h[e * 64 + i] - t0) * 1e-3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+  }
   return cudaGetLastError();
 }
 

@@ -223,8 +223,8 @@ __global__ void pack_probe_kernel(const T* __restrict__ k, int64_t t0, int n_loc
 
 template <typename T>
 __global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t t0, int n_loc,
-                                    int m_loc, int c, int Hkv, int d, T* __restrict__ rec) {
-  // rec[j][kv][kvh][p][x], zero padding past n_loc
+                                    int m_loc, int c, int Hkv, int d, int swz, T* __restrict__ rec) {
+  // one record per chunk j (layout: rec_elem), zero padding past n_loc
   const int64_t per = (int64_t)2 * Hkv * c * d;
   const int64_t total = (int64_t)m_loc * per;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -237,7 +237,7 @@ __global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict
     const int64_t i = (int64_t)j * c + p;
     T val = from_f<T>(0.f);
     if (i < n_loc) val = (kv == 0 ? k : v)[((t0 + i) * Hkv + kvh) * d + x];
-    rec[e] = val;
+    rec[(int64_t)j * per + rec_elem(swz, kv, kvh, p, x, Hkv, c, d)] = val;
   }
 }
 
@@ -278,16 +278,16 @@ cudaError_t launch_pack_probe(const T* k, int64_t t0, int n_loc, int n_pad, int 
 }
 template <typename T>
 cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int n_loc, int m_loc, int c, int Hkv, int d,
-                                T* staging, cudaStream_t st) {
-  pack_records_kernel<T><<<1184, 256, 0, st>>>(k, v, t0, n_loc, m_loc, c, Hkv, d, staging);
+                                int swz, T* staging, cudaStream_t st) {
+  pack_records_kernel<T><<<1184, 256, 0, st>>>(k, v, t0, n_loc, m_loc, c, Hkv, d, swz, staging);
   return cudaGetLastError();
 }
 template cudaError_t launch_pack_probe<float>(const float*, int64_t, int, int, int, int, float*, cudaStream_t);
 template cudaError_t launch_pack_probe<__nv_bfloat16>(const __nv_bfloat16*, int64_t, int, int, int, int,
                                                       __nv_bfloat16*, cudaStream_t);
-template cudaError_t launch_pack_records<float>(const float*, const float*, int64_t, int, int, int, int, int, float*,
-                                                cudaStream_t);
+template cudaError_t launch_pack_records<float>(const float*, const float*, int64_t, int, int, int, int, int, int,
+                                                float*, cudaStream_t);
 template cudaError_t launch_pack_records<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, int64_t, int,
-                                                        int, int, int, int, __nv_bfloat16*, cudaStream_t);
+                                                        int, int, int, int, int, __nv_bfloat16*, cudaStream_t);
 
 }  // namespace ckv
