@@ -93,26 +93,12 @@ __device__ __forceinline__ void issue_pv(const AttnParams& p, uint32_t tmem_O, u
   ptx::tc_fence_after();
   const uint32_t sa = ptx::smem_u32(kvbuf0 + stage * kKVBytes);
   uint32_t acc = jj > 0 ? 1u : 0u;
-  if (prefix) {
-    const int c = p.g.c;
-    for (int q = 0; q < nv; ++q) {
-      const uint32_t vbase = sa + q * p.chunk_bytes + 2 * c * 128;
-      for (int s16 = 0; s16 < c / 16; ++s16) {
-        const int kk = q * c + s16 * 16;  // key index inside the tile
-        const uint64_t adesc = ptx::umma_desc_sw128(pa + (kk >> 6) * (kPBytes / 2) + ((kk & 63) >> 4) * 32);
-        const uint64_t bdesc = ptx::umma_desc_sw128_mn(vbase + s16 * 16 * 128, c * 128);
-        ptx::mma_bf16(tmem_O, adesc, bdesc, idesc_o, acc);
-        acc = 1u;
-      }
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < BN / 16; ++k) {
-      const uint64_t adesc = ptx::umma_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32);
-      const uint64_t bdesc = ptx::umma_desc_sw128_mn(sa + kKVBytes / 2 + k * 16 * 128, kKVBytes / 4);
-      ptx::mma_bf16(tmem_O, adesc, bdesc, idesc_o, acc);
-      acc = 1u;
-    }
+  const int ksteps = prefix ? (nv * p.g.c + 15) / 16 : BN / 16;  // keys of absent chunks are skipped
+  for (int k = 0; k < ksteps; ++k) {
+    const uint64_t adesc = ptx::umma_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32);
+    const uint64_t bdesc = ptx::umma_desc_sw128_mn(sa + kKVBytes / 2 + k * 16 * 128, kKVBytes / 4);
+    ptx::mma_bf16(tmem_O, adesc, bdesc, idesc_o, acc);
+    acc = 1u;
   }
   ptx::mma_commit(p_empty);
   ptx::mma_commit(&kv_empty[stage]);
@@ -193,19 +179,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* kb = kvbuf0 + st * kKVBytes;
         const bool prefix = t < p.NTp_cap;
         const int nv = prefix ? min(cpt, n_kept - t * cpt) : 0;
+        // c = 8 with an odd chunk count: the last 16-key MMA step also spans the next (absent)
+        // chunk position, so fill it with a duplicate (finite V; its P is masked to 0)
+        const int ncopy = (prefix && (nv * p.g.c) % 16) ? nv + 1 : nv;
         if (lane == 0) {
           ptx::mbar_wait(&kv_empty[st], ((kvcount >> 1) & 1) ^ 1);
-          ptx::mbar_expect_tx(&kv_full[st], prefix ? nv * p.chunk_bytes : kKVBytes);
+          ptx::mbar_expect_tx(&kv_full[st], prefix ? ncopy * p.chunk_bytes : kKVBytes);
           trace_ev(p, 0, kvcount);
         }
         if (prefix) {
-          // one contiguous bulk copy per kept chunk: its (kv head) K+V block, already in the
-          // swizzled shared-memory image (rec_elem)
-          for (int q = 0; q < nv; ++q) {
-            const int slot = __shfl_sync(0xffffffffu, my_slot, q);
-            if (lane == 0)
-              ptx::bulk_g2s(kb + q * p.chunk_bytes, p.pool + slot * p.rec_bytes + (int64_t)kvh * p.chunk_bytes,
-                            p.chunk_bytes, &kv_full[st]);
+          // four contiguous bulk copies per kept chunk: its (kv head) K and V halves, already in
+          // the swizzled shared-memory image (rec_elem), land at rows [q c, (q+1) c) of the
+          // [half][128 keys][128 B] K and V tiles
+          const uint32_t hb = p.g.c * 128u;  // bytes of one (K|V, half) block
+          for (int q = 0; q < ncopy; ++q) {
+            const int slot = __shfl_sync(0xffffffffu, my_slot, q < nv ? q : nv - 1);
+            if (lane == 0) {
+              const char* src = p.pool + slot * p.rec_bytes + (int64_t)kvh * p.chunk_bytes;
+              uint8_t* dst = kb + q * hb;
+              ptx::bulk_g2s(dst, src, hb, &kv_full[st]);
+              ptx::bulk_g2s(dst + kKVBytes / 4, src + hb, hb, &kv_full[st]);
+              ptx::bulk_g2s(dst + kKVBytes / 2, src + 2 * hb, hb, &kv_full[st]);
+              ptx::bulk_g2s(dst + 3 * (kKVBytes / 4), src + 3 * hb, hb, &kv_full[st]);
+            }
           }
         } else if (lane == 0) {
           const int ts0 = (t - p.NTp_cap) * BN;
@@ -224,7 +220,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);
       constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(BM, D, true);
-      const uint32_t idesc_sc = ptx::idesc_bf16_f32(BM, p.g.c, false);
       const int cpt = BN / p.g.c;
       int icount = 0, kvcount = 0, scount = 0, pcount = 0;
       const uint32_t qa = ptx::smem_u32(qbuf);
@@ -246,26 +241,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t ka = ptx::smem_u32(kvbuf0 + st * kKVBytes);
           const bool prefix = t < p.NTp_cap;
           const int nv = prefix ? min(cpt, n_kept - t * cpt) : 0;
-          if (prefix) {
-            // one N = c MMA chain per chunk block (keys of different chunks are not uniformly strided)
-            for (int q = 0; q < nv; ++q) {
-              const uint32_t kbase = ka + q * p.chunk_bytes;
 #pragma unroll
-              for (int k = 0; k < D / 16; ++k) {
-                const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
-                const uint32_t off_k = (k >> 2) * (p.g.c * 128) + (k & 3) * 32;
-                ptx::mma_bf16(tmem + sb * BN + q * p.g.c, ptx::umma_desc_sw128(qa + off_q),
-                              ptx::umma_desc_sw128(kbase + off_k), idesc_sc, k > 0 ? 1u : 0u);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < D / 16; ++k) {
-              const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
-              const uint32_t off_k = (k >> 2) * (kKVBytes / 4) + (k & 3) * 32;
-              ptx::mma_bf16(tmem + sb * BN, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k),
-                            idesc_s, k > 0 ? 1u : 0u);
-            }
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+            const uint32_t off_k = (k >> 2) * (kKVBytes / 4) + (k & 3) * 32;
+            ptx::mma_bf16(tmem + sb * BN, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k),
+                          idesc_s, k > 0 ? 1u : 0u);
           }
           ptx::mma_commit(&s_full[sb]);
           trace_ev(p, 2, scount);
@@ -468,8 +449,8 @@ int sm_count() {
 }  // namespace
 
 bool attn_tc_supported(const LayerGeom& g) {
-  // chunk blocks feed N = c MMAs (M = 128 needs N % 16 == 0) and must tile 128 keys
-  return g.d == D && g.rec_swz == 1 && g.c >= 16 && g.c <= BN && (BN % g.c) == 0;
+  // chunk blocks (c rows, 8-row swizzle atoms) must tile 128 keys
+  return g.d == D && g.rec_swz == 1 && g.c >= 8 && g.c <= BN && (BN % g.c) == 0;
 }
 
 int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix) {
