@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* kvbuf0 = smem + kQBytes;
   uint8_t* pbuf = kvbuf0 + 2 * kKVBytes;
   __shared__ float red_m[256], red_l[256];  // [2 warps of a quadrant][128 rows]
+  __shared__ int slot_of_pos[16];          // producer: slot of each chunk position of a tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + kPBytes);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
@@ -192,16 +193,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           // the swizzled shared-memory image (rec_elem), land at rows [q c, (q+1) c) of the
           // [half][128 keys][128 B] K and V tiles
           const uint32_t hb = p.g.c * 128u;  // bytes of one (K|V, half) block
-          for (int q = 0; q < ncopy; ++q) {
-            const int slot = __shfl_sync(0xffffffffu, my_slot, q < nv ? q : nv - 1);
-            if (lane == 0) {
-              const char* src = p.pool + slot * p.rec_bytes + (int64_t)kvh * p.chunk_bytes;
-              uint8_t* dst = kb + q * hb;
-              ptx::bulk_g2s(dst, src, hb, &kv_full[st]);
-              ptx::bulk_g2s(dst + kKVBytes / 4, src + hb, hb, &kv_full[st]);
-              ptx::bulk_g2s(dst + kKVBytes / 2, src + 2 * hb, hb, &kv_full[st]);
-              ptx::bulk_g2s(dst + 3 * (kKVBytes / 4), src + 3 * hb, hb, &kv_full[st]);
-            }
+          // copies are issued by many lanes at once (a single issuing thread serialises them):
+          // lane = (chunk position q, block b) with b in {K h0, K h1, V h0, V h1}
+          if (lane < cpt) slot_of_pos[lane] = my_slot;
+          __syncwarp();  // slot ids visible; expect_tx (lane 0) precedes every complete_tx of this phase
+          for (int w = lane; w < ncopy * 4; w += 32) {
+            const int q = w >> 2, b = w & 3;
+            const int sl = slot_of_pos[q < nv ? q : nv - 1];
+            const char* src = p.pool + (int64_t)sl * p.rec_bytes + (int64_t)kvh * p.chunk_bytes + b * hb;
+            ptx::bulk_g2s(kb + b * (kKVBytes / 4) + q * hb, src, hb, &kv_full[st]);
           }
         } else if (lane == 0) {
           const int ts0 = (t - p.NTp_cap) * BN;
