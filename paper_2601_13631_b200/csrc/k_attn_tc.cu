@@ -28,7 +28,9 @@ namespace ckv {
 namespace {
 
 constexpr int BM = 128, BN = 128, D = 128;
-constexpr int kSoftWarps = 8;
+constexpr int kSoftWarps = 16;
+constexpr int NWQ = kSoftWarps / 4;  // softmax warps per TMEM lane quadrant
+constexpr int CPW = BN / NWQ;        // key / O columns per softmax warp
 constexpr int kThreads = 64 + 32 * kSoftWarps;
 constexpr uint32_t kQBytes = BM * D * 2;           // 32 KB
 constexpr uint32_t kKVBytes = 2 * BN * D * 2;      // K + V = 64 KB
@@ -113,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* qbuf = smem;
   uint8_t* kvbuf0 = smem + kQBytes;
   uint8_t* pbuf = kvbuf0 + 2 * kKVBytes;
-  __shared__ float red_m[256], red_l[256];  // [2 warps of a quadrant][128 rows]
+  __shared__ float red_m[NWQ * 128], red_l[NWQ * 128];  // [warp of a quadrant][128 rows]
   __shared__ int slot_of_pos[16];          // producer: slot of each chunk position of a tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + kPBytes);
   uint64_t* q_full = bars + 0;
@@ -172,10 +174,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_load_2d(qbuf, &tmQ, q_full, 0, yq);
         ptx::tma_load_2d(qbuf + kQBytes / 2, &tmQ, q_full, 64, yq);
       }
+      int next_slot = -1;
+      {
+        int tn = tl.t0;
+        while (tn < tl.t1 && !tile_present(p, tl, tn)) ++tn;
+        next_slot = (tn < p.NTp_cap && lane < cpt && tn * cpt + lane < n_kept) ? p.kept_slots[tn * cpt + lane] : -1;
+      }
       for (int t = tl.t0; t < tl.t1; ++t) {
         if (!tile_present(p, tl, t)) continue;
-        int my_slot = -1;
-        if (t < p.NTp_cap && lane < cpt && t * cpt + lane < n_kept) my_slot = p.kept_slots[t * cpt + lane];
+        const int my_slot = next_slot;  // loaded one tile ahead
+        {
+          int tn = t + 1;
+          while (tn < tl.t1 && !tile_present(p, tl, tn)) ++tn;
+          next_slot = (tn < p.NTp_cap && lane < cpt && tn * cpt + lane < n_kept) ? p.kept_slots[tn * cpt + lane] : -1;
+        }
         const int st = kvcount & 1;
         uint8_t* kb = kvbuf0 + st * kKVBytes;
         const bool prefix = t < p.NTp_cap;
@@ -269,10 +281,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
+    // kSoftWarps = 16: four warps per TMEM lane quadrant, each owning CPW = 32 key columns
+    // of S, the same 32 columns of O, and 32 keys (64 bytes) of every P row.
     const int e = warp - 2, quad = warp & 3, h = e >> 2;
     const int rit = quad * 32 + lane;  // row in tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t bar_id = 1 + quad;  // named barrier shared by the two warps of a quadrant
+    const uint32_t bar_id = 1 + quad;  // named barrier of the quadrant's NWQ warps
     int icount = 0, scount = 0, pcount = 0;
     const float sc = p.scale;
     int n_valid_prefix = 0;
@@ -294,84 +308,69 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(&s_full[sb], (scount >> 1) & 1);
         if (warp == 2 && lane == 0) trace_ev(p, 3, scount);
         ptx::tc_fence_after();
-        // S columns of this warp: pass 1 = masked max, pass 2 = P (re-read from TMEM, so only
-        // 32 logits are live at a time)
-        const uint32_t s_addr = tmem + sb * BN + h * 64 + lane_off;
+        float x[CPW];
+        ptx::tmem_ld32p(tmem + sb * BN + h * CPW + lane_off, x);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);  // S buffer consumed into registers
+        ++scount;
         const bool pre = t < p.NTp_cap;
-        const int base = (pre ? t * BN : (t - p.NTp_cap) * BN) + h * 64;
+        const int b0 = (pre ? t * BN : (t - p.NTp_cap) * BN) + h * CPW;
         const int lim = pre ? n_valid_prefix : min(r + 1, p.g.ns);  // key valid iff index < lim
-        float tmax = -INFINITY;
-#pragma unroll 1
-        for (int hh = 0; hh < 2; ++hh) {
-          float x[32];
-          ptx::tmem_ld32p(s_addr + hh * 32, x);
-          const int b0 = base + hh * 32;
-          if (b0 + 32 > lim) {
+        if (b0 + CPW > lim) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (b0 + i >= lim) x[i] = -INFINITY;
-          }
-#pragma unroll
-          for (int n = 16; n >= 1; n >>= 1)
-#pragma unroll
-            for (int i = 0; i < n; ++i) x[i] = fmaxf(x[i], x[i + n]);
-          tmax = fmaxf(tmax, x[0]);
+          for (int i = 0; i < CPW; ++i)
+            if (b0 + i >= lim) x[i] = -INFINITY;
         }
-        red_m[h * 128 + rit] = tmax;
-        ptx::named_bar_sync(bar_id, 64);
-        tmax = fmaxf(red_m[rit], red_m[128 + rit]) * sc;
-        ptx::named_bar_sync(bar_id, 64);  // red_m reusable
+        float mx[CPW / 2];
+#pragma unroll
+        for (int i = 0; i < CPW / 2; ++i) mx[i] = fmaxf(x[i], x[i + CPW / 2]);
+#pragma unroll
+        for (int n = CPW / 4; n >= 1; n >>= 1)
+#pragma unroll
+          for (int i = 0; i < n; ++i) mx[i] = fmaxf(mx[i], mx[i + n]);
+        red_m[h * 128 + rit] = mx[0];
+        ptx::named_bar_sync(bar_id, 32 * NWQ);
+        float tmax = red_m[rit];
+#pragma unroll
+        for (int w = 1; w < NWQ; ++w) tmax = fmaxf(tmax, red_m[w * 128 + rit]);
+        tmax *= sc;
+        ptx::named_bar_sync(bar_id, 32 * NWQ);  // red_m reusable
         const float m_new = fmaxf(m_ref, tmax);
         const bool resc = (j > 0) && (m_ref != -INFINITY) && (m_new > m_ref + kRescaleThresh);
         const float f = resc ? fast_exp2(m_ref - m_new) : 1.f;
         if (j == 0 || m_ref == -INFINITY || resc) m_ref = m_new;
         const float msub = (m_ref == -INFINITY) ? 0.f : m_ref;
-        float lsum = 0.f;
-        uint32_t pk[32];
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[CPW / 2];
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          float x[32];
-          ptx::tmem_ld32p(s_addr + hh * 32, x);
-          const int b0 = base + hh * 32;
-          if (b0 + 32 > lim) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (b0 + i >= lim) x[i] = -INFINITY;
-          }
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float p0 = fast_exp2(fmaf(x[2 * i], sc, -msub));
-            const float p1 = fast_exp2(fmaf(x[2 * i + 1], sc, -msub));
-            lsum += p0 + p1;
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            pk[hh * 16 + i] = *reinterpret_cast<uint32_t*>(&b2);
-          }
+        for (int i = 0; i < CPW / 2; ++i) {
+          const float p0 = fast_exp2(fmaf(x[2 * i], sc, -msub));
+          const float p1 = fast_exp2(fmaf(x[2 * i + 1], sc, -msub));
+          ls[i & 3] += p0 + p1;
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+          pk[i] = *reinterpret_cast<uint32_t*>(&b2);
         }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);
-        ++scount;
+        const float lsum = (ls[0] + ls[1]) + (ls[2] + ls[3]);
         if (__any_sync(0xffffffffu, resc)) {
           // lazy rescale: O must hold PV(j-1) before it is multiplied by 2^(m_old - m_new)
           ptx::mbar_wait(p_empty, (pcount - 1) & 1);
           ptx::tc_fence_after();
+          float o[32];
+          const uint32_t ta = tmem_O + h * CPW + lane_off;
+          ptx::tmem_ld32(ta, o);
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            float o[32];
-            const uint32_t ta = tmem_O + h * 64 + half * 32 + lane_off;
-            ptx::tmem_ld32(ta, o);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] *= f;
-            ptx::tmem_st32(ta, o);
-          }
+          for (int i = 0; i < 32; ++i) o[i] *= f;
+          ptx::tmem_st32(ta, o);
         }
         l = l * f + lsum;
-        // P buffer free (PV(j-1) done reading it)?
+        // P buffer free (PV(j-1) done reading it)?  keys [h*32, h*32+32) = half h/2, units
+        // 4*(h&1) .. 4*(h&1)+3 of the 128-byte row, swizzled by (row & 7)
         ptx::mbar_wait(p_empty, (pcount & 1) ^ 1);
-        const uint32_t prow = ptx::smem_u32(pbuf) + h * (kPBytes / 2) + rit * 128;
+        const uint32_t prow = ptx::smem_u32(pbuf) + (h >> 1) * (kPBytes / 2) + rit * 128;
 #pragma unroll
-        for (int c16 = 0; c16 < 8; ++c16) {
-          const uint32_t phys = (uint32_t)(c16 ^ (rit & 7));
+        for (int c16 = 0; c16 < CPW / 8; ++c16) {
+          const uint32_t phys = (uint32_t)(((h & 1) * 4 + c16) ^ (rit & 7));
           ptx::st_shared_v4(prow + phys * 16, pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]);
         }
         ptx::fence_proxy_async_smem();
@@ -386,22 +385,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_wait(o_full, icount & 1);
       ptx::tc_fence_after();
       red_l[h * 128 + rit] = l;
-      ptx::named_bar_sync(bar_id, 64);
-      const float ltot = red_l[rit] + red_l[128 + rit];
-      ptx::named_bar_sync(bar_id, 64);
-      float o[64];
-      if (j > 0) {
-        ptx::tmem_ld32p(tmem_O + h * 64 + lane_off, o);
-        ptx::tmem_ld32p(tmem_O + h * 64 + 32 + lane_off, o + 32);
-      }
+      ptx::named_bar_sync(bar_id, 32 * NWQ);
+      float ltot = 0.f;
+#pragma unroll
+      for (int w = 0; w < NWQ; ++w) ltot += red_l[w * 128 + rit];
+      ptx::named_bar_sync(bar_id, 32 * NWQ);
+      float o[32];
+      if (j > 0) ptx::tmem_ld32(tmem_O + h * CPW + lane_off, o);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(o_empty);
       if (row_ok) {
         const float inv = (j > 0 && ltot > 0.f) ? 1.f / ltot : 0.f;
-        float* dst = p.o_part + (((size_t)sp * p.g.Hkv + kvh) * p.g.R + rho) * D + h * 64;
+        float* dst = p.o_part + (((size_t)sp * p.g.Hkv + kvh) * p.g.R + rho) * D + h * CPW;
 #pragma unroll
-        for (int i = 0; i < 64; i += 4)
+        for (int i = 0; i < CPW; i += 4)
           *reinterpret_cast<float4*>(dst + i) =
               (j > 0) ? make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv)
                       : make_float4(0.f, 0.f, 0.f, 0.f);

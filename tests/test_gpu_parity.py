@@ -123,7 +123,7 @@ def test_tensor_core_paths_vs_oracle_shapes(c, ns, k):
     cfg = ShapeConfig("tcshape", 1, 8, 2, 128, 5003, c, ns, 1000, "bf16")
     a, prefix = make_ctx(cfg, k=k)
     b, _ = make_ctx(cfg, k=k, flags=CKV_FLAG_SIMT_ATTN | CKV_FLAG_SIMT_SCORE)
-    assert a.attn_kernel_kind == (1 if c >= 16 else 0) and b.attn_kernel_kind == 0
+    assert a.attn_kernel_kind == 1 and b.attn_kernel_kind == 0
     ra = run_layers(a, cfg, prefix, [0])[0]
     rb = run_layers(b, cfg, prefix, [0])[0]
     check_layer(ra["ids"], ra["out"], ra["A"], ra["qs"], ra["ks"], ra["vs"], *prefix[0], cfg, k)
