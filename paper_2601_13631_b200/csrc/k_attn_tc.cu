@@ -88,8 +88,9 @@ __device__ __forceinline__ bool tile_present(const AttnParams& p, const Tiles& t
 // of 128 rows each.  V is the MN-major B operand (d contiguous), P the K-major A operand.
 __device__ __forceinline__ void issue_pv(const AttnParams& p, uint32_t tmem_O, uint32_t pa, uint8_t* kvbuf0,
                                          uint64_t* p_full, uint64_t* p_empty, uint64_t* o_empty, uint64_t* kv_empty,
-                                         uint32_t idesc_o, int jj, int stage, bool prefix, int nv, int icount,
-                                         int& pcount) {
+                                         uint64_t* v_full, uint32_t idesc_o, int jj, int stage, int stage_use,
+                                         bool prefix, int nv, int icount, int& pcount) {
+  ptx::mbar_wait(&v_full[stage], (stage_use >> 1) & 1);
   ptx::mbar_wait(p_full, pcount & 1);
   if (jj == 0) ptx::mbar_wait(o_empty, (icount & 1) ^ 1);
   ptx::tc_fence_after();
@@ -120,15 +121,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + kPBytes);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;   // [2]
-  uint64_t* kv_empty = bars + 4;  // [2]
+  uint64_t* k_full = bars + 2;    // [2] K half of a stage landed
+  uint64_t* k_empty = bars + 14;  // [2] S(j) done with K of the stage
+  uint64_t* v_full = bars + 18;   // [2] V half landed
+  uint64_t* kv_empty = bars + 4;  // [2] PV(j) done with V of the stage
   uint64_t* s_full = bars + 6;    // [2]
   uint64_t* s_empty = bars + 8;   // [2]
   uint64_t* p_full = bars + 10;
   uint64_t* p_empty = bars + 11;
   uint64_t* o_full = bars + 12;
   uint64_t* o_empty = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);  // bars 16, 17 hold the slot
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_kept = *p.n_kept_dev;
@@ -138,7 +141,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&s_empty[i], kSoftWarps);
@@ -195,33 +200,35 @@ __global__ void __launch_bounds__(kThreads, 1)
         // c = 8 with an odd chunk count: the last 16-key MMA step also spans the next (absent)
         // chunk position, so fill it with a duplicate (finite V; its P is masked to 0)
         const int ncopy = (prefix && (nv * p.g.c) % 16) ? nv + 1 : nv;
-        if (lane == 0) {
-          ptx::mbar_wait(&kv_empty[st], ((kvcount >> 1) & 1) ^ 1);
-          ptx::mbar_expect_tx(&kv_full[st], prefix ? ncopy * p.chunk_bytes : kKVBytes);
-          trace_ev(p, 0, kvcount);
-        }
-        if (prefix) {
-          // four contiguous bulk copies per kept chunk: its (kv head) K and V halves, already in
-          // the swizzled shared-memory image (rec_elem), land at rows [q c, (q+1) c) of the
-          // [half][128 keys][128 B] K and V tiles
-          const uint32_t hb = p.g.c * 128u;  // bytes of one (K|V, half) block
-          // copies are issued by many lanes at once (a single issuing thread serialises them):
-          // lane = (chunk position q, block b) with b in {K h0, K h1, V h0, V h1}
-          if (lane < cpt) slot_of_pos[lane] = my_slot;
-          __syncwarp();  // slot ids visible; expect_tx (lane 0) precedes every complete_tx of this phase
-          for (int w = lane; w < ncopy * 4; w += 32) {
-            const int q = w >> 2, b = w & 3;
-            const int sl = slot_of_pos[q < nv ? q : nv - 1];
-            const char* src = p.pool + (int64_t)sl * p.rec_bytes + (int64_t)kvh * p.chunk_bytes + b * hb;
-            ptx::bulk_g2s(kb + b * (kKVBytes / 4) + q * hb, src, hb, &kv_full[st]);
+        // K and V of a stage have separate barriers: K(j+2) may land as soon as S(j) is done,
+        // V(j+2) once PV(j) is done
+        const uint32_t hb = p.g.c * 128u;  // bytes of one (K|V, half) block
+        if (prefix && lane < cpt) slot_of_pos[lane] = my_slot;
+        for (int kv = 0; kv < 2; ++kv) {
+          uint64_t* full = kv == 0 ? &k_full[st] : &v_full[st];
+          if (lane == 0) {
+            ptx::mbar_wait(kv == 0 ? &k_empty[st] : &kv_empty[st], ((kvcount >> 1) & 1) ^ 1);
+            ptx::mbar_expect_tx(full, prefix ? ncopy * 2 * hb : kKVBytes / 2);
+            if (kv == 0) trace_ev(p, 0, kvcount);
           }
-        } else if (lane == 0) {
-          const int ts0 = (t - p.NTp_cap) * BN;
-          uint8_t* vb = kb + kKVBytes / 2;
-          ptx::tma_load_3d(kb, &tmKs, &kv_full[st], 0, kvh, ts0);
-          ptx::tma_load_3d(kb + kKVBytes / 4, &tmKs, &kv_full[st], 64, kvh, ts0);
-          ptx::tma_load_3d(vb, &tmVs, &kv_full[st], 0, kvh, ts0);
-          ptx::tma_load_3d(vb + kKVBytes / 4, &tmVs, &kv_full[st], 64, kvh, ts0);
+          __syncwarp();  // slot ids visible; expect_tx precedes every complete_tx of this phase
+          uint8_t* dstb = kb + kv * (kKVBytes / 2);
+          if (prefix) {
+            // two contiguous bulk copies per kept chunk and operand (h0, h1 of the swizzled
+            // record image, rec_elem) into rows [q c, (q+1) c) of the [half][128 keys][128 B]
+            // tile; issued by many lanes at once (one issuing thread serialises them)
+            for (int w = lane; w < ncopy * 2; w += 32) {
+              const int q = w >> 1, hh = w & 1;
+              const int sl = slot_of_pos[q < nv ? q : nv - 1];
+              const char* src = p.pool + (int64_t)sl * p.rec_bytes + (int64_t)kvh * p.chunk_bytes + (kv * 2 + hh) * hb;
+              ptx::bulk_g2s(dstb + hh * (kKVBytes / 4) + q * hb, src, hb, full);
+            }
+          } else if (lane == 0) {
+            const int ts0 = (t - p.NTp_cap) * BN;
+            const CUtensorMap* m = kv == 0 ? &tmKs : &tmVs;
+            ptx::tma_load_3d(dstb, m, full, 0, kvh, ts0);
+            ptx::tma_load_3d(dstb + kKVBytes / 4, m, full, 64, kvh, ts0);
+          }
         }
         __syncwarp();
         ++kvcount;
@@ -240,12 +247,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int sp = it % p.nsplit;
         const Tiles tl = item_tiles(p, sp, n_kept);
         ptx::mbar_wait(q_full, icount & 1);
-        int j = 0, prev_stage = 0, prev_nv = 0;
+        int j = 0, prev_stage = 0, prev_nv = 0, prev_use = 0;
         bool prev_prefix = false;
         for (int t = tl.t0; t < tl.t1; ++t) {
           if (!tile_present(p, tl, t)) continue;
           const int st = kvcount & 1;
-          ptx::mbar_wait(&kv_full[st], (kvcount >> 1) & 1);
+          ptx::mbar_wait(&k_full[st], (kvcount >> 1) & 1);
           trace_ev(p, 1, kvcount);
           const int sb = scount & 1;
           ptx::mbar_wait(&s_empty[sb], ((scount >> 1) & 1) ^ 1);
@@ -261,20 +268,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                           idesc_s, k > 0 ? 1u : 0u);
           }
           ptx::mma_commit(&s_full[sb]);
+          ptx::mma_commit(&k_empty[st]);
           trace_ev(p, 2, scount);
           ++scount;
           if (j > 0)
-            issue_pv(p, tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, idesc_o, j - 1, prev_stage,
-                     prev_prefix, prev_nv, icount, pcount);
+            issue_pv(p, tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, v_full, idesc_o, j - 1, prev_stage,
+                     prev_use, prev_prefix, prev_nv, icount, pcount);
           prev_stage = st;
+          prev_use = kvcount;
           prev_prefix = prefix;
           prev_nv = nv;
           ++kvcount;
           ++j;
         }
         if (j > 0)
-          issue_pv(p, tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, idesc_o, j - 1, prev_stage, prev_prefix,
-                   prev_nv, icount, pcount);
+          issue_pv(p, tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, v_full, idesc_o, j - 1, prev_stage,
+                   prev_use, prev_prefix, prev_nv, icount, pcount);
         ptx::mma_commit(q_empty);
         ptx::mma_commit(o_full);
       }
