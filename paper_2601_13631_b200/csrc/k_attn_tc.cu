@@ -36,7 +36,8 @@ constexpr uint32_t kQBytes = BM * D * 2;           // 32 KB
 constexpr uint32_t kKVBytes = 2 * BN * D * 2;      // K + V = 64 KB
 constexpr uint32_t kPBytes = BM * BN * 2;          // 32 KB
 constexpr size_t kSmem = kQBytes + 2 * kKVBytes + kPBytes + 4096 + 1024;
-constexpr float kRescaleThresh = 8.f;              // log2 units
+constexpr float kRescaleThresh = 8.f;
+constexpr int kSlotBuf = 1024;              // log2 units
 
 struct AttnParams {
   LayerGeom g;
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* pbuf = kvbuf0 + 2 * kKVBytes;
   __shared__ float red_m[NWQ * 128], red_l[NWQ * 128];  // [warp of a quadrant][128 rows]
   __shared__ int slot_of_pos[16];          // producer: slot of each chunk position of a tile
+  __shared__ int slot_buf[kSlotBuf];       // producer: slot ids of the current item
   uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + kPBytes);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
@@ -179,20 +181,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_load_2d(qbuf, &tmQ, q_full, 0, yq);
         ptx::tma_load_2d(qbuf + kQBytes / 2, &tmQ, q_full, 64, yq);
       }
-      int next_slot = -1;
-      {
-        int tn = tl.t0;
-        while (tn < tl.t1 && !tile_present(p, tl, tn)) ++tn;
-        next_slot = (tn < p.NTp_cap && lane < cpt && tn * cpt + lane < n_kept) ? p.kept_slots[tn * cpt + lane] : -1;
-      }
+      // all slot ids of the item's kept chunks, staged in shared memory once per item
+      const int c_beg = min(tl.t0, p.NTp_cap) * cpt;
+      const int c_end = min(min(tl.t1, p.NTp_cap) * cpt, n_kept);
+      for (int i = c_beg + lane; i < c_end && i - c_beg < kSlotBuf; i += 32) slot_buf[i - c_beg] = p.kept_slots[i];
+      __syncwarp();
       for (int t = tl.t0; t < tl.t1; ++t) {
         if (!tile_present(p, tl, t)) continue;
-        const int my_slot = next_slot;  // loaded one tile ahead
-        {
-          int tn = t + 1;
-          while (tn < tl.t1 && !tile_present(p, tl, tn)) ++tn;
-          next_slot = (tn < p.NTp_cap && lane < cpt && tn * cpt + lane < n_kept) ? p.kept_slots[tn * cpt + lane] : -1;
-        }
         const int st = kvcount & 1;
         uint8_t* kb = kvbuf0 + st * kKVBytes;
         const bool prefix = t < p.NTp_cap;
@@ -203,7 +198,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // K and V of a stage have separate barriers: K(j+2) may land as soon as S(j) is done,
         // V(j+2) once PV(j) is done
         const uint32_t hb = p.g.c * 128u;  // bytes of one (K|V, half) block
-        if (prefix && lane < cpt) slot_of_pos[lane] = my_slot;
+        if (prefix && lane < cpt && lane < nv) {
+          const int ci = t * cpt + lane;
+          slot_of_pos[lane] = (ci - c_beg < kSlotBuf) ? slot_buf[ci - c_beg] : p.kept_slots[ci];
+        }
         for (int kv = 0; kv < 2; ++kv) {
           uint64_t* full = kv == 0 ? &k_full[st] : &v_full[st];
           if (lane == 0) {
