@@ -31,7 +31,7 @@ constexpr int BM = 128, BN = 128, D = 128;
 constexpr int kSoftWarps = 16;
 constexpr int NWQ = kSoftWarps / 4;  // softmax warps per TMEM lane quadrant
 constexpr int CPW = BN / NWQ;        // key / O columns per softmax warp
-constexpr int kThreads = 96 + 32 * kSoftWarps;  // 2 producer warps, MMA warp, softmax warps
+constexpr int kThreads = 64 + 32 * kSoftWarps;
 constexpr uint32_t kQBytes = BM * D * 2;           // 32 KB
 constexpr uint32_t kKVBytes = 2 * BN * D * 2;      // K + V = 64 KB
 constexpr uint32_t kPBytes = BM * BN * 2;          // 32 KB
@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* kvbuf0 = smem + kQBytes;
   uint8_t* pbuf = kvbuf0 + 2 * kKVBytes;
   __shared__ float red_m[NWQ * 128], red_l[NWQ * 128];  // [warp of a quadrant][128 rows]
-  __shared__ int slot_of_pos[32];          // producers: slot of each chunk position of their tile
+  __shared__ int slot_of_pos[16];          // producer: slot of each chunk position of a tile
+  __shared__ int slot_buf[kSlotBuf];       // producer: slot ids of the current item
   uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + kPBytes);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
@@ -142,9 +143,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&k_full[i], 32);
+      ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
-      ptx::mbar_init(&v_full[i], 32);
+      ptx::mbar_init(&v_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&s_empty[i], kSoftWarps);
@@ -155,89 +156,83 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(o_empty, kSoftWarps);
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc<512>(tmem_slot);
+  if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tmem_O = tmem + 256;
 
-  if (warp < 2) {
-    // ------------------------------------------------------------ producers: warp s fills
-    // stage s (tiles of its parity).  Prefix tiles: cp.async 16-byte copies by all 32 lanes
-    // (the TMA engine serialises many small copies), completion -> proxy fence -> arrive;
-    // suffix tiles: 3-D TMA through k_suf / v_suf.  Warp 0 also loads the Q tile of an item.
-    const int s_own = warp;
-    if (warp == 0 && lane == 0) ptx::tma_prefetch_desc(&tmQ);
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer (whole warp:
+    // lanes fetch the tile's slot ids in parallel, lane 0 issues the copies)
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmQ);
+    }
     int icount = 0, kvcount = 0;
     const int cpt = BN / p.g.c;  // chunks per key tile (<= 16)
-    int* my_pos = slot_of_pos + 16 * s_own;
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
       const int sp = it % p.nsplit, mt = (it / p.nsplit) % p.MT, kvh = it / (p.nsplit * p.MT);
       const Tiles tl = item_tiles(p, sp, n_kept);
-      if (warp == 0 && lane == 0) {
+      if (lane == 0) {
         ptx::mbar_wait(q_empty, (icount & 1) ^ 1);
         ptx::mbar_expect_tx(q_full, kQBytes);
         const int yq = kvh * p.R_pad + mt * BM;
         ptx::tma_load_2d(qbuf, &tmQ, q_full, 0, yq);
         ptx::tma_load_2d(qbuf + kQBytes / 2, &tmQ, q_full, 64, yq);
       }
+      // all slot ids of the item's kept chunks, staged in shared memory once per item
+      const int c_beg = min(tl.t0, p.NTp_cap) * cpt;
+      const int c_end = min(min(tl.t1, p.NTp_cap) * cpt, n_kept);
+      for (int i = c_beg + lane; i < c_end && i - c_beg < kSlotBuf; i += 32) slot_buf[i - c_beg] = p.kept_slots[i];
+      __syncwarp();
       for (int t = tl.t0; t < tl.t1; ++t) {
         if (!tile_present(p, tl, t)) continue;
         const int st = kvcount & 1;
-        const int use = kvcount;
-        ++kvcount;
-        if (st != s_own) continue;
         uint8_t* kb = kvbuf0 + st * kKVBytes;
         const bool prefix = t < p.NTp_cap;
         const int nv = prefix ? min(cpt, n_kept - t * cpt) : 0;
         // c = 8 with an odd chunk count: the last 16-key MMA step also spans the next (absent)
         // chunk position, so fill it with a duplicate (finite V; its P is masked to 0)
         const int ncopy = (prefix && (nv * p.g.c) % 16) ? nv + 1 : nv;
+        // K and V of a stage have separate barriers: K(j+2) may land as soon as S(j) is done,
+        // V(j+2) once PV(j) is done
         const uint32_t hb = p.g.c * 128u;  // bytes of one (K|V, half) block
-        if (prefix && lane < ncopy) my_pos[lane] = p.kept_slots[t * cpt + (lane < nv ? lane : nv - 1)];
+        if (prefix && lane < cpt && lane < nv) {
+          const int ci = t * cpt + lane;
+          slot_of_pos[lane] = (ci - c_beg < kSlotBuf) ? slot_buf[ci - c_beg] : p.kept_slots[ci];
+        }
         for (int kv = 0; kv < 2; ++kv) {
           uint64_t* full = kv == 0 ? &k_full[st] : &v_full[st];
           if (lane == 0) {
-            ptx::mbar_wait(kv == 0 ? &k_empty[st] : &kv_empty[st], ((use >> 1) & 1) ^ 1);
-            if (kv == 0) trace_ev(p, 0, use);
+            ptx::mbar_wait(kv == 0 ? &k_empty[st] : &kv_empty[st], ((kvcount >> 1) & 1) ^ 1);
+            ptx::mbar_expect_tx(full, prefix ? ncopy * 2 * hb : kKVBytes / 2);
+            if (kv == 0) trace_ev(p, 0, kvcount);
           }
-          __syncwarp();
+          __syncwarp();  // slot ids visible; expect_tx precedes every complete_tx of this phase
           uint8_t* dstb = kb + kv * (kKVBytes / 2);
           if (prefix) {
-            // unit u: chunk position q, half hh, 16-byte unit w of the (kv head, K|V, half)
-            // block of the swizzled record image (rec_elem) -> rows [q c, (q+1) c) of half hh
-            const int upb = (int)(hb / 16);
-            const int nunits = ncopy * 2 * upb;
-            for (int u = lane; u < nunits; u += 32) {
-              const int q = u / (2 * upb), hh = (u / upb) & 1, w = u % upb;
-              const char* src = p.pool + (int64_t)my_pos[q] * p.rec_bytes + (int64_t)kvh * p.chunk_bytes +
-                                (kv * 2 + hh) * hb + w * 16;
-              ptx::cp_async16(dstb + hh * (kKVBytes / 4) + q * hb + w * 16, src);
+            // two contiguous bulk copies per kept chunk and operand (h0, h1 of the swizzled
+            // record image, rec_elem) into rows [q c, (q+1) c) of the [half][128 keys][128 B]
+            // tile; issued by many lanes at once (one issuing thread serialises them)
+            for (int w = lane; w < ncopy * 2; w += 32) {
+              const int q = w >> 1, hh = w & 1;
+              const int sl = slot_of_pos[q < nv ? q : nv - 1];
+              const char* src = p.pool + (int64_t)sl * p.rec_bytes + (int64_t)kvh * p.chunk_bytes + (kv * 2 + hh) * hb;
+              ptx::bulk_g2s(dstb + hh * (kKVBytes / 4) + q * hb, src, hb, full);
             }
-            ptx::cp_async_commit();
           } else if (lane == 0) {
             const int ts0 = (t - p.NTp_cap) * BN;
             const CUtensorMap* m = kv == 0 ? &tmKs : &tmVs;
-            ptx::mbar_expect_tx(full, kKVBytes / 2);
             ptx::tma_load_3d(dstb, m, full, 0, kvh, ts0);
             ptx::tma_load_3d(dstb + kKVBytes / 4, m, full, 64, kvh, ts0);
-          } else {
-            ptx::mbar_arrive(full);
           }
         }
-        if (prefix) {  // K group, then V group: land -> make visible to the async proxy -> arrive
-          ptx::cp_async_wait<1>();
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&k_full[st]);
-          ptx::cp_async_wait<0>();
-          ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive(&v_full[st]);
-        }
         __syncwarp();
+        ++kvcount;
       }
     }
-  } else if (warp == 2) {
+  } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);
@@ -295,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ softmax / epilogue
     // kSoftWarps = 16: four warps per TMEM lane quadrant, each owning CPW = 32 key columns
     // of S, the same 32 columns of O, and 32 keys (64 bytes) of every P row.
-    const int e = warp - 3, quad = warp & 3, h = e >> 2;
+    const int e = warp - 2, quad = warp & 3, h = e >> 2;
     const int rit = quad * 32 + lane;  // row in tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t bar_id = 1 + quad;  // named barrier of the quadrant's NWQ warps
@@ -318,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!tile_present(p, tl, t)) continue;
         const int sb = scount & 1;
         ptx::mbar_wait(&s_full[sb], (scount >> 1) & 1);
-        if (warp == 3 && lane == 0) trace_ev(p, 3, scount);
+        if (warp == 2 && lane == 0) trace_ev(p, 3, scount);
         ptx::tc_fence_after();
         float x[CPW];
         ptx::tmem_ld32p(tmem + sb * BN + h * CPW + lane_off, x);
@@ -389,7 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(p_full);
-        if (warp == 3 && lane == 0) trace_ev(p, 4, pcount);
+        if (warp == 2 && lane == 0) trace_ev(p, 4, pcount);
         ++pcount;
         ++j;
       }
@@ -423,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
   }
