@@ -31,6 +31,7 @@ struct ckv_ctx {
   int nsplit_score_max = 1, nsplit_attn_max = 1;
   int score_kind = 0;  // 0 SIMT, 1 tcgen05
   int rec_swz = 0;     // chunk-record layout (rec_elem)
+  int qpack_ns = 0;    // n_s of the GQA-packed Q the tcgen05 score kernel left in tmap_cache (0: none)
   int attn_kind = 0;   // 0 SIMT, 1 tcgen05
 
   void* probe = nullptr;
@@ -183,11 +184,16 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
   int nsplit = 0;
   cudaError_t e = cudaErrorNotSupported;
   PROF_BEGIN(0);
+  ctx->qpack_ns = 0;
   if (ctx->score_kind == 1) {
     nsplit = score_tc_nsplit(g);
     e = launch_score_tc(g, static_cast<const __nv_bfloat16*>(q),
                         static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)), ctx->lam2, ctx->lampart, nsplit,
                         ctx->tmap_cache, st);
+    if (e == cudaSuccess) {
+      ctx->launches += 1;  // + the Q pack kernel
+      ctx->qpack_ns = ns;
+    }
   }
   if (e == cudaErrorNotSupported) {
     nsplit = simt_score_nsplit(ctx, ns);
@@ -264,11 +270,14 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
     cudaError_t e = cudaErrorNotSupported;
     if (ctx->attn_kind == 1) {
       nsplit = attn_tc_nsplit(g, ctx->k, include_suffix);
+      if (nsplit > ctx->nsplit_attn_max) nsplit = ctx->nsplit_attn_max;  // o_part / lse_part capacity
       e = launch_attn_tc(g, static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(ks),
                          static_cast<const __nv_bfloat16*>(vs),
                          reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->P, ctx->kept_slots, ids,
-                         n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->tmap_cache, st);
-      if (e == cudaSuccess) ctx->launches += 1;  // + the Q pack kernel
+                         n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->tmap_cache,
+                         ctx->qpack_ns == ns, st);
+      if (e == cudaSuccess && ctx->qpack_ns != ns) ctx->launches += 1;  // + the Q pack kernel
+      ctx->qpack_ns = 0;
     }
     if (e == cudaErrorNotSupported) {
       nsplit = attn_nsplit(ctx, ns, ctx->k);

@@ -122,7 +122,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, int P_slots,
                            const int32_t* kept_slots, const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap,
                            int include_suffix, int nsplit, float* o_part, float* lse_part, void* qpack_ws,
-                           cudaStream_t st);
+                           bool qpack_ready, cudaStream_t st);
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit,
                                 T* out, float* o_f32, float* lse_nat, cudaStream_t st);

@@ -185,35 +185,63 @@ __global__ void __launch_bounds__(NT) attn_simt_kernel(LayerGeom g, const T* __r
   }
 }
 
-// Merge of split partials. Output row index (r, h); input row (kvh, rho = g*ns + r).
+// Merge of split partials, one warp per row (input row (kvh, rho = g*ns + r), output row
+// (r, h)): the split weights 2^(lse_s - M) are computed once per lane-split and broadcast;
+// each lane owns d/32 contiguous output columns (float4 loads when d % 128 == 0).
 template <typename T>
 __global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_part, const float* __restrict__ lse_part,
                                     int nsplit, T* __restrict__ out, float* __restrict__ o_f32,
                                     float* __restrict__ lse_nat) {
-  const int row = blockIdx.x;  // kvh * R + rho
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // kvh * R + rho
+  const int lane = threadIdx.x & 31;
+  const int64_t nrow = (int64_t)g.Hkv * g.R;
+  if (row >= nrow) return;
   const int kvh = row / g.R, rho = row % g.R;
   const int gq = rho / g.ns, r = rho % g.ns, h = kvh * g.G + gq;
-  const int64_t nrow = (int64_t)g.Hkv * g.R;
-  float M = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, lse_part[s * nrow + row]);
-  float den = 0.f;
-  for (int s = 0; s < nsplit; ++s) {
-    const float l = lse_part[s * nrow + row];
-    den += (l == -INFINITY) ? 0.f : fast_exp2(l - M);
-  }
+  // lane s < nsplit holds split s's lse (nsplit <= 64: two rounds)
+  float l0 = (lane < nsplit) ? lse_part[lane * nrow + row] : -INFINITY;
+  float l1 = (lane + 32 < nsplit) ? lse_part[(lane + 32) * nrow + row] : -INFINITY;
+  float M = fmaxf(l0, l1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  const float w0 = (l0 == -INFINITY) ? 0.f : fast_exp2(l0 - M);
+  const float w1 = (l1 == -INFINITY) ? 0.f : fast_exp2(l1 - M);
+  float den = w0 + w1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
   const int64_t obase = ((int64_t)r * g.Hq + h) * g.d;
-  for (int x = threadIdx.x; x < g.d; x += blockDim.x) {
-    float num = 0.f;
-    for (int s = 0; s < nsplit; ++s) {
-      const float l = lse_part[s * nrow + row];
-      if (l != -INFINITY) num += fast_exp2(l - M) * o_part[(s * nrow + row) * g.d + x];
+  const float inv = den > 0.f ? 1.f / den : 0.f;
+  if ((g.d & 127) == 0) {
+    for (int x = lane * 4; x < g.d; x += 128) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int sp = 0; sp < nsplit; ++sp) {
+        const float w = __shfl_sync(0xffffffffu, sp < 32 ? w0 : w1, sp & 31);
+        if (w == 0.f) continue;
+        const float4 v = *reinterpret_cast<const float4*>(o_part + (sp * nrow + row) * g.d + x);
+        acc.x += w * v.x;
+        acc.y += w * v.y;
+        acc.z += w * v.z;
+        acc.w += w * v.w;
+      }
+      const float o4[4] = {acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (out) out[obase + x + i] = from_f<T>(o4[i]);
+        if (o_f32) o_f32[obase + x + i] = o4[i];
+      }
     }
-    const float o = den > 0.f ? num / den : 0.f;
-    if (out) out[obase + x] = from_f<T>(o);
-    if (o_f32) o_f32[obase + x] = o;
+  } else {
+    for (int x = lane; x < g.d; x += 32) {
+      float num = 0.f;
+      for (int sp = 0; sp < nsplit; ++sp) {
+        const float w = __shfl_sync(0xffffffffu, sp < 32 ? w0 : w1, sp & 31);
+        if (w != 0.f) num += w * o_part[(sp * nrow + row) * g.d + x];
+      }
+      if (out) out[obase + x] = from_f<T>(num * inv);
+      if (o_f32) o_f32[obase + x] = num * inv;
+    }
   }
-  if (lse_nat && threadIdx.x == 0)
-    lse_nat[(int64_t)r * g.Hq + h] = den > 0.f ? (M + log2f(den)) * kLn2 : -INFINITY;
+  if (lse_nat && lane == 0) lse_nat[(int64_t)r * g.Hq + h] = den > 0.f ? (M + log2f(den)) * kLn2 : -INFINITY;
 }
 
 __global__ void lse_merge_prepare_kernel(int rows, int d, const float* __restrict__ o, const float* __restrict__ lse,
@@ -261,7 +289,7 @@ cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, con
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit, T* out,
                                 float* o_f32, float* lse_nat, cudaStream_t st) {
-  attn_combine_kernel<T><<<g.Hkv * g.R, 128, 0, st>>>(g, o_part, lse_part, nsplit, out, o_f32, lse_nat);
+  attn_combine_kernel<T><<<(g.Hkv * g.R + 7) / 8, 256, 0, st>>>(g, o_part, lse_part, nsplit, out, o_f32, lse_nat);
   return cudaGetLastError();
 }
 

@@ -471,7 +471,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, int P_slots,
                            const int32_t* kept_slots, const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap,
                            int include_suffix, int nsplit, float* o_part, float* lse_part, void* qpack_ws,
-                           cudaStream_t st) {
+                           bool qpack_ready, cudaStream_t st) {
   if (!attn_tc_supported(g) || !qpack_ws) return cudaErrorNotSupported;
   AttnParams p;
   p.g = g;
@@ -495,9 +495,12 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   p.o_part = o_part;
   p.lse_part = lse_part;
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
-  pack_q_attn_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (!qpack_ready) {  // the tcgen05 score kernel already packed this layer's Q otherwise
+    pack_q_attn_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
   CUtensorMap tmQ, tmKs, tmVs;
   if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_3d(&tmKs, k_suf, D, g.Hkv, g.ns, BN)) return cudaErrorInvalidValue;

@@ -19,42 +19,76 @@ __device__ __forceinline__ void lse2_acc(float& M, float& S, float v) {
     S += fast_exp2(v - M);
   }
 }
+// merge a partial (m, s) = m + log2(s) into (M, S)
+__device__ __forceinline__ void lse2_merge(float& M, float& S, float m, float s) {
+  if (s <= 0.f) return;
+  if (S <= 0.f) {
+    M = m;
+    S = s;
+  } else if (m > M) {
+    S = S * fast_exp2(M - m) + s;
+    M = m;
+  } else {
+    S += s * fast_exp2(m - M);
+  }
+}
 
-// Block = 8 warps x 32 rows: lane <-> row, warp w reduces splits w, w+8, ... (fixed order),
-// then warp 0 merges the 8 partials in order and adds the FULLROW suffix term.
+constexpr int kRowsPerBlock = 32;
+constexpr int kRowGroups = kRowsPerBlock / 4;  // 8 threads x 4 rows
+constexpr int kSplitGroups = 256 / kRowGroups;  // 32 split groups
+
+// Block = 256 threads over 32 flattened rows (idx = kvh * R + row = h * ns + r): thread t owns
+// rows 4*(t % 8) .. +3 and splits t/8, t/8 + 32, ...  (4 independent accumulators, coalesced
+// 128-byte row segments per split); the 32 split-group partials are merged in a fixed order.
 template <typename T>
 __global__ void __launch_bounds__(256) row_lse_kernel(LayerGeom g, const float* __restrict__ lampart, int nsplit,
                                                       const T* __restrict__ q, const T* __restrict__ ks, int fullrow,
                                                       const float* __restrict__ lam_all, int W,
                                                       float* __restrict__ Lam2, float* __restrict__ lam_local_out) {
-  __shared__ float sM[8][32], sS[8][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int idx = blockIdx.x * 32 + lane;  // = kvh * R + row = h * ns + r
-  const bool ok = idx < g.Hkv * g.R;
-  const int kvh = ok ? idx / g.R : 0, row = ok ? idx % g.R : 0;
-  float M = -INFINITY, S = 0.f;
-  if (ok) {
-    if (lam_all == nullptr) {
-      const float* src = lampart + (size_t)kvh * nsplit * g.R + row;
-      for (int sp = warp; sp < nsplit; sp += 8) lse2_acc(M, S, src[(size_t)sp * g.R]);
-    } else {
-      const int n = g.Hkv * g.R;
-      for (int w = warp; w < W; w += 8) lse2_acc(M, S, lam_all[(size_t)w * n + idx]);
-    }
+  __shared__ float sM[kSplitGroups][kRowsPerBlock + 1], sS[kSplitGroups][kRowsPerBlock + 1];
+  const int nrows = g.Hkv * g.R;
+  const int rg = threadIdx.x % kRowGroups, sg = threadIdx.x / kRowGroups;
+  const int idx0 = blockIdx.x * kRowsPerBlock + rg * 4;
+  float M[4], S[4];
+  const float* base[4];
+  int stride = 0, nparts = 0;
+  if (lam_all == nullptr) {
+    stride = g.R;
+    nparts = nsplit;
+  } else {
+    stride = nrows;
+    nparts = W;
   }
-  sM[warp][lane] = M;
-  sS[warp][lane] = S;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    M[i] = -INFINITY;
+    S[i] = 0.f;
+    const int idx = min(idx0 + i, nrows - 1);
+    const int kvh = idx / g.R, row = idx % g.R;
+    base[i] = lam_all ? lam_all + idx : lampart + (size_t)kvh * nsplit * g.R + row;
+  }
+  for (int sp = sg; sp < nparts; sp += kSplitGroups) {
+    float v[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = base[i][(size_t)sp * stride];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lse2_acc(M[i], S[i], v[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    sM[sg][rg * 4 + i] = M[i];
+    sS[sg][rg * 4 + i] = S[i];
+  }
   __syncthreads();
-  if (warp != 0 || !ok) return;
-  M = -INFINITY;
-  S = 0.f;
-  for (int w = 0; w < 8; ++w) {
-    const float m = sM[w][lane], s = sS[w][lane];
-    if (s > 0.f) lse2_acc(M, S, m + fast_log2(s));
-  }
-  if (lam_all == nullptr && lam_local_out) lam_local_out[idx] = (S > 0.f) ? M + fast_log2(S) : -INFINITY;
+  if (threadIdx.x >= kRowsPerBlock) return;
+  const int idx = blockIdx.x * kRowsPerBlock + threadIdx.x;
+  if (idx >= nrows) return;
+  float Mt = -INFINITY, St = 0.f;
+  for (int w = 0; w < kSplitGroups; ++w) lse2_merge(Mt, St, sM[w][threadIdx.x], sS[w][threadIdx.x]);
+  if (lam_all == nullptr && lam_local_out) lam_local_out[idx] = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
   if (fullrow) {
     // causal suffix keys t <= r of the same KV head (Q1 FULLROW, Q9)
+    const int kvh = idx / g.R, row = idx % g.R;
     const int gq = row / g.ns, r = row % g.ns, h = kvh * g.G + gq;
     const float scale = kLog2e * rsqrtf((float)g.d);
     const T* qr = q + ((size_t)r * g.Hq + h) * g.d;
@@ -62,27 +96,41 @@ __global__ void __launch_bounds__(256) row_lse_kernel(LayerGeom g, const float* 
       const T* kt = ks + ((size_t)t * g.Hkv + kvh) * g.d;
       float acc = 0.f;
       for (int x = 0; x < g.d; ++x) acc = fmaf(to_f(qr[x]), to_f(kt[x]), acc);
-      lse2_acc(M, S, acc * scale);
+      lse2_acc(Mt, St, acc * scale);
     }
   }
-  Lam2[idx] = (S > 0.f) ? M + fast_log2(S) : -INFINITY;
+  Lam2[idx] = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
 }
 
-// One warp per chunk j: lanes stride over (kvh, row), then a fixed xor-tree reduce.
+// One warp per chunk j: lanes take 4 consecutive rows at a time (float4 when R % 4 == 0),
+// 4 independent partial sums, then a fixed xor-tree reduce.
 __global__ void chunk_sum_kernel(LayerGeom g, const float* __restrict__ lam2, const float* __restrict__ Lam2,
                                  float* __restrict__ A) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= g.m_loc) return;
-  float acc = 0.f;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool vec = (g.R & 3) == 0;
   for (int kvh = 0; kvh < g.Hkv; ++kvh) {
     const float* src = lam2 + ((size_t)kvh * g.m_loc + warp) * g.R;
     const float* L = Lam2 + (size_t)kvh * g.R;
-    for (int row = lane; row < g.R; row += 32) acc += fast_exp2(src[row] - L[row]);
+    if (vec) {
+      for (int row = lane * 4; row < g.R; row += 128) {
+        const float4 a = *reinterpret_cast<const float4*>(src + row);
+        const float4 b = *reinterpret_cast<const float4*>(L + row);
+        acc[0] += fast_exp2(a.x - b.x);
+        acc[1] += fast_exp2(a.y - b.y);
+        acc[2] += fast_exp2(a.z - b.z);
+        acc[3] += fast_exp2(a.w - b.w);
+      }
+    } else {
+      for (int row = lane; row < g.R; row += 32) acc[row & 3] += fast_exp2(src[row] - L[row]);
+    }
   }
+  float s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) A[warp] = acc;
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) A[warp] = s;
 }
 
 }  // namespace
@@ -92,8 +140,8 @@ cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit,
                            int fullrow, const float* lam_all, int W, float* Lam2, float* lam_local_out,
                            cudaStream_t st) {
   const int n = g.Hkv * g.R;
-  row_lse_kernel<T><<<(n + 31) / 32, 256, 0, st>>>(g, lampart, nsplit, q, k_suf, fullrow, lam_all, W, Lam2,
-                                                     lam_local_out);
+  row_lse_kernel<T><<<(n + kRowsPerBlock - 1) / kRowsPerBlock, 256, 0, st>>>(g, lampart, nsplit, q, k_suf, fullrow,
+                                                                             lam_all, W, Lam2, lam_local_out);
   return cudaGetLastError();
 }
 template cudaError_t launch_row_lse<float>(const LayerGeom&, const float*, int, const float*, const float*, int,
