@@ -16,6 +16,7 @@
 // Work units (kv head, key tile, row tile) are linearised with the row tile fastest and split
 // into contiguous ranges per CTA, so each K tile crosses HBM about once.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -53,7 +54,22 @@ __device__ __forceinline__ void tree_sum(float* a) {
   }
 }
 
-template <int C>
+// 2^x on the FMA/ALU pipes (x <= 0): round-to-nearest split x = i + f with the 1.5*2^23 trick,
+// degree-5 Taylor of 2^f on [-0.5, 0.5] (rel. error < 3e-6), exponent added in the integer
+// domain.  Used for part of the exponentials so the MUFU (ex2) pipe is not the only bound.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -125.f);
+  const float r = x + 12582912.f;
+  const float f = x - (r - 12582912.f);
+  float p = fmaf(f, 1.3333558e-3f, 9.6181291e-3f);
+  p = fmaf(p, f, 5.5504109e-2f);
+  p = fmaf(p, f, 2.4022651e-1f);
+  p = fmaf(p, f, 6.9314718e-1f);
+  p = fmaf(p, f, 1.0f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
+}
+
+template <int C, int NP>
 __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32], int key0, int kvh, int rho,
                                                bool row_ok, float& HM, float& HS, float& CM, float& CS) {
   const float sc = p.scale;
@@ -72,7 +88,10 @@ __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32]
   const float gm = m[0];
   const float gms = (gm == -INFINITY) ? 0.f : gm * sc;
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = fast_exp2(fmaf(v[j], sc, -gms));
+  for (int j = 0; j < 32; ++j) {
+    const float t = fmaf(v[j], sc, -gms);
+    v[j] = ((j & 7) < NP) ? exp2_poly(t) : fast_exp2(t);  // NP of every 8 on the FMA pipe
+  }
   constexpr int CG = C < 32 ? C : 32;  // chunk piece inside this group
   tree_sum<32, CG>(v);                 // v[0 .. 32/CG) = chunk (piece) sums
   float cs[32 / CG];
@@ -118,7 +137,7 @@ __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32]
   }
 }
 
-template <int C>
+template <int C, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -239,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int col0 = half * (BN / kColSplit) + gi * 32;
         float v[32];
         ptx::tmem_ld32(tmem_base + (uint32_t)(ab * BN + col0) + ((uint32_t)(quad * 32) << 16), v);
-        epilogue_group<C>(p, v, kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
+        epilogue_group<C, NP>(p, v, kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
       }
       if (row_ok)
         p.lampart[((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho] =
@@ -286,16 +305,36 @@ int num_sms() {
   return n;
 }
 
-template <int C>
-cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
+template <int C, int NP>
+cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<C, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  score_tc_kernel<C><<<grid, kThreads, kSmem, st>>>(tmK, tmQ, p);
+  score_tc_kernel<C, NP><<<grid, kThreads, kSmem, st>>>(tmK, tmQ, p);
   return cudaGetLastError();
+}
+
+// share of exponentials evaluated by exp2_poly (of every 8); CKV_SCORE_POLY overrides (tuning)
+int poly_share() {
+  static int np = -1;
+  if (np < 0) {
+    const char* e = getenv("CKV_SCORE_POLY");
+    np = e ? atoi(e) : 2;
+    if (np != 0 && np != 2 && np != 3) np = 2;
+  }
+  return np;
+}
+
+template <int C>
+cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
+  switch (poly_share()) {
+    case 0: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
+    case 3: return launch_cp<C, 3>(tmK, tmQ, p, grid, st);
+    default: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
+  }
 }
 
 }  // namespace
