@@ -257,8 +257,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int gi = 0; gi < BN / kColSplit / 32; ++gi) {
         const int col0 = half * (BN / kColSplit) + gi * 32;
         float v[32];
-        ptx::tmem_ld32(tmem_base + (uint32_t)(ab * BN + col0) + ((uint32_t)(quad * 32) << 16), v);
-        epilogue_group<C, NP>(p, v, kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
+        if constexpr (NP == 11) {  // tuning skeleton: pipeline only
+          HS += 1.f;
+        } else {
+          ptx::tmem_ld32(tmem_base + (uint32_t)(ab * BN + col0) + ((uint32_t)(quad * 32) << 16), v);
+          if constexpr (NP == 10) {  // tuning: TMEM drain only
+            HS += v[0] + v[31];
+          } else {
+            epilogue_group<C, NP>(p, v, kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
+          }
+        }
       }
       if (row_ok)
         p.lampart[((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho] =
@@ -323,7 +331,7 @@ int poly_share() {
   if (np < 0) {
     const char* e = getenv("CKV_SCORE_POLY");
     np = e ? atoi(e) : 2;
-    if (np != 0 && np != 2 && np != 3) np = 2;
+    if (np != 0 && np != 2 && np != 3 && np != 10 && np != 11) np = 2;
   }
   return np;
 }
@@ -333,6 +341,8 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
   switch (poly_share()) {
     case 0: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
     case 3: return launch_cp<C, 3>(tmK, tmQ, p, grid, st);
+    case 10: return launch_cp<C, 10>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
+    case 11: return launch_cp<C, 11>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
     default: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
   }
 }
