@@ -5,16 +5,18 @@
 // (Q2-Q5), and per (row, 64-key quarter tile) a partial base-2 LSE.
 //
 // Layout / schedule (persistent, one CTA per SM, 576 threads):
-//   warp 0      TMA producer: K tiles [256 keys x 128] (64 KB, double-buffered, loaded once per
-//               (kv head, key tile) = K-stationary) and Q tiles [128 rows x 128] (32 KB, 2 stages)
-//               from a GQA-packed Q [Hkv][R_pad][128]; 128-byte swizzle.
-//   warp 1      TMEM allocator + single-thread MMA issuer: D[128 x 256] fp32 in TMEM
-//               (two accumulators = all 512 columns), 8 x tcgen05.mma kind::f16 (K = 16 each).
-//   warps 2..17 epilogue: tcgen05.ld 32 columns at a time, one suffix row per thread (TMEM lane),
-//               four warps per lane quadrant (64 columns each); per-chunk LSE in registers,
-//               coalesced lam2 stores ([kvh][chunk][row] layout).
-// Work units (kv head, key tile, row tile) are linearised with the row tile fastest and split
-// into contiguous ranges per CTA, so each K tile crosses HBM about once.
+//   Work unit = (kv head, row group, 128-key tile); a row group is up to MG = 4 GQA-packed
+//   128-row tiles of Q, kept resident in shared memory (MG x 32 KB) while the CTA streams its
+//   contiguous range of key tiles, so neither Q nor K is re-read per row tile.
+//   warp 0      TMA producer: the row group's Q tiles once per group; K tiles [128 keys x 128]
+//               (32 KB, double-buffered), 128-byte swizzle.
+//   warp 1      TMEM allocator + single-thread MMA issuer: one D[128 x 128] fp32 accumulator
+//               per resident row tile (4 x 128 = all 512 TMEM columns), 8 x tcgen05.mma
+//               kind::f16 (K = 16) per accumulator.
+//   warps 2..17 epilogue: warp group g (4 warps, one per TMEM lane quadrant) drains
+//               accumulator g: one suffix row per thread, tcgen05.ld 32 columns at a time;
+//               per-chunk LSE in registers, coalesced lam2 stores ([kvh][chunk][row] layout),
+//               one partial row LSE per (row, key tile).
 #include <cstdio>
 #include <cstdlib>
 
@@ -24,23 +26,23 @@
 namespace ckv {
 namespace {
 
-constexpr int BM = 128, BN = 256, D = 128;
-constexpr int kEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 key columns each
-constexpr int kColSplit = kEpiWarps / 4;
+constexpr int BM = 128, BN = 128, D = 128, MG = 4;
+constexpr int kEpiWarps = 4 * MG;  // one warp group (4 lane quadrants) per resident row tile
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr uint32_t kKBytes = BN * D * 2;  // 65536
-constexpr uint32_t kQBytes = BM * D * 2;  // 32768
-constexpr size_t kSmem = 2 * kKBytes + 2 * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t kKBytes = BN * D * 2;  // 32 KB
+constexpr uint32_t kQBytes = BM * D * 2;  // 32 KB per row tile
+constexpr size_t kSmem = 2 * kKBytes + MG * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 struct TcParams {
   LayerGeom g;
   float* lam2;
   float* lampart;
-  int nsplit;   // = 2 * NKT
+  int nsplit;   // = NKT (one partial row LSE per key tile)
   int NKT;      // key tiles per kv head
   int MT;       // row tiles per kv head
+  int NRG;      // row groups per kv head
   int R_pad;
-  int n_units;  // Hkv * NKT * MT
+  int n_units;  // Hkv * NRG * NKT
   float scale;  // log2(e) / sqrt(d)
 };
 
@@ -99,7 +101,7 @@ __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32]
   for (int i = 0; i < 32 / CG; ++i) cs[i] = v[i];
   tree_sum<32 / CG, 32 / CG>(v);
   const float gs = v[0];
-  if (gs > 0.f) {  // running LSE of this warp's 64-key quarter tile
+  if (gs > 0.f) {  // running LSE of this row over the 128-key tile
     if (HS == 0.f) {
       HM = gms;
       HS = gs;
@@ -144,14 +146,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* kbuf0 = smem;
   uint8_t* qbuf0 = smem + 2 * kKBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kKBytes + 2 * kQBytes);
-  uint64_t* k_full = bars + 0;
-  uint64_t* k_empty = bars + 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kKBytes + MG * kQBytes);
+  uint64_t* k_full = bars + 0;        // [2]
+  uint64_t* k_empty = bars + 2;       // [2]
   uint64_t* q_full = bars + 4;
-  uint64_t* q_empty = bars + 6;
-  uint64_t* acc_full = bars + 8;
-  uint64_t* acc_empty = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* q_empty = bars + 5;
+  uint64_t* acc_full = bars + 6;      // [MG]
+  uint64_t* acc_empty = bars + 6 + MG;  // [MG]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * MG);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
@@ -161,10 +163,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
-      ptx::mbar_init(&q_full[i], 1);
-      ptx::mbar_init(&q_empty[i], 1);
+    }
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(q_empty, 1);
+    for (int i = 0; i < MG; ++i) {
       ptx::mbar_init(&acc_full[i], 1);
-      ptx::mbar_init(&acc_empty[i], kEpiWarps);
+      ptx::mbar_init(&acc_empty[i], 4);
     }
     ptx::fence_mbar_init();
   }
@@ -180,87 +184,88 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tma_prefetch_desc(&tmQ);
       int kcount = 0, qcount = 0, cur = -1;
       for (int u = u0; u < u1; ++u) {
-        const int pr = u / p.MT, mt = u % p.MT;
-        const int kvh = pr / p.NKT, kt = pr % p.NKT;
-        if (pr != cur) {
-          const int kb = kcount & 1;
-          ptx::mbar_wait(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
-          ptx::mbar_expect_tx(&k_full[kb], kKBytes);
-          const int y = kvh * p.g.n_pad + kt * BN;
-          uint8_t* dst = kbuf0 + kb * kKBytes;
-          ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
-          ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
-          cur = pr;
-          ++kcount;
+        const int grp = u / p.NKT, kt = u % p.NKT;
+        const int kvh = grp / p.NRG, rg = grp % p.NRG;
+        if (grp != cur) {  // new row group: its Q tiles, once
+          const int nm = min(MG, p.MT - rg * MG);
+          ptx::mbar_wait(q_empty, (qcount & 1) ^ 1);
+          ptx::mbar_expect_tx(q_full, nm * kQBytes);
+          for (int m = 0; m < nm; ++m) {
+            const int yq = kvh * p.R_pad + (rg * MG + m) * BM;
+            uint8_t* dq = qbuf0 + m * kQBytes;
+            ptx::tma_load_2d(dq, &tmQ, q_full, 0, yq);
+            ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, q_full, 64, yq);
+          }
+          cur = grp;
+          ++qcount;
         }
-        const int qs = qcount & 1;
-        ptx::mbar_wait(&q_empty[qs], ((qcount >> 1) & 1) ^ 1);
-        ptx::mbar_expect_tx(&q_full[qs], kQBytes);
-        const int yq = kvh * p.R_pad + mt * BM;
-        uint8_t* dq = qbuf0 + qs * kQBytes;
-        ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
-        ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
-        ++qcount;
+        const int kb = kcount & 1;
+        ptx::mbar_wait(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
+        ptx::mbar_expect_tx(&k_full[kb], kKBytes);
+        const int y = kvh * p.g.n_pad + kt * BN;
+        uint8_t* dst = kbuf0 + kb * kKBytes;
+        ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
+        ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
+        ++kcount;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
-      int kcount = 0, qcount = 0, acount = 0, cur = -1, kb = 0;
+      int kcount = 0, qcount = 0, cur = -1, nm = 0;
+      int acount[MG] = {};
       for (int u = u0; u < u1; ++u) {
-        const int pr = u / p.MT;
-        if (pr != cur) {
-          kb = kcount & 1;
-          ptx::mbar_wait(&k_full[kb], (kcount >> 1) & 1);
-          ++kcount;
-          cur = pr;
+        const int grp = u / p.NKT;
+        if (grp != cur) {
+          if (cur >= 0) ptx::mma_commit(q_empty);  // previous row group's Q fully consumed
+          nm = min(MG, p.MT - (grp % p.NRG) * MG);
+          ptx::mbar_wait(q_full, qcount & 1);
+          ++qcount;
+          cur = grp;
         }
-        const int qs = qcount & 1;
-        ptx::mbar_wait(&q_full[qs], (qcount >> 1) & 1);
-        const int ab = acount & 1;
-        ptx::mbar_wait(&acc_empty[ab], ((acount >> 1) & 1) ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + ab * BN;
-        const uint32_t qa = ptx::smem_u32(qbuf0 + qs * kQBytes);
+        const int kb = kcount & 1;
+        ptx::mbar_wait(&k_full[kb], (kcount >> 1) & 1);
         const uint32_t ka = ptx::smem_u32(kbuf0 + kb * kKBytes);
+        for (int m = 0; m < nm; ++m) {
+          ptx::mbar_wait(&acc_empty[m], ((acount[m] >> 0) & 1) ^ 1);
+          ptx::tc_fence_after();
+          const uint32_t qa = ptx::smem_u32(qbuf0 + m * kQBytes);
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
-          const uint32_t off_k = (k >> 2) * (kKBytes / 2) + (k & 3) * 32;
-          ptx::mma_bf16(d_tmem, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k), idesc,
-                        k > 0 ? 1u : 0u);
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t off = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+            const uint32_t offk = (k >> 2) * (kKBytes / 2) + (k & 3) * 32;
+            ptx::mma_bf16(tmem_base + m * BN, ptx::umma_desc_sw128(qa + off), ptx::umma_desc_sw128(ka + offk), idesc,
+                          k > 0 ? 1u : 0u);
+          }
+          ptx::mma_commit(&acc_full[m]);
+          ++acount[m];
         }
-        ptx::mma_commit(&q_empty[qs]);
-        ptx::mma_commit(&acc_full[ab]);
-        const bool last_of_pair = (u + 1 == u1) || ((u + 1) / p.MT != pr);
-        if (last_of_pair) ptx::mma_commit(&k_empty[kb]);
-        ++qcount;
-        ++acount;
+        ptx::mma_commit(&k_empty[kb]);
+        ++kcount;
       }
     }
   } else {
     const int e = warp - 2;
-    const int quad = warp & 3;
-    const int half = e >> 2;  // column quarter
-    const int row_in_tile = quad * 32 + lane;
+    const int m = e >> 2;        // accumulator / resident row tile of this warp group
+    const int quad = warp & 3;   // TMEM lane quadrant
     int acount = 0;
     for (int u = u0; u < u1; ++u) {
-      const int pr = u / p.MT, mt = u % p.MT;
-      const int kvh = pr / p.NKT, kt = pr % p.NKT;
-      const int ab = acount & 1;
-      ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
+      const int grp = u / p.NKT, kt = u % p.NKT;
+      const int kvh = grp / p.NRG, rg = grp % p.NRG;
+      if (m >= min(MG, p.MT - rg * MG)) continue;  // this row group has fewer row tiles
+      ptx::mbar_wait(&acc_full[m], acount & 1);
       ptx::tc_fence_after();
-      const int rho = mt * BM + row_in_tile;
+      const int rho = (rg * MG + m) * BM + quad * 32 + lane;
       const bool row_ok = rho < p.g.R;
       float HM = -INFINITY, HS = 0.f, CM = -INFINITY, CS = 0.f;
 #pragma unroll 1
-      for (int gi = 0; gi < BN / kColSplit / 32; ++gi) {
-        const int col0 = half * (BN / kColSplit) + gi * 32;
+      for (int gi = 0; gi < BN / 32; ++gi) {
+        const int col0 = gi * 32;
         float v[32];
         if constexpr (NP == 11) {  // tuning skeleton: pipeline only
           HS += 1.f;
         } else {
-          ptx::tmem_ld32(tmem_base + (uint32_t)(ab * BN + col0) + ((uint32_t)(quad * 32) << 16), v);
+          ptx::tmem_ld32(tmem_base + (uint32_t)(m * BN + col0) + ((uint32_t)(quad * 32) << 16), v);
           if constexpr (NP == 10) {  // tuning: TMEM drain only
             HS += v[0] + v[31];
           } else {
@@ -268,13 +273,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (row_ok)
-        p.lampart[((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho] =
-            (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);
       ++acount;
+      if (row_ok)
+        p.lampart[((size_t)kvh * p.nsplit + kt) * p.g.R + rho] = (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
     }
   }
   ptx::tc_fence_before();
@@ -351,8 +355,8 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
 
 int score_tc_nsplit(const LayerGeom& g) {
   if (g.d != D) return 0;
-  if (g.c < 1 || g.c > BN / kColSplit || ((BN / kColSplit) % g.c) != 0) return 0;
-  return kColSplit * ((g.n_loc + BN - 1) / BN);
+  if (g.c < 1 || g.c > BN || (BN % g.c) != 0) return 0;
+  return (g.n_loc + BN - 1) / BN;
 }
 
 size_t score_tc_qpack_elems(int Hkv, int R_max) { return (size_t)Hkv * ((R_max + BM - 1) / BM) * BM * D; }
@@ -365,17 +369,18 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   p.lam2 = lam2;
   p.lampart = lampart;
   p.nsplit = nsplit;
-  p.NKT = nsplit / kColSplit;
+  p.NKT = nsplit;
   p.MT = (g.R + BM - 1) / BM;
   p.R_pad = p.MT * BM;
-  p.n_units = g.Hkv * p.NKT * p.MT;
+  p.NRG = (p.MT + MG - 1) / MG;
+  p.n_units = g.Hkv * p.NRG * p.NKT;
   p.scale = kLog2e / sqrtf((float)g.d);
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
   pack_q_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap tmK, tmQ;
-  if (!make_tmap_bf16_2d(&tmK, probe_layer, D, (uint64_t)g.Hkv * g.n_pad, BN)) return cudaErrorInvalidValue;
+  if (!make_tmap_bf16_2d(&tmK, probe_layer, D, (uint64_t)g.Hkv * g.n_pad, BN)) return cudaErrorInvalidValue;  // box 64 x 128
   if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) return cudaErrorInvalidValue;
   const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
   switch (g.c) {
@@ -386,6 +391,7 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
     case 16: return launch_c<16>(tmK, tmQ, p, grid, st);
     case 32: return launch_c<32>(tmK, tmQ, p, grid, st);
     case 64: return launch_c<64>(tmK, tmQ, p, grid, st);
+    case 128: return launch_c<128>(tmK, tmQ, p, grid, st);
     default: return cudaErrorNotSupported;
   }
 }
