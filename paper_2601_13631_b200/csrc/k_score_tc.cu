@@ -27,7 +27,7 @@ namespace ckv {
 namespace {
 
 constexpr int BM = 128, BN = 128, D = 128, MG = 4;
-constexpr int kEpiWarps = 4 * MG;  // one warp group (4 lane quadrants) per resident row tile
+constexpr int kEpiWarps = 16;  // 4 lane quadrants x 4 column quarters of the 128-key tile
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kKBytes = BN * D * 2;  // 32 KB
 constexpr uint32_t kQBytes = BM * D * 2;  // 32 KB per row tile
@@ -44,7 +44,16 @@ struct TcParams {
   int R_pad;
   int n_units;  // Hkv * NRG * NKT
   float scale;  // log2(e) / sqrt(d)
+  unsigned long long* trace;  // debug (CKV_SCORE_TRACE=1): %globaltimer events of CTA 0, else null
 };
+
+__device__ __forceinline__ void strace(const TcParams& p, int ev, int i) {
+  if (p.trace && blockIdx.x == 0 && i < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[ev * 64 + i] = t;
+  }
+}
 
 // In-place pairwise tree: after the call a[0..N/G) hold sums of consecutive groups of G.
 template <int N, int G>
@@ -71,9 +80,12 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
 }
 
+// One 32-key group of one row: masked max -> 2^(l - max) (MUFU or exp2_poly) -> chunk sums.
+// Writes lam2 for chunks inside the group (C <= 32); returns the group's (max, sum) in log2
+// units so the caller can assemble larger chunks and the row's partial LSE.
 template <int C, int NP>
 __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32], int key0, int kvh, int rho,
-                                               bool row_ok, float& HM, float& HS, float& CM, float& CS) {
+                                               bool row_ok, float& gms_out, float& gs_out) {
   const float sc = p.scale;
   if (key0 + 32 > p.g.n_loc) {  // only the shard's last key tile (warp-uniform)
 #pragma unroll
@@ -100,42 +112,28 @@ __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32]
 #pragma unroll
   for (int i = 0; i < 32 / CG; ++i) cs[i] = v[i];
   tree_sum<32 / CG, 32 / CG>(v);
-  const float gs = v[0];
-  if (gs > 0.f) {  // running LSE of this row over the 128-key tile
-    if (HS == 0.f) {
-      HM = gms;
-      HS = gs;
-    } else {
-      const float nm = fmaxf(HM, gms);
-      HS = HS * fast_exp2(HM - nm) + gs * fast_exp2(gms - nm);
-      HM = nm;
-    }
-  }
-  float* lam = p.lam2 + (size_t)kvh * p.g.m_loc * p.g.R + rho;
+  gms_out = gms;
+  gs_out = v[0];
   if constexpr (C <= 32) {
+    float* lam = p.lam2 + (size_t)kvh * p.g.m_loc * p.g.R + rho;
 #pragma unroll
     for (int i = 0; i < 32 / C; ++i) {
       const int chunk = key0 / C + i;
       if (row_ok && chunk < p.g.m_loc)
         lam[(size_t)chunk * p.g.R] = (cs[i] > 0.f) ? gms + fast_log2(cs[i]) : -INFINITY;
     }
+  }
+}
+
+__device__ __forceinline__ void lse2_merge(float& M, float& S, float m, float s) {
+  if (s <= 0.f) return;
+  if (S <= 0.f) {
+    M = m;
+    S = s;
   } else {
-    if (gs > 0.f) {
-      if (CS == 0.f) {
-        CM = gms;
-        CS = gs;
-      } else {
-        const float nm = fmaxf(CM, gms);
-        CS = CS * fast_exp2(CM - nm) + gs * fast_exp2(gms - nm);
-        CM = nm;
-      }
-    }
-    if (((key0 + 32) % C) == 0) {
-      const int chunk = key0 / C;
-      if (row_ok && chunk < p.g.m_loc) lam[(size_t)chunk * p.g.R] = (CS > 0.f) ? CM + fast_log2(CS) : -INFINITY;
-      CM = -INFINITY;
-      CS = 0.f;
-    }
+    const float nm = fmaxf(M, m);
+    S = S * fast_exp2(M - nm) + s * fast_exp2(m - nm);
+    M = nm;
   }
 }
 
@@ -154,6 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 6;      // [MG]
   uint64_t* acc_empty = bars + 6 + MG;  // [MG]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * MG);
+  __shared__ float2 xchg[2 * 4 * 128];  // [iteration parity][column quarter][row]: (max, sum)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
@@ -168,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(q_empty, 1);
     for (int i = 0; i < MG; ++i) {
       ptx::mbar_init(&acc_full[i], 1);
-      ptx::mbar_init(&acc_empty[i], 4);
+      ptx::mbar_init(&acc_empty[i], kEpiWarps);
     }
     ptx::fence_mbar_init();
   }
@@ -202,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb = kcount & 1;
         ptx::mbar_wait(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
         ptx::mbar_expect_tx(&k_full[kb], kKBytes);
+        strace(p, 0, kcount);
         const int y = kvh * p.g.n_pad + kt * BN;
         uint8_t* dst = kbuf0 + kb * kKBytes;
         ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int kb = kcount & 1;
         ptx::mbar_wait(&k_full[kb], (kcount >> 1) & 1);
+        strace(p, 1, kcount);
         const uint32_t ka = ptx::smem_u32(kbuf0 + kb * kKBytes);
         for (int m = 0; m < nm; ++m) {
           ptx::mbar_wait(&acc_empty[m], ((acount[m] >> 0) & 1) ^ 1);
@@ -241,44 +242,77 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++acount[m];
         }
         ptx::mma_commit(&k_empty[kb]);
+        strace(p, 2, kcount);
         ++kcount;
       }
     }
   } else {
+    // all 16 epilogue warps drain one accumulator at a time (m = 0, 1, ...), so the MMA of the
+    // next key tile refills accumulator m while the others are being drained
     const int e = warp - 2;
-    const int m = e >> 2;        // accumulator / resident row tile of this warp group
-    const int quad = warp & 3;   // TMEM lane quadrant
-    int acount = 0;
+    const int quad = warp & 3;   // TMEM lane quadrant -> rows quad*32 .. +31
+    const int colq = e >> 2;     // key columns colq*32 .. +31 of the 128-key tile
+    const int rit = quad * 32 + lane;
+    int acount[MG] = {};
+    int it = 0;
     for (int u = u0; u < u1; ++u) {
       const int grp = u / p.NKT, kt = u % p.NKT;
       const int kvh = grp / p.NRG, rg = grp % p.NRG;
-      if (m >= min(MG, p.MT - rg * MG)) continue;  // this row group has fewer row tiles
-      ptx::mbar_wait(&acc_full[m], acount & 1);
-      ptx::tc_fence_after();
-      const int rho = (rg * MG + m) * BM + quad * 32 + lane;
-      const bool row_ok = rho < p.g.R;
-      float HM = -INFINITY, HS = 0.f, CM = -INFINITY, CS = 0.f;
-#pragma unroll 1
-      for (int gi = 0; gi < BN / 32; ++gi) {
-        const int col0 = gi * 32;
-        float v[32];
+      const int nm = min(MG, p.MT - rg * MG);
+      for (int m = 0; m < nm; ++m, ++it) {
+        ptx::mbar_wait(&acc_full[m], acount[m] & 1);
+        ++acount[m];
+        ptx::tc_fence_after();
+        const int rho = (rg * MG + m) * BM + rit;
+        const bool row_ok = rho < p.g.R;
+        const int key0 = kt * BN + colq * 32;
+        float gms = 0.f, gs = 0.f;
         if constexpr (NP == 11) {  // tuning skeleton: pipeline only
-          HS += 1.f;
+          gs = 1.f;
         } else {
-          ptx::tmem_ld32(tmem_base + (uint32_t)(m * BN + col0) + ((uint32_t)(quad * 32) << 16), v);
+          float v[32];
+          ptx::tmem_ld32(tmem_base + (uint32_t)(m * BN + colq * 32) + ((uint32_t)(quad * 32) << 16), v);
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);  // accumulator columns now in registers
           if constexpr (NP == 10) {  // tuning: TMEM drain only
-            HS += v[0] + v[31];
+            gs = v[0] + v[31];
           } else {
-            epilogue_group<C, NP>(p, v, kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
+            epilogue_group<C, NP>(p, v, key0, kvh, rho, row_ok, gms, gs);
           }
         }
+        if constexpr (NP == 11) {
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);
+        }
+        // exchange the four 32-key pieces of each row within the quadrant's warps
+        float2* xb = xchg + (it & 1) * (4 * 128);
+        xb[colq * 128 + rit] = make_float2(gms, gs);
+        ptx::named_bar_sync(1 + quad, 128);
+        if constexpr (C > 32) {  // chunks spanning several warps' pieces
+          constexpr int PW = C / 32;
+          if ((colq % PW) == 0) {
+            float CM = -INFINITY, CS = 0.f;
+#pragma unroll
+            for (int w = 0; w < PW; ++w) {
+              const float2 pc = xb[(colq + w) * 128 + rit];
+              lse2_merge(CM, CS, pc.x, pc.y);
+            }
+            const int chunk = key0 / C;
+            if (row_ok && chunk < p.g.m_loc)
+              p.lam2[((size_t)kvh * p.g.m_loc + chunk) * p.g.R + rho] = (CS > 0.f) ? CM + fast_log2(CS) : -INFINITY;
+          }
+        }
+        if (colq == 0) {  // the row's partial normaliser over this key tile
+          float HM = -INFINITY, HS = 0.f;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const float2 pc = xb[w * 128 + rit];
+            lse2_merge(HM, HS, pc.x, pc.y);
+          }
+          if (row_ok) p.lampart[((size_t)kvh * p.nsplit + kt) * p.g.R + rho] = (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
+        }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);
-      ++acount;
-      if (row_ok)
-        p.lampart[((size_t)kvh * p.nsplit + kt) * p.g.R + rho] = (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
     }
   }
   ptx::tc_fence_before();
@@ -287,6 +321,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem_base);
   }
+}
+
+__global__ void trace_start_kernel(unsigned long long* t) {
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(*t));
 }
 
 // GQA row packing: qpack[kvh][rho][x] = q[r][kvh*G + g][x], rho = g*ns + r, zero rows past R.
@@ -325,7 +363,32 @@ cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPa
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  score_tc_kernel<C, NP><<<grid, kThreads, kSmem, st>>>(tmK, tmQ, p);
+  static int trace_mode = -1;
+  static unsigned long long* tbuf = nullptr;
+  if (trace_mode < 0) {
+    const char* ev = getenv("CKV_SCORE_TRACE");
+    trace_mode = (ev && ev[0] == '1') ? 1 : 0;
+    if (trace_mode) cudaMalloc(&tbuf, 7 * 64 * sizeof(unsigned long long));
+  }
+  TcParams pp = p;
+  pp.trace = tbuf;
+  if (tbuf) cudaMemsetAsync(tbuf, 0, 7 * 64 * sizeof(unsigned long long), st);
+  if (tbuf) {  // kernel start reference: recorded by a 1-thread marker launched just before
+    trace_start_kernel<<<1, 1, 0, st>>>(tbuf + 6 * 64);
+  }
+  score_tc_kernel<C, NP><<<grid, kThreads, kSmem, st>>>(tmK, tmQ, pp);
+  if (tbuf) {
+    unsigned long long h[7 * 64];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost);
+    const unsigned long long t0 = h[6 * 64];
+    const char* nm[6] = {"k_issue", "k_full", "mma_done", "acc0_full", "acc3_full", "acc0_free"};
+    for (int e = 0; e < 6; ++e) {
+      fprintf(stderr, "[score trace] %-9s", nm[e]);
+      for (int i = 0; i < 14; ++i) fprintf(stderr, " %6.2f", h[e * 64 + i] ? (h[e * 64 + i] - t0) * 1e-3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+  }
   return cudaGetLastError();
 }
 
