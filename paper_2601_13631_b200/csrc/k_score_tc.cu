@@ -26,10 +26,11 @@
 namespace ckv {
 namespace {
 
-constexpr int BM = 128, BN = 128, D = 128, MG = 4;
-constexpr int kEpiWarps = 16;  // 4 lane quadrants x 4 column quarters of the 128-key tile
+constexpr int BM = 128, BN = 256, D = 128, MG = 2;
+constexpr int kEpiWarps = 16;  // 4 lane quadrants x 4 column quarters of the key tile
+constexpr int QC = BN / 4;     // key columns per epilogue warp
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr uint32_t kKBytes = BN * D * 2;  // 32 KB
+constexpr uint32_t kKBytes = BN * D * 2;  // 64 KB
 constexpr uint32_t kQBytes = BM * D * 2;  // 32 KB per row tile
 constexpr size_t kSmem = 2 * kKBytes + MG * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
 
@@ -265,42 +266,61 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         const int rho = (rg * MG + m) * BM + rit;
         const bool row_ok = rho < p.g.R;
-        const int key0 = kt * BN + colq * 32;
-        float gms = 0.f, gs = 0.f;
+        // this warp: key columns [colq*QC, (colq+1)*QC) of the tile, in 32-key groups
+        const int key0 = kt * BN + colq * QC;
+        float gms = -INFINITY, gs = 0.f;  // (max, sum) of the warp's QC keys for this row
+        float CM = -INFINITY, CS = 0.f;   // running chunk piece for 32 < C <= QC
         if constexpr (NP == 11) {  // tuning skeleton: pipeline only
+          gms = 0.f;
           gs = 1.f;
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);
         } else {
-          float v[32];
-          ptx::tmem_ld32(tmem_base + (uint32_t)(m * BN + colq * 32) + ((uint32_t)(quad * 32) << 16), v);
+          float v[QC / 32][32];
+#pragma unroll
+          for (int gi = 0; gi < QC / 32; ++gi)
+            ptx::tmem_ld32(tmem_base + (uint32_t)(m * BN + colq * QC + gi * 32) + ((uint32_t)(quad * 32) << 16), v[gi]);
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);  // accumulator columns now in registers
-          if constexpr (NP == 10) {  // tuning: TMEM drain only
-            gs = v[0] + v[31];
-          } else {
-            epilogue_group<C, NP>(p, v, key0, kvh, rho, row_ok, gms, gs);
+#pragma unroll
+          for (int gi = 0; gi < QC / 32; ++gi) {
+            float g_m = 0.f, g_s = 0.f;
+            if constexpr (NP == 10) {  // tuning: TMEM drain only
+              g_s = v[gi][0] + v[gi][31];
+            } else {
+              epilogue_group<C, NP>(p, v[gi], key0 + gi * 32, kvh, rho, row_ok, g_m, g_s);
+            }
+            lse2_merge(gms, gs, g_m, g_s);
+            if constexpr (C > 32 && C <= QC) {  // chunk spans groups of this warp only
+              lse2_merge(CM, CS, g_m, g_s);
+              if (((gi + 1) * 32) % C == 0) {
+                const int chunk = (key0 + gi * 32) / C;
+                if (row_ok && chunk < p.g.m_loc)
+                  p.lam2[((size_t)kvh * p.g.m_loc + chunk) * p.g.R + rho] =
+                      (CS > 0.f) ? CM + fast_log2(CS) : -INFINITY;
+                CM = -INFINITY;
+                CS = 0.f;
+              }
+            }
           }
         }
-        if constexpr (NP == 11) {
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);
-        }
-        // exchange the four 32-key pieces of each row within the quadrant's warps
+        // exchange the four QC-key pieces of each row within the quadrant's warps
         float2* xb = xchg + (it & 1) * (4 * 128);
         xb[colq * 128 + rit] = make_float2(gms, gs);
         ptx::named_bar_sync(1 + quad, 128);
-        if constexpr (C > 32) {  // chunks spanning several warps' pieces
-          constexpr int PW = C / 32;
+        if constexpr (C > QC) {  // chunks spanning several warps' pieces
+          constexpr int PW = C / QC;
           if ((colq % PW) == 0) {
-            float CM = -INFINITY, CS = 0.f;
+            float M2 = -INFINITY, S2 = 0.f;
 #pragma unroll
             for (int w = 0; w < PW; ++w) {
               const float2 pc = xb[(colq + w) * 128 + rit];
-              lse2_merge(CM, CS, pc.x, pc.y);
+              lse2_merge(M2, S2, pc.x, pc.y);
             }
             const int chunk = key0 / C;
             if (row_ok && chunk < p.g.m_loc)
-              p.lam2[((size_t)kvh * p.g.m_loc + chunk) * p.g.R + rho] = (CS > 0.f) ? CM + fast_log2(CS) : -INFINITY;
+              p.lam2[((size_t)kvh * p.g.m_loc + chunk) * p.g.R + rho] = (S2 > 0.f) ? M2 + fast_log2(S2) : -INFINITY;
           }
         }
         if (colq == 0) {  // the row's partial normaliser over this key tile
