@@ -27,8 +27,8 @@ namespace ckv {
 namespace {
 
 constexpr int BM = 128, BN = 256, D = 128, MG = 2;
-constexpr int kEpiWarps = 16;  // 4 lane quadrants x 4 column quarters of the key tile
-constexpr int QC = BN / 4;     // key columns per epilogue warp
+constexpr int kEpiWarps = 16;  // 2 groups (one per accumulator) x 4 lane quadrants x 2 column halves
+constexpr int QC = BN / 2;     // key columns per epilogue warp
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kKBytes = BN * D * 2;  // 64 KB
 constexpr uint32_t kQBytes = BM * D * 2;  // 32 KB per row tile
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 6;      // [MG]
   uint64_t* acc_empty = bars + 6 + MG;  // [MG]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * MG);
-  __shared__ float2 xchg[2 * 4 * 128];  // [iteration parity][column quarter][row]: (max, sum)
+  __shared__ float2 xchg[2 * MG * 2 * 128];  // [iteration parity][group][column half][row]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::mbar_init(q_empty, 1);
     for (int i = 0; i < MG; ++i) {
       ptx::mbar_init(&acc_full[i], 1);
-      ptx::mbar_init(&acc_empty[i], kEpiWarps);
+      ptx::mbar_init(&acc_empty[i], kEpiWarps / MG);
     }
     ptx::fence_mbar_init();
   }
@@ -248,21 +248,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // all 16 epilogue warps drain one accumulator at a time (m = 0, 1, ...), so the MMA of the
-    // next key tile refills accumulator m while the others are being drained
+    // warp group m (8 warps: 4 lane quadrants x 2 column halves) drains accumulator m; the two
+    // groups run out of phase (their accumulators complete one M-tile MMA apart), so one
+    // group's exponentials overlap the other's reductions on every SM sub-partition
     const int e = warp - 2;
-    const int quad = warp & 3;   // TMEM lane quadrant -> rows quad*32 .. +31
-    const int colq = e >> 2;     // key columns colq*32 .. +31 of the 128-key tile
+    const int m = e >> 3;               // accumulator / resident row tile of this warp group
+    const int quad = warp & 3;          // TMEM lane quadrant -> rows quad*32 .. +31
+    const int colq = (e >> 2) & 1;      // key columns colq*QC .. +QC-1 of the tile
     const int rit = quad * 32 + lane;
-    int acount[MG] = {};
+    const uint32_t bar_id = 1 + m * 4 + quad;  // the 2 warps sharing (group, quadrant)
+    int acount = 0;
     int it = 0;
     for (int u = u0; u < u1; ++u) {
       const int grp = u / p.NKT, kt = u % p.NKT;
       const int kvh = grp / p.NRG, rg = grp % p.NRG;
       const int nm = min(MG, p.MT - rg * MG);
-      for (int m = 0; m < nm; ++m, ++it) {
-        ptx::mbar_wait(&acc_full[m], acount[m] & 1);
-        ++acount[m];
+      if (m < nm) {
+        ++it;
+        ptx::mbar_wait(&acc_full[m], acount & 1);
+        ++acount;
         ptx::tc_fence_after();
         const int rho = (rg * MG + m) * BM + rit;
         const bool row_ok = rho < p.g.R;
@@ -305,10 +309,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        // exchange the four QC-key pieces of each row within the quadrant's warps
-        float2* xb = xchg + (it & 1) * (4 * 128);
+        // exchange the two QC-key pieces of each row within the (group, quadrant) warp pair
+        float2* xb = xchg + ((it & 1) * MG + m) * (2 * 128);
         xb[colq * 128 + rit] = make_float2(gms, gs);
-        ptx::named_bar_sync(1 + quad, 128);
+        ptx::named_bar_sync(bar_id, 64);
         if constexpr (C > QC) {  // chunks spanning several warps' pieces
           constexpr int PW = C / QC;
           if ((colq % PW) == 0) {
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (colq == 0) {  // the row's partial normaliser over this key tile
           float HM = -INFINITY, HS = 0.f;
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
+          for (int w = 0; w < 2; ++w) {
             const float2 pc = xb[w * 128 + rit];
             lse2_merge(HM, HS, pc.x, pc.y);
           }
