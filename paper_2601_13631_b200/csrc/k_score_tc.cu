@@ -5,18 +5,16 @@
 // (Q2-Q5), and per (row, 64-key quarter tile) a partial base-2 LSE.
 //
 // Layout / schedule (persistent, one CTA per SM, 576 threads):
-//   Work unit = (kv head, row group, 128-key tile); a row group is up to MG = 4 GQA-packed
-//   128-row tiles of Q, kept resident in shared memory (MG x 32 KB) while the CTA streams its
-//   contiguous range of key tiles, so neither Q nor K is re-read per row tile.
-//   warp 0      TMA producer: the row group's Q tiles once per group; K tiles [128 keys x 128]
-//               (32 KB, double-buffered), 128-byte swizzle.
-//   warp 1      TMEM allocator + single-thread MMA issuer: one D[128 x 128] fp32 accumulator
-//               per resident row tile (4 x 128 = all 512 TMEM columns), 8 x tcgen05.mma
-//               kind::f16 (K = 16) per accumulator.
-//   warps 2..17 epilogue: warp group g (4 warps, one per TMEM lane quadrant) drains
-//               accumulator g: one suffix row per thread, tcgen05.ld 32 columns at a time;
-//               per-chunk LSE in registers, coalesced lam2 stores ([kvh][chunk][row] layout),
-//               one partial row LSE per (row, key tile).
+//   warp 0      TMA producer: K tiles [256 keys x 128] (64 KB, double-buffered, loaded once per
+//               (kv head, key tile) = K-stationary) and Q tiles [128 rows x 128] (32 KB, 2 stages)
+//               from a GQA-packed Q [Hkv][R_pad][128]; 128-byte swizzle.
+//   warp 1      TMEM allocator + single-thread MMA issuer: D[128 x 256] fp32 in TMEM
+//               (two accumulators = all 512 columns), 8 x tcgen05.mma kind::f16 (K = 16 each).
+//   warps 2..17 epilogue: tcgen05.ld 32 columns at a time, one suffix row per thread (TMEM lane),
+//               four warps per lane quadrant (64 columns each); per-chunk LSE in registers,
+//               coalesced lam2 stores ([kvh][chunk][row] layout).
+// Work units (kv head, key tile, row tile) are linearised with the row tile fastest and split
+// into contiguous ranges per CTA, so each K tile crosses HBM about once.
 #include <cstdio>
 #include <cstdlib>
 
@@ -26,35 +24,25 @@
 namespace ckv {
 namespace {
 
-constexpr int BM = 128, BN = 256, D = 128, MG = 2;
-constexpr int kEpiWarps = 16;  // 2 groups (one per accumulator) x 4 lane quadrants x 2 column halves
-constexpr int QC = BN / 2;     // key columns per epilogue warp
+constexpr int BM = 128, BN = 256, D = 128;
+constexpr int kEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 key columns each
+constexpr int kColSplit = kEpiWarps / 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr uint32_t kKBytes = BN * D * 2;  // 64 KB
-constexpr uint32_t kQBytes = BM * D * 2;  // 32 KB per row tile
-constexpr size_t kSmem = 2 * kKBytes + MG * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t kKBytes = BN * D * 2;  // 65536
+constexpr uint32_t kQBytes = BM * D * 2;  // 32768
+constexpr size_t kSmem = 2 * kKBytes + 2 * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 struct TcParams {
   LayerGeom g;
   float* lam2;
   float* lampart;
-  int nsplit;   // = NKT (one partial row LSE per key tile)
+  int nsplit;   // = 2 * NKT
   int NKT;      // key tiles per kv head
   int MT;       // row tiles per kv head
-  int NRG;      // row groups per kv head
   int R_pad;
-  int n_units;  // Hkv * NRG * NKT
+  int n_units;  // Hkv * NKT * MT
   float scale;  // log2(e) / sqrt(d)
-  unsigned long long* trace;  // debug (CKV_SCORE_TRACE=1): %globaltimer events of CTA 0, else null
 };
-
-__device__ __forceinline__ void strace(const TcParams& p, int ev, int i) {
-  if (p.trace && blockIdx.x == 0 && i < 64) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[ev * 64 + i] = t;
-  }
-}
 
 // In-place pairwise tree: after the call a[0..N/G) hold sums of consecutive groups of G.
 template <int N, int G>
@@ -81,12 +69,9 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
 }
 
-// One 32-key group of one row: masked max -> 2^(l - max) (MUFU or exp2_poly) -> chunk sums.
-// Writes lam2 for chunks inside the group (C <= 32); returns the group's (max, sum) in log2
-// units so the caller can assemble larger chunks and the row's partial LSE.
 template <int C, int NP>
 __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32], int key0, int kvh, int rho,
-                                               bool row_ok, float& gms_out, float& gs_out) {
+                                               bool row_ok, float& HM, float& HS, float& CM, float& CS) {
   const float sc = p.scale;
   if (key0 + 32 > p.g.n_loc) {  // only the shard's last key tile (warp-uniform)
 #pragma unroll
@@ -113,28 +98,42 @@ __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32]
 #pragma unroll
   for (int i = 0; i < 32 / CG; ++i) cs[i] = v[i];
   tree_sum<32 / CG, 32 / CG>(v);
-  gms_out = gms;
-  gs_out = v[0];
+  const float gs = v[0];
+  if (gs > 0.f) {  // running LSE of this warp's 64-key quarter tile
+    if (HS == 0.f) {
+      HM = gms;
+      HS = gs;
+    } else {
+      const float nm = fmaxf(HM, gms);
+      HS = HS * fast_exp2(HM - nm) + gs * fast_exp2(gms - nm);
+      HM = nm;
+    }
+  }
+  float* lam = p.lam2 + (size_t)kvh * p.g.m_loc * p.g.R + rho;
   if constexpr (C <= 32) {
-    float* lam = p.lam2 + (size_t)kvh * p.g.m_loc * p.g.R + rho;
 #pragma unroll
     for (int i = 0; i < 32 / C; ++i) {
       const int chunk = key0 / C + i;
       if (row_ok && chunk < p.g.m_loc)
         lam[(size_t)chunk * p.g.R] = (cs[i] > 0.f) ? gms + fast_log2(cs[i]) : -INFINITY;
     }
-  }
-}
-
-__device__ __forceinline__ void lse2_merge(float& M, float& S, float m, float s) {
-  if (s <= 0.f) return;
-  if (S <= 0.f) {
-    M = m;
-    S = s;
   } else {
-    const float nm = fmaxf(M, m);
-    S = S * fast_exp2(M - nm) + s * fast_exp2(m - nm);
-    M = nm;
+    if (gs > 0.f) {
+      if (CS == 0.f) {
+        CM = gms;
+        CS = gs;
+      } else {
+        const float nm = fmaxf(CM, gms);
+        CS = CS * fast_exp2(CM - nm) + gs * fast_exp2(gms - nm);
+        CM = nm;
+      }
+    }
+    if (((key0 + 32) % C) == 0) {
+      const int chunk = key0 / C;
+      if (row_ok && chunk < p.g.m_loc) lam[(size_t)chunk * p.g.R] = (CS > 0.f) ? CM + fast_log2(CS) : -INFINITY;
+      CM = -INFINITY;
+      CS = 0.f;
+    }
   }
 }
 
@@ -145,15 +144,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* kbuf0 = smem;
   uint8_t* qbuf0 = smem + 2 * kKBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kKBytes + MG * kQBytes);
-  uint64_t* k_full = bars + 0;        // [2]
-  uint64_t* k_empty = bars + 2;       // [2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kKBytes + 2 * kQBytes);
+  uint64_t* k_full = bars + 0;
+  uint64_t* k_empty = bars + 2;
   uint64_t* q_full = bars + 4;
-  uint64_t* q_empty = bars + 5;
-  uint64_t* acc_full = bars + 6;      // [MG]
-  uint64_t* acc_empty = bars + 6 + MG;  // [MG]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 + 2 * MG);
-  __shared__ float2 xchg[2 * MG * 2 * 128];  // [iteration parity][group][column half][row]
+  uint64_t* q_empty = bars + 6;
+  uint64_t* acc_full = bars + 8;
+  uint64_t* acc_empty = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
@@ -163,12 +161,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
-    }
-    ptx::mbar_init(q_full, 1);
-    ptx::mbar_init(q_empty, 1);
-    for (int i = 0; i < MG; ++i) {
+      ptx::mbar_init(&q_full[i], 1);
+      ptx::mbar_init(&q_empty[i], 1);
       ptx::mbar_init(&acc_full[i], 1);
-      ptx::mbar_init(&acc_empty[i], kEpiWarps / MG);
+      ptx::mbar_init(&acc_empty[i], kEpiWarps);
     }
     ptx::fence_mbar_init();
   }
@@ -184,159 +180,108 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tma_prefetch_desc(&tmQ);
       int kcount = 0, qcount = 0, cur = -1;
       for (int u = u0; u < u1; ++u) {
-        const int grp = u / p.NKT, kt = u % p.NKT;
-        const int kvh = grp / p.NRG, rg = grp % p.NRG;
-        if (grp != cur) {  // new row group: its Q tiles, once
-          const int nm = min(MG, p.MT - rg * MG);
-          ptx::mbar_wait(q_empty, (qcount & 1) ^ 1);
-          ptx::mbar_expect_tx(q_full, nm * kQBytes);
-          for (int m = 0; m < nm; ++m) {
-            const int yq = kvh * p.R_pad + (rg * MG + m) * BM;
-            uint8_t* dq = qbuf0 + m * kQBytes;
-            ptx::tma_load_2d(dq, &tmQ, q_full, 0, yq);
-            ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, q_full, 64, yq);
-          }
-          cur = grp;
-          ++qcount;
+        const int pr = u / p.MT, mt = u % p.MT;
+        const int kvh = pr / p.NKT, kt = pr % p.NKT;
+        if (pr != cur) {
+          const int kb = kcount & 1;
+          ptx::mbar_wait(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
+          ptx::mbar_expect_tx(&k_full[kb], kKBytes);
+          const int y = kvh * p.g.n_pad + kt * BN;
+          uint8_t* dst = kbuf0 + kb * kKBytes;
+          ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
+          ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
+          cur = pr;
+          ++kcount;
         }
-        const int kb = kcount & 1;
-        ptx::mbar_wait(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
-        ptx::mbar_expect_tx(&k_full[kb], kKBytes);
-        strace(p, 0, kcount);
-        const int y = kvh * p.g.n_pad + kt * BN;
-        uint8_t* dst = kbuf0 + kb * kKBytes;
-        ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
-        ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
-        ++kcount;
+        const int qs = qcount & 1;
+        ptx::mbar_wait(&q_empty[qs], ((qcount >> 1) & 1) ^ 1);
+        ptx::mbar_expect_tx(&q_full[qs], kQBytes);
+        const int yq = kvh * p.R_pad + mt * BM;
+        uint8_t* dq = qbuf0 + qs * kQBytes;
+        ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
+        ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
+        ++qcount;
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
-      int kcount = 0, qcount = 0, cur = -1, nm = 0;
-      int acount[MG] = {};
+      int kcount = 0, qcount = 0, acount = 0, cur = -1, kb = 0;
       for (int u = u0; u < u1; ++u) {
-        const int grp = u / p.NKT;
-        if (grp != cur) {
-          if (cur >= 0) ptx::mma_commit(q_empty);  // previous row group's Q fully consumed
-          nm = min(MG, p.MT - (grp % p.NRG) * MG);
-          ptx::mbar_wait(q_full, qcount & 1);
-          ++qcount;
-          cur = grp;
+        const int pr = u / p.MT;
+        if (pr != cur) {
+          kb = kcount & 1;
+          ptx::mbar_wait(&k_full[kb], (kcount >> 1) & 1);
+          ++kcount;
+          cur = pr;
         }
-        const int kb = kcount & 1;
-        ptx::mbar_wait(&k_full[kb], (kcount >> 1) & 1);
-        strace(p, 1, kcount);
+        const int qs = qcount & 1;
+        ptx::mbar_wait(&q_full[qs], (qcount >> 1) & 1);
+        const int ab = acount & 1;
+        ptx::mbar_wait(&acc_empty[ab], ((acount >> 1) & 1) ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + ab * BN;
+        const uint32_t qa = ptx::smem_u32(qbuf0 + qs * kQBytes);
         const uint32_t ka = ptx::smem_u32(kbuf0 + kb * kKBytes);
-        for (int m = 0; m < nm; ++m) {
-          ptx::mbar_wait(&acc_empty[m], ((acount[m] >> 0) & 1) ^ 1);
-          ptx::tc_fence_after();
-          const uint32_t qa = ptx::smem_u32(qbuf0 + m * kQBytes);
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
-            const uint32_t offk = (k >> 2) * (kKBytes / 2) + (k & 3) * 32;
-            ptx::mma_bf16(tmem_base + m * BN, ptx::umma_desc_sw128(qa + off), ptx::umma_desc_sw128(ka + offk), idesc,
-                          k > 0 ? 1u : 0u);
-          }
-          ptx::mma_commit(&acc_full[m]);
-          ++acount[m];
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
+          const uint32_t off_k = (k >> 2) * (kKBytes / 2) + (k & 3) * 32;
+          ptx::mma_bf16(d_tmem, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k), idesc,
+                        k > 0 ? 1u : 0u);
         }
-        ptx::mma_commit(&k_empty[kb]);
-        strace(p, 2, kcount);
-        ++kcount;
+        ptx::mma_commit(&q_empty[qs]);
+        ptx::mma_commit(&acc_full[ab]);
+        const bool last_of_pair = (u + 1 == u1) || ((u + 1) / p.MT != pr);
+        if (last_of_pair) ptx::mma_commit(&k_empty[kb]);
+        ++qcount;
+        ++acount;
       }
     }
   } else {
-    // warp group m (8 warps: 4 lane quadrants x 2 column halves) drains accumulator m; the two
-    // groups run out of phase (their accumulators complete one M-tile MMA apart), so one
-    // group's exponentials overlap the other's reductions on every SM sub-partition
     const int e = warp - 2;
-    const int m = e >> 3;               // accumulator / resident row tile of this warp group
-    const int quad = warp & 3;          // TMEM lane quadrant -> rows quad*32 .. +31
-    const int colq = (e >> 2) & 1;      // key columns colq*QC .. +QC-1 of the tile
-    const int rit = quad * 32 + lane;
-    const uint32_t bar_id = 1 + m * 4 + quad;  // the 2 warps sharing (group, quadrant)
+    const int quad = warp & 3;
+    const int half = e >> 2;  // column quarter
+    const int row_in_tile = quad * 32 + lane;
     int acount = 0;
-    int it = 0;
     for (int u = u0; u < u1; ++u) {
-      const int grp = u / p.NKT, kt = u % p.NKT;
-      const int kvh = grp / p.NRG, rg = grp % p.NRG;
-      const int nm = min(MG, p.MT - rg * MG);
-      if (m < nm) {
-        ++it;
-        ptx::mbar_wait(&acc_full[m], acount & 1);
-        ++acount;
-        ptx::tc_fence_after();
-        const int rho = (rg * MG + m) * BM + rit;
-        const bool row_ok = rho < p.g.R;
-        // this warp: key columns [colq*QC, (colq+1)*QC) of the tile, in 32-key groups
-        const int key0 = kt * BN + colq * QC;
-        float gms = -INFINITY, gs = 0.f;  // (max, sum) of the warp's QC keys for this row
-        float CM = -INFINITY, CS = 0.f;   // running chunk piece for 32 < C <= QC
+      const int pr = u / p.MT, mt = u % p.MT;
+      const int kvh = pr / p.NKT, kt = pr % p.NKT;
+      const int ab = acount & 1;
+      ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
+      ptx::tc_fence_after();
+      const int rho = mt * BM + row_in_tile;
+      const bool row_ok = rho < p.g.R;
+      float HM = -INFINITY, HS = 0.f, CM = -INFINITY, CS = 0.f;
+      // both 32-key groups are read from TMEM first (the accumulator is then released early)
+      // and processed in one unrolled block, so the compiler can overlap the two groups'
+      // exponentials with their reductions
+      float v[BN / kColSplit / 32][32];
+      if constexpr (NP != 11) {
+#pragma unroll
+        for (int gi = 0; gi < BN / kColSplit / 32; ++gi)
+          ptx::tmem_ld32(tmem_base + (uint32_t)(ab * BN + half * (BN / kColSplit) + gi * 32) +
+                             ((uint32_t)(quad * 32) << 16),
+                         v[gi]);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
+#pragma unroll
+      for (int gi = 0; gi < BN / kColSplit / 32; ++gi) {
+        const int col0 = half * (BN / kColSplit) + gi * 32;
         if constexpr (NP == 11) {  // tuning skeleton: pipeline only
-          gms = 0.f;
-          gs = 1.f;
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);
+          HS += 1.f;
+        } else if constexpr (NP == 10) {  // tuning: TMEM drain only
+          HS += v[gi][0] + v[gi][31];
         } else {
-          float v[QC / 32][32];
-#pragma unroll
-          for (int gi = 0; gi < QC / 32; ++gi)
-            ptx::tmem_ld32(tmem_base + (uint32_t)(m * BN + colq * QC + gi * 32) + ((uint32_t)(quad * 32) << 16), v[gi]);
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&acc_empty[m]);  // accumulator columns now in registers
-#pragma unroll
-          for (int gi = 0; gi < QC / 32; ++gi) {
-            float g_m = 0.f, g_s = 0.f;
-            if constexpr (NP == 10) {  // tuning: TMEM drain only
-              g_s = v[gi][0] + v[gi][31];
-            } else {
-              epilogue_group<C, NP>(p, v[gi], key0 + gi * 32, kvh, rho, row_ok, g_m, g_s);
-            }
-            lse2_merge(gms, gs, g_m, g_s);
-            if constexpr (C > 32 && C <= QC) {  // chunk spans groups of this warp only
-              lse2_merge(CM, CS, g_m, g_s);
-              if (((gi + 1) * 32) % C == 0) {
-                const int chunk = (key0 + gi * 32) / C;
-                if (row_ok && chunk < p.g.m_loc)
-                  p.lam2[((size_t)kvh * p.g.m_loc + chunk) * p.g.R + rho] =
-                      (CS > 0.f) ? CM + fast_log2(CS) : -INFINITY;
-                CM = -INFINITY;
-                CS = 0.f;
-              }
-            }
-          }
-        }
-        // exchange the two QC-key pieces of each row within the (group, quadrant) warp pair
-        float2* xb = xchg + ((it & 1) * MG + m) * (2 * 128);
-        xb[colq * 128 + rit] = make_float2(gms, gs);
-        ptx::named_bar_sync(bar_id, 64);
-        if constexpr (C > QC) {  // chunks spanning several warps' pieces
-          constexpr int PW = C / QC;
-          if ((colq % PW) == 0) {
-            float M2 = -INFINITY, S2 = 0.f;
-#pragma unroll
-            for (int w = 0; w < PW; ++w) {
-              const float2 pc = xb[(colq + w) * 128 + rit];
-              lse2_merge(M2, S2, pc.x, pc.y);
-            }
-            const int chunk = key0 / C;
-            if (row_ok && chunk < p.g.m_loc)
-              p.lam2[((size_t)kvh * p.g.m_loc + chunk) * p.g.R + rho] = (S2 > 0.f) ? M2 + fast_log2(S2) : -INFINITY;
-          }
-        }
-        if (colq == 0) {  // the row's partial normaliser over this key tile
-          float HM = -INFINITY, HS = 0.f;
-#pragma unroll
-          for (int w = 0; w < 2; ++w) {
-            const float2 pc = xb[w * 128 + rit];
-            lse2_merge(HM, HS, pc.x, pc.y);
-          }
-          if (row_ok) p.lampart[((size_t)kvh * p.nsplit + kt) * p.g.R + rho] = (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
+          epilogue_group<C, NP>(p, v[gi], kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
         }
       }
+      if (row_ok)
+        p.lampart[((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho] =
+            (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
+      ++acount;
     }
   }
   ptx::tc_fence_before();
@@ -345,10 +290,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem_base);
   }
-}
-
-__global__ void trace_start_kernel(unsigned long long* t) {
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(*t));
 }
 
 // GQA row packing: qpack[kvh][rho][x] = q[r][kvh*G + g][x], rho = g*ns + r, zero rows past R.
@@ -387,32 +328,7 @@ cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPa
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  static int trace_mode = -1;
-  static unsigned long long* tbuf = nullptr;
-  if (trace_mode < 0) {
-    const char* ev = getenv("CKV_SCORE_TRACE");
-    trace_mode = (ev && ev[0] == '1') ? 1 : 0;
-    if (trace_mode) cudaMalloc(&tbuf, 7 * 64 * sizeof(unsigned long long));
-  }
-  TcParams pp = p;
-  pp.trace = tbuf;
-  if (tbuf) cudaMemsetAsync(tbuf, 0, 7 * 64 * sizeof(unsigned long long), st);
-  if (tbuf) {  // kernel start reference: recorded by a 1-thread marker launched just before
-    trace_start_kernel<<<1, 1, 0, st>>>(tbuf + 6 * 64);
-  }
-  score_tc_kernel<C, NP><<<grid, kThreads, kSmem, st>>>(tmK, tmQ, pp);
-  if (tbuf) {
-    unsigned long long h[7 * 64];
-    cudaStreamSynchronize(st);
-    cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost);
-    const unsigned long long t0 = h[6 * 64];
-    const char* nm[6] = {"k_issue", "k_full", "mma_done", "acc0_full", "acc3_full", "acc0_free"};
-    for (int e = 0; e < 6; ++e) {
-      fprintf(stderr, "[score trace] %-9s", nm[e]);
-      for (int i = 0; i < 14; ++i) fprintf(stderr, " %6.2f", h[e * 64 + i] ? (h[e * 64 + i] - t0) * 1e-3 : -1.0);
-      fprintf(stderr, "\n");
-    }
-  }
+  score_tc_kernel<C, NP><<<grid, kThreads, kSmem, st>>>(tmK, tmQ, p);
   return cudaGetLastError();
 }
 
@@ -442,8 +358,8 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
 
 int score_tc_nsplit(const LayerGeom& g) {
   if (g.d != D) return 0;
-  if (g.c < 1 || g.c > BN || (BN % g.c) != 0) return 0;
-  return (g.n_loc + BN - 1) / BN;
+  if (g.c < 1 || g.c > BN / kColSplit || ((BN / kColSplit) % g.c) != 0) return 0;
+  return kColSplit * ((g.n_loc + BN - 1) / BN);
 }
 
 size_t score_tc_qpack_elems(int Hkv, int R_max) { return (size_t)Hkv * ((R_max + BM - 1) / BM) * BM * D; }
@@ -456,18 +372,17 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   p.lam2 = lam2;
   p.lampart = lampart;
   p.nsplit = nsplit;
-  p.NKT = nsplit;
+  p.NKT = nsplit / kColSplit;
   p.MT = (g.R + BM - 1) / BM;
   p.R_pad = p.MT * BM;
-  p.NRG = (p.MT + MG - 1) / MG;
-  p.n_units = g.Hkv * p.NRG * p.NKT;
+  p.n_units = g.Hkv * p.NKT * p.MT;
   p.scale = kLog2e / sqrtf((float)g.d);
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
   pack_q_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap tmK, tmQ;
-  if (!make_tmap_bf16_2d(&tmK, probe_layer, D, (uint64_t)g.Hkv * g.n_pad, BN)) return cudaErrorInvalidValue;  // box 64 x 128
+  if (!make_tmap_bf16_2d(&tmK, probe_layer, D, (uint64_t)g.Hkv * g.n_pad, BN)) return cudaErrorInvalidValue;
   if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) return cudaErrorInvalidValue;
   const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
   switch (g.c) {
@@ -478,7 +393,6 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
     case 16: return launch_c<16>(tmK, tmQ, p, grid, st);
     case 32: return launch_c<32>(tmK, tmQ, p, grid, st);
     case 64: return launch_c<64>(tmK, tmQ, p, grid, st);
-    case 128: return launch_c<128>(tmK, tmQ, p, grid, st);
     default: return cudaErrorNotSupported;
   }
 }
