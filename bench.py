@@ -5,7 +5,8 @@
 
 Workload (config.workload): Qwen2.5-7B shape, 28 layers, 28 Q / 4 KV heads, d = 128,
 32K-token prefix, chunk 16, 128-token suffix, 10% budget (k = 204), bf16, inter-layer
-speculative prefetch on (quota k), HBM chunk cache of 2k + quota slots per layer,
+speculative prefetch on (quota k), HBM chunk cache of k + quota + k/2 slots per layer
+(~25% of the 2048 chunks of a layer),
 R = 8 distinct requests cycling over the shared prefix (synthetic, seed 42).
 A step = one request's Re-Prefill over all 28 layers (A1-A9 each layer).
 value = effective KV GB/s = (probe-K + kept K+V + suffix K+V bytes per layer) x layers
@@ -174,9 +175,11 @@ def run_ckv(args, rank, world):
     cfg = CONFIGS[CFG_NAME]
     k = ckv.ckv_budget_chunks(cfg.prefix_len, cfg.chunk_size, cfg.budget_bp)
     quota = k if args.prefetch else 0
+    cache_slots = k + quota + k // 2
     ctx = ckv.Context(cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.chunk_size,
                       cfg.prefix_len, cfg.suffix_len, dtype=cfg.dtype, budget_bp=cfg.budget_bp,
-                      prefetch_chunks=quota, device=local_rank, shard_index=rank, num_shards=world)
+                      prefetch_chunks=quota, cache_slots=cache_slots, device=local_rank, shard_index=rank,
+                      num_shards=world)
     dt = ctx.torch_dtype
     for l in range(cfg.num_layers):
         kp, vp = make_prefix(cfg, l)
@@ -287,6 +290,17 @@ def run_ckv(args, rank, world):
             host_ids[l].copy_(ids[l], non_blocking=True)
 
     ms_e2e = timed(e2e_step, args.steps) / args.steps
+
+    # cold HBM cache: every step starts from an empty chunk cache (all selected chunks cross the
+    # host link; speculative prefetch still overlaps the next layer's loads)
+    cold_ms = []
+    ctx.reset_stats()
+    for i in range(min(args.steps, 5)):
+        ctx.reset_cache()
+        torch.cuda.synchronize()
+        cold_ms.append(timed(main_step, 1))
+    cold_stats = ctx.get_stats()
+    cold_layers = max(cold_stats["total_layers"], 1)
     h2d = sum(t.numel() * t.element_size() for lay in reqs_host[0] for t in lay)
     d2h = L * (outs[0].numel() * outs[0].element_size() + k * 4)
 
@@ -325,7 +339,7 @@ def run_ckv(args, rank, world):
         "config": {"workload": CFG_NAME, "layers": L, "prefix_len": cfg.prefix_len, "chunk": cfg.chunk_size,
                    "suffix": cfg.suffix_len, "heads": f"{cfg.num_q_heads}/{cfg.num_kv_heads}",
                    "head_dim": cfg.head_dim, "budget_chunks": k, "prefetch_quota": quota,
-                   "requests": N_REQUESTS, "parallelism": f"prefix-shard{world}" if world > 1 else "single",
+                   "requests": N_REQUESTS, "cache_slots_per_layer": cache_slots, "parallelism": f"prefix-shard{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (0.94 GB of probe keys streamed per step)",
                    "bytes_per_layer": bpl},
         "roofline": {"kernel": "score_partial (A1)", "bound": "tensor", "achieved": achieved, "peak": peak,
@@ -340,6 +354,12 @@ def run_ckv(args, rank, world):
                   "spec_loads_per_layer": stats["total_spec_loads"] / n_lay,
                   "spec_used_per_layer": stats["total_spec_used"] / n_lay,
                   "link_bytes_per_layer": (stats["total_link_bytes_delta"] + stats["total_link_bytes_spec"]) / n_lay},
+        "cold_cache": {"ms_per_step": sum(cold_ms) / len(cold_ms), "us_per_layer": sum(cold_ms) / len(cold_ms) * 1e3 / L,
+                       "hit_rate": cold_stats["total_hits"] / max(cold_stats["total_hits"] + cold_stats["total_misses"], 1),
+                       "link_bytes_per_layer": (cold_stats["total_link_bytes_delta"] + cold_stats["total_link_bytes_spec"])
+                       / cold_layers,
+                       "link_gbs": (cold_stats["total_link_bytes_delta"] + cold_stats["total_link_bytes_spec"])
+                       / (sum(cold_ms) * 1e-3) / 1e9},
         "e2e": {"value": bpl * L / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,  # kernels per K steps (counted on the eager pass; the graphs hold the same)

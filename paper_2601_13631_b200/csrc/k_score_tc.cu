@@ -337,8 +337,8 @@ int poly_share() {
   static int np = -1;
   if (np < 0) {
     const char* e = getenv("CKV_SCORE_POLY");
-    np = e ? atoi(e) : 2;
-    if (np != 0 && np != 2 && np != 3 && np != 10 && np != 11) np = 2;
+    np = e ? atoi(e) : 0;  // measured on B200: the MUFU-only path is fastest (no FMA offload)
+    if (np != 0 && np != 2 && np != 3 && np != 10 && np != 11) np = 0;
   }
   return np;
 }
@@ -346,11 +346,11 @@ int poly_share() {
 template <int C>
 cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
   switch (poly_share()) {
-    case 0: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
     case 3: return launch_cp<C, 3>(tmK, tmQ, p, grid, st);
     case 10: return launch_cp<C, 10>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
     case 11: return launch_cp<C, 11>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
-    default: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
+    case 2: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
+    default: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
   }
 }
 
