@@ -301,6 +301,20 @@ def run_ckv(args, rank, world):
         cold_ms.append(timed(main_step, 1))
     cold_stats = ctx.get_stats()
     cold_layers = max(cold_stats["total_layers"], 1)
+
+    # host-link peak: pinned H2D cudaMemcpy, 256 MiB, best of 5 (the gather's roofline)
+    hbuf = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+    dbuf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    link_ms = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dbuf.copy_(hbuf, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        link_ms.append(e0.elapsed_time(e1))
+    link_peak = (256 << 20) / (min(link_ms) * 1e-3) / 1e9
+    del hbuf, dbuf
     h2d = sum(t.numel() * t.element_size() for lay in reqs_host[0] for t in lay)
     d2h = L * (outs[0].numel() * outs[0].element_size() + k * 4)
 
@@ -359,7 +373,8 @@ def run_ckv(args, rank, world):
                        "link_bytes_per_layer": (cold_stats["total_link_bytes_delta"] + cold_stats["total_link_bytes_spec"])
                        / cold_layers,
                        "link_gbs": (cold_stats["total_link_bytes_delta"] + cold_stats["total_link_bytes_spec"])
-                       / (sum(cold_ms) * 1e-3) / 1e9},
+                       / (sum(cold_ms) * 1e-3) / 1e9,
+                       "link_peak_gbs": link_peak, "link_peak_how": "pinned H2D cudaMemcpy 256 MiB, best of 5"},
         "e2e": {"value": bpl * L / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,  # kernels per K steps (counted on the eager pass; the graphs hold the same)
