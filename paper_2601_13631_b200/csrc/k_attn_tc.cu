@@ -5,17 +5,18 @@
 // visible, partial-chunk padding masked) and the causal suffix keys t <= r
 // (Q6, Q9).  A8 (attn_combine) merges the splits.
 //
-// Per work item (kv head, 128-row tile, key split), 1 CTA per SM, 320 threads:
-//   warp 0      TMA: Q tile (GQA-packed [Hkv][R_pad][128]); per 128-key tile the K and V
-//               blocks of 128/c kept chunks straight from their HBM cache slots (one 2-D box
-//               per chunk: [c tokens][64] x 2 halves, record layout [K|V][Hkv][c][d]), or the
-//               suffix tile through a 3-D map over k_suf / v_suf; missing chunks are fetched
-//               out of bounds (zero fill).  Two 64 KB K|V stages.
+// Per work item (kv head, 128-row tile, key split), 1 CTA per SM, 576 threads:
+//   warp 0      producer: Q tile by TMA (the GQA-packed [Hkv][R_pad][128] Q left by the score
+//               kernel); per 128-key tile the K and V halves of up to 128/c kept chunks straight
+//               from their HBM cache slots, one 1-D bulk copy per (chunk, K|V, half) issued by
+//               many lanes at once (records are stored pre-swizzled, rec_elem), or the suffix
+//               tile through a 3-D TMA map over k_suf / v_suf.  Two 64 KB stages; K and V of a
+//               stage have separate barriers (K(j+2) lands as soon as S(j) is done).
 //   warp 1      TMEM alloc + MMA issue: S = Q K^T (M 128, N 128, K 128; K-major / K-major) into one
 //               of two TMEM S buffers, then O += P V (P K-major from smem, V MN-major) into the TMEM
 //               O accumulator, software-pipelined one tile behind S.
-//   warps 2..9  softmax: one row per thread, two warps per TMEM lane quadrant (64 key columns
-//               and 64 O columns each); row max exchanged through shared memory; lazy O rescale
+//   warps 2..17 softmax: one row per thread, four warps per TMEM lane quadrant (32 key columns
+//               and 32 O columns each); row max exchanged through shared memory; lazy O rescale
 //               (only when the running max grows by > 8 in log2 units) via tcgen05.ld/st;
 //               P = 2^(s - m) written as bf16 in the 128-byte-swizzled K-major layout.
 #include <cstdio>
