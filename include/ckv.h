@@ -86,6 +86,12 @@ typedef struct {
   int32_t shard_index;     /* position shard owned by this ctx; 0 for one GPU */
   int32_t num_shards;      /* W >= 1; shard g owns chunks [g*ceil(m/W), min((g+1)*ceil(m/W), m)) */
   uint32_t flags;          /* CKV_FLAG_* */
+  int32_t period;          /* p >= 1 (0 => 1): layers [P p, (P+1) p) reuse the chunk ids identified at
+                              layer P p (Def. 3); the other layers skip A1-A3 and
+                              their chunks are prefetched right after identification (intra-period
+                              prefetch).  p > 1 needs num_shards == 1. */
+  int32_t subperiod;       /* sp in [1, p] (0 => 1): the first layer of a period starts attention only
+                              after the chunks of sp layers are loaded (subperiod_size) */
 } ckv_config;
 
 /* Counters of the last completed ckv_reprefill_layer / ckv_shard_attend call plus
@@ -129,8 +135,12 @@ ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const vo
  *  out    device [n_suffix, Hq, d]  attention output, cfg.dtype
  *  selected_ids  device int32 [k]   selected chunk ids, ascending (global ids)
  *  chunk_scores  device float [m] or NULL: A_j (Eq. 1) for parity/debug
- * Layer 0 starts a new request.  If prefetch_chunks > 0 and layer + 1 < L, the
- * call also enqueues the speculative prefetch of layer + 1 on the side stream.
+ * Layer 0 starts a new request; layers must be called in order.  With period p = 1 every
+ * layer runs A1-A9; if prefetch_chunks > 0 and layer + 1 < L the call also enqueues the
+ * speculative prefetch of layer + 1 (this layer's ids) on the side stream.  With p > 1 only the
+ * first layer of a period identifies chunks; it then enqueues the loads of the period's other
+ * layers (exact ids) and the speculative load of the next period's first layer; the other
+ * layers reuse the ids (selected_ids / chunk_scores report the period's).
  * Errors: CKV_EINVAL (null/range, 1 <= n_suffix <= max_suffix_len), CKV_ESTATE
  * (layer not stored, or num_shards > 1), CKV_ECUDA. */
 ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const void* k_suf,

@@ -25,6 +25,7 @@ from .ckv_oracle import (  # noqa: F401
     attention,
     lse_merge,
     reprefill_layer,
+    reprefill_periods,
     sharded_reprefill_layer,
     coverage_ratio,
 )

@@ -280,3 +280,24 @@ def sharded_reprefill_layer(W: int, Qs, Ks, Vs, Kp, Vp, c: int, k: int, G: int,
                                include_suffix=(g == W - 1)))
     O, lse = lse_merge(parts)
     return {"ids": sel, "out": O, "lse": lse, "A": A_full, "Lambda": lam}
+
+
+def reprefill_periods(layers, c: int, k: int, G: int, period: int, norm: int = NORM_PREFIX):
+    """Re-Prefill of consecutive layers with Periods (Def. 3):
+    the chunk ids of layer l are identified at the first layer of its Period, p*floor(l/p), and
+    reused by the other p-1 layers ("For the rest layers within the same Period, we reuse the same
+    ContiguousChunk indices").  `layers` is a list of (Qs, Ks, Vs, Kp, Vp) per layer.
+    Returns one reprefill_layer result per layer ('A' and 'gap' are those of the Period's first layer)."""
+    if period < 1:
+        raise ValueError("period must be >= 1")
+    out = []
+    first = None
+    for l, (Qs, Ks, Vs, Kp, Vp) in enumerate(layers):
+        if l % period == 0:
+            first = reprefill_layer(Qs, Ks, Vs, Kp, Vp, c, k, G, norm=norm)
+            out.append(first)
+        else:
+            r = reprefill_layer(Qs, Ks, Vs, Kp, Vp, c, k, G, norm=norm, sel=first["ids"])
+            r["A"], r["gap"] = first["A"], first["gap"]
+            out.append(r)
+    return out

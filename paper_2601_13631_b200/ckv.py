@@ -31,7 +31,8 @@ class ckv_config(ctypes.Structure):
         ("prefix_len", ctypes.c_int64), ("max_suffix_len", ctypes.c_int32), ("budget_chunks", ctypes.c_int32),
         ("budget_bp", ctypes.c_int32), ("score_norm", ctypes.c_int32), ("cache_slots", ctypes.c_int32),
         ("prefetch_chunks", ctypes.c_int32), ("device", ctypes.c_int32), ("shard_index", ctypes.c_int32),
-        ("num_shards", ctypes.c_int32), ("flags", ctypes.c_uint32),
+        ("num_shards", ctypes.c_int32), ("flags", ctypes.c_uint32), ("period", ctypes.c_int32),
+        ("subperiod", ctypes.c_int32),
     ]
 
 
@@ -115,12 +116,12 @@ class Context:
 
     def __init__(self, num_layers, num_q_heads, num_kv_heads, head_dim, chunk_size, prefix_len, max_suffix_len,
                  dtype="bf16", budget_chunks=0, budget_bp=1000, score_norm=CKV_NORM_PREFIX, cache_slots=0,
-                 prefetch_chunks=0, device=0, shard_index=0, num_shards=1, flags=0):
+                 prefetch_chunks=0, device=0, shard_index=0, num_shards=1, flags=0, period=1, subperiod=1):
         self.lib = load_library()
         self.torch_dtype = torch.bfloat16 if dtype == "bf16" else torch.float32
         cfg = ckv_config(num_layers, num_q_heads, num_kv_heads, head_dim, CKV_BF16 if dtype == "bf16" else CKV_FP32,
                          chunk_size, prefix_len, max_suffix_len, budget_chunks, budget_bp, score_norm, cache_slots,
-                         prefetch_chunks, device, shard_index, num_shards, flags)
+                         prefetch_chunks, device, shard_index, num_shards, flags, period, subperiod)
         self.cfg = cfg
         self.device = torch.device("cuda", device)
         h = ctypes.c_void_p()

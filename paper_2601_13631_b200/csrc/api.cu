@@ -26,7 +26,7 @@ struct ckv_ctx {
   int W = 1, shard = 0, j0 = 0, j1 = 0, m_loc = 0;
   int64_t t0 = 0;
   int n_loc = 0, n_pad = 0;
-  int k = 0, P = 0, quota = 0, max_ns = 0;
+  int k = 0, P = 0, quota = 0, max_ns = 0, period = 1, subperiod = 1;
   int64_t rec_elems = 0, rec_bytes = 0;
   int nsplit_score_max = 1, nsplit_attn_max = 1;
   int score_kind = 0;  // 0 SIMT, 1 tcgen05
@@ -387,6 +387,10 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   ctx->P = c.cache_slots > 0 ? c.cache_slots : 2 * ctx->k + ctx->quota;
   if (ctx->P < ctx->k + ctx->quota) return bad("cache_slots < k + prefetch_chunks");
   ctx->max_ns = c.max_suffix_len;
+  ctx->period = c.period > 0 ? c.period : 1;
+  ctx->subperiod = c.subperiod > 0 ? c.subperiod : 1;
+  if (ctx->subperiod > ctx->period) return bad("subperiod > period");
+  if (ctx->period > 1 && ctx->W > 1) return (delete ctx, CKV_EUNSUPPORTED);
   ctx->rec_elems = (int64_t)2 * ctx->Hkv * ctx->c * ctx->d;
   ctx->rec_bytes = ctx->rec_elems * ctx->esz;
   ctx->rec_swz = (ctx->dtype == CKV_BF16 && ctx->d == 128) ? 1 : 0;
@@ -554,18 +558,30 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     ++ctx->epoch;
     LK(launch_epoch_inc(ctx->epoch_dev, st));
   }
-  int nsplit = 0;
-  if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
-  LayerGeom g = geom(ctx, n_suffix);
-  PROF_BEGIN(2);
-  LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->A, st));
-  PROF_END(2);
-  int32_t* ids = ctx->ids_buf[layer & 1];
-  int32_t* nids = ctx->n_ids_buf[layer & 1];
-  PROF_BEGIN(6);
-  LK(launch_topk_scores(ctx->A, ctx->m_loc, ctx->k, 0, ids, nullptr, 0, nids, st));
-  PROF_END(6);
-  if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st)) != CKV_OK) return s;
+  const int p = ctx->period;
+  const int pid = layer / p;
+  const bool first = (layer % p) == 0;
+  const int pend = (pid + 1) * p < ctx->L ? (pid + 1) * p : ctx->L;  // end of this period
+  int32_t* ids = ctx->ids_buf[pid & 1];  // double-buffered by period: side-stream plans may still read it
+  int32_t* nids = ctx->n_ids_buf[pid & 1];
+  if (first) {  // identification: A1 -> A2 -> A3
+    int nsplit = 0;
+    if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
+    LayerGeom g = geom(ctx, n_suffix);
+    PROF_BEGIN(2);
+    LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->A, st));
+    PROF_END(2);
+    PROF_BEGIN(6);
+    LK(launch_topk_scores(ctx->A, ctx->m_loc, ctx->k, 0, ids, nullptr, 0, nids, st));
+    PROF_END(6);
+    // intra-period loads (exact ids) for the period's other layers, then the speculative load of
+    // the next period's first layer (A6), all on the side stream in layer order
+    for (int lp = layer + 1; lp <= pend && lp < ctx->L; ++lp)
+      if ((s = issue_prefetch(ctx, lp, ids, nids, st)) != CKV_OK) return s;
+    // subperiod gate: attention of the first layer waits for sp layers' chunks
+    for (int lp = layer + 1; lp < layer + ctx->subperiod && lp < pend; ++lp)
+      if (ctx->pf_issued[lp] == ctx->epoch) CK(cudaStreamWaitEvent(st, ctx->ev_pf[lp], 0));
+  }
   if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, st)) != CKV_OK)
     return s;
   CK(cudaMemcpyAsync(selected_ids, ids, sizeof(int32_t) * ctx->k, cudaMemcpyDeviceToDevice, st));

@@ -27,9 +27,10 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_struct_layout_matches_header():
-    # ckv_config: 6 int32, int64 (offset 24), 10 int32  -> 72 bytes
+    # ckv_config: 6 int32, int64 (offset 24), 12 int32  -> 80 bytes
     assert ckv.ckv_config.prefix_len.offset == 24
-    assert ckv.ctypes.sizeof(ckv.ckv_config) == 72
+    assert ckv.ckv_config.period.offset == 72
+    assert ckv.ctypes.sizeof(ckv.ckv_config) == 80
     assert ckv.ckv_stats.total_hits.offset == 16
 
 

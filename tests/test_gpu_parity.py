@@ -168,6 +168,38 @@ def test_cuda_graph_replay_matches_eager():
     ctx.get_stats()  # raises if the planner ever saw a cache overflow
 
 
+@pytest.mark.parametrize("period,sub", [(4, 2), (3, 1), (8, 4)])
+def test_periods_intra_period_prefetch(period, sub):
+    """NEXT-1: layers of a Period reuse the ids identified at its first layer (Def. 3,
+    PAPER.md:349-355); the other layers' chunks are loaded right after identification."""
+    cfg = C2_SMALL.replace(num_layers=8, prefix_len=4096)
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg, prefetch=k)
+    ctx.close()
+    from paper_2601_13631_b200 import Context
+    ctx = Context(cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.chunk_size, cfg.prefix_len,
+                  cfg.suffix_len, dtype=cfg.dtype, budget_bp=cfg.budget_bp, prefetch_chunks=k, period=period,
+                  subperiod=sub)
+    for l, (kp, vp) in enumerate(prefix):
+        ctx.store_prefix(l, to_dev(kp, torch.bfloat16), to_dev(vp, torch.bfloat16))
+    for rep in range(2):  # second pass: warm cache
+        res = run_layers(ctx, cfg, prefix, range(cfg.num_layers), request=rep)
+        for r in res:
+            l = r["layer"]
+            kp, vp = prefix[l]
+            if l % period == 0:
+                first = r
+                check_layer(r["ids"], r["out"], r["A"], r["qs"], r["ks"], r["vs"], kp, vp, cfg, k)
+            else:
+                assert np.array_equal(r["ids"], first["ids"])
+                ref = O.reprefill_layer(r["qs"], r["ks"], r["vs"], kp, vp, cfg.chunk_size, k, cfg.group,
+                                        sel=r["ids"].astype(np.int64))
+                from tests.gpu_util import row_rel_err
+                assert row_rel_err(r["out"], ref["out"]) < 2e-2
+    st = ctx.get_stats()
+    assert st["total_spec_loads"] > 0
+
+
 # ---------------------------------------------------------------- top-k (bit exact)
 @pytest.mark.parametrize("m", [1, 7, 300, 2048, 32768])
 def test_topk_exact_with_ties(m):

@@ -323,3 +323,30 @@ def test_synth_deterministic_and_shaped():
     assert q.shape == (32, 14, 64) and ks.shape == (32, 2, 64)
     q2, _, _ = make_request(cfg, 0, request=4)
     assert not np.array_equal(q, q2)
+
+
+# ------------------------------------------------------------ periods (NEXT-1, Q10)
+def _layers(n_layers, seed=20):
+    return [rand_case(seed + l, n=96, c=8, ns=4, scale=2.0) for l in range(n_layers)]
+
+
+def test_period_one_is_per_layer():
+    lay = _layers(4)
+    per = O.reprefill_periods(lay, 8, 3, 2, period=1)
+    for (Qs, Ks, Vs, Kp, Vp), r in zip(lay, per):
+        ref = O.reprefill_layer(Qs, Ks, Vs, Kp, Vp, 8, 3, 2)
+        assert r["ids"].tolist() == ref["ids"].tolist()
+        np.testing.assert_array_equal(r["out"], ref["out"])
+
+
+def test_period_reuses_first_layer_ids():
+    lay = _layers(6)
+    per = O.reprefill_periods(lay, 8, 3, 2, period=4)
+    first = [O.reprefill_layer(*lay[l], 8, 3, 2)["ids"].tolist() for l in (0, 4)]
+    for l, r in enumerate(per):
+        assert r["ids"].tolist() == first[l // 4]
+    # a non-first layer attends exactly over the first layer's chunks (library special case:
+    # dense attention restricted to those tokens == SDPA with the kept-token mask)
+    Qs, Ks, Vs, Kp, Vp = lay[2]
+    toks = O.kept_token_index(first[0], 96, 8)
+    np.testing.assert_allclose(per[2]["out"], O.attention(Qs, Ks, Vs, Kp, Vp, toks, 2)[0], atol=1e-14)
