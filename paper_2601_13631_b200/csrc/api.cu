@@ -40,7 +40,7 @@ struct ckv_ctx {
   char* pool = nullptr;
   int32_t *slot_of = nullptr, *owner = nullptr, *pf_epoch = nullptr, *F = nullptr;
   float* I = nullptr;
-  float *lam2 = nullptr, *lampart = nullptr, *Lam2 = nullptr, *A = nullptr;
+  float *lam2 = nullptr, *lampart = nullptr, *Lam2 = nullptr, *A = nullptr, *Apart = nullptr;
   int32_t* ids_buf[2] = {nullptr, nullptr};
   int32_t* n_ids_buf[2] = {nullptr, nullptr};
   int32_t *kept_slots = nullptr, *ids_glob = nullptr, *flag = nullptr;
@@ -310,7 +310,7 @@ void free_all(ckv_ctx* ctx) {
   cudaSetDevice(ctx->cfg.device);
   cudaDeviceSynchronize();
   void* dev_ptrs[] = {ctx->probe, ctx->pool, ctx->slot_of, ctx->owner, ctx->pf_epoch, ctx->F, ctx->I, ctx->lam2,
-                      ctx->lampart, ctx->Lam2, ctx->A, ctx->ids_buf[0], ctx->ids_buf[1], ctx->n_ids_buf[0],
+                      ctx->lampart, ctx->Lam2, ctx->A, ctx->Apart, ctx->ids_buf[0], ctx->ids_buf[1], ctx->n_ids_buf[0],
                       ctx->n_ids_buf[1], ctx->kept_slots, ctx->ids_glob, ctx->flag, ctx->scratch_main,
                       ctx->scratch_side, ctx->gl_main, ctx->gl_side, ctx->nload_main, ctx->nload_side, ctx->counts,
                       ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache, ctx->epoch_dev};
@@ -436,6 +436,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   CKC(dalloc(&ctx->lampart, (size_t)ctx->Hkv * ctx->nsplit_score_max * R_max));
   CKC(dalloc(&ctx->Lam2, (size_t)ctx->Hkv * R_max));
   CKC(dalloc(&ctx->A, (size_t)ctx->m_loc));
+  CKC(dalloc(&ctx->Apart, (size_t)ctx->m_loc * ctx->Hkv));
   for (int i = 0; i < 2; ++i) {
     CKC(dalloc(&ctx->ids_buf[i], (size_t)ctx->k));
     CKC(dalloc(&ctx->n_ids_buf[i], 1));
@@ -569,10 +570,10 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
     LayerGeom g = geom(ctx, n_suffix);
     PROF_BEGIN(2);
-    LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->A, st));
+    LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
     PROF_END(2);
     PROF_BEGIN(6);
-    LK(launch_topk_scores(ctx->A, ctx->m_loc, ctx->k, 0, ids, nullptr, 0, nids, st));
+    LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, ids, nullptr, 0, nids, st));
     PROF_END(6);
     // intra-period loads (exact ids) for the period's other layers, then the speculative load of
     // the next period's first layer (A6), all on the side stream in layer order
@@ -623,8 +624,8 @@ ckv_status ckv_shard_select(ckv_ctx* ctx, int32_t layer, const void* q, const vo
     LK(launch_row_lse<__nv_bfloat16>(g, nullptr, 0, static_cast<const __nv_bfloat16*>(q),
                                      static_cast<const __nv_bfloat16*>(k_suf), ctx->fullrow, lam_all, ctx->W,
                                      ctx->Lam2, nullptr, st));
-  LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->A, st));
-  LK(launch_topk_scores(ctx->A, ctx->m_loc, ctx->k, ctx->j0, nullptr, cand, ctx->k, nullptr, st));
+  LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
+  LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, ctx->j0, nullptr, cand, ctx->k, nullptr, st));
   if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;
 }
@@ -761,7 +762,8 @@ ckv_status ckv_test_topk(ckv_ctx* ctx, const float* A, int32_t m, int32_t k, int
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
   if (!A || !ids || m < 1 || k < 1 || k > m) return fail(ctx, CKV_EINVAL, "bad argument");
-  LK(launch_topk_scores(A, m, k, 0, ids, nullptr, 0, nullptr, static_cast<cudaStream_t>(stream)));
+  LK(launch_topk_scores(const_cast<float*>(A), nullptr, 0, m, k, 0, ids, nullptr, 0, nullptr,
+                        static_cast<cudaStream_t>(stream)));
   return CKV_OK;
 }
 

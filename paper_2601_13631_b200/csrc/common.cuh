@@ -67,10 +67,11 @@ template <typename T>
 cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit, const T* q, const T* k_suf,
                            int fullrow, const float* lam_all, int W, float* Lam2, float* lam_local_out,
                            cudaStream_t st);
-cudaError_t launch_chunk_sum(const LayerGeom& g, const float* lam2, const float* Lam2, float* A,
-                             cudaStream_t st);
+cudaError_t launch_chunk_sum(const LayerGeom& g, const float* lam2, const float* Lam2, float* Apart,
+                             cudaStream_t st);  // Apart [Hkv][m_loc]
 // A3
-cudaError_t launch_topk_scores(const float* A, int m, int k, int id_offset, int32_t* ids,
+// A [m] is written first as sum_h Apart[h][j] when Apart != nullptr (else A is the input)
+cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, int k, int id_offset, int32_t* ids,
                                uint64_t* cand_out, int n_cand_out, int32_t* n_out, cudaStream_t st);
 cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1,
                               int32_t* flag_scratch, int32_t* ids_glob, int32_t* ids_local,

@@ -102,35 +102,34 @@ __global__ void __launch_bounds__(256) row_lse_kernel(LayerGeom g, const float* 
   Lam2[idx] = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
 }
 
-// One warp per chunk j: lanes take 4 consecutive rows at a time (float4 when R % 4 == 0),
-// 4 independent partial sums, then a fixed xor-tree reduce.
+// One warp per (kv head, chunk j): lanes take 4 consecutive rows at a time (float4 when
+// R % 4 == 0), 4 independent partial sums, then a fixed xor-tree reduce.  Writes the per-KV-head
+// partial Apart[kvh][j]; the top-k kernel adds the Hkv partials in a fixed order.
 __global__ void chunk_sum_kernel(LayerGeom g, const float* __restrict__ lam2, const float* __restrict__ Lam2,
-                                 float* __restrict__ A) {
+                                 float* __restrict__ Apart) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= g.m_loc) return;
+  if (warp >= g.m_loc * g.Hkv) return;
+  const int kvh = warp / g.m_loc, j = warp % g.m_loc;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  const bool vec = (g.R & 3) == 0;
-  for (int kvh = 0; kvh < g.Hkv; ++kvh) {
-    const float* src = lam2 + ((size_t)kvh * g.m_loc + warp) * g.R;
-    const float* L = Lam2 + (size_t)kvh * g.R;
-    if (vec) {
-      for (int row = lane * 4; row < g.R; row += 128) {
-        const float4 a = *reinterpret_cast<const float4*>(src + row);
-        const float4 b = *reinterpret_cast<const float4*>(L + row);
-        acc[0] += fast_exp2(a.x - b.x);
-        acc[1] += fast_exp2(a.y - b.y);
-        acc[2] += fast_exp2(a.z - b.z);
-        acc[3] += fast_exp2(a.w - b.w);
-      }
-    } else {
-      for (int row = lane; row < g.R; row += 32) acc[row & 3] += fast_exp2(src[row] - L[row]);
+  const float* src = lam2 + ((size_t)kvh * g.m_loc + j) * g.R;
+  const float* L = Lam2 + (size_t)kvh * g.R;
+  if ((g.R & 3) == 0) {
+    for (int row = lane * 4; row < g.R; row += 128) {
+      const float4 a = *reinterpret_cast<const float4*>(src + row);
+      const float4 b = *reinterpret_cast<const float4*>(L + row);
+      acc[0] += fast_exp2(a.x - b.x);
+      acc[1] += fast_exp2(a.y - b.y);
+      acc[2] += fast_exp2(a.z - b.z);
+      acc[3] += fast_exp2(a.w - b.w);
     }
+  } else {
+    for (int row = lane; row < g.R; row += 32) acc[row & 3] += fast_exp2(src[row] - L[row]);
   }
   float s = (acc[0] + acc[1]) + (acc[2] + acc[3]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) A[warp] = s;
+  if (lane == 0) Apart[warp] = s;
 }
 
 }  // namespace
@@ -150,10 +149,11 @@ template cudaError_t launch_row_lse<__nv_bfloat16>(const LayerGeom&, const float
                                                    const __nv_bfloat16*, int, const float*, int, float*, float*,
                                                    cudaStream_t);
 
-cudaError_t launch_chunk_sum(const LayerGeom& g, const float* lam2, const float* Lam2, float* A, cudaStream_t st) {
+cudaError_t launch_chunk_sum(const LayerGeom& g, const float* lam2, const float* Lam2, float* Apart,
+                             cudaStream_t st) {
   const int threads = 256, warps_per_block = threads / 32;
-  const int blocks = (g.m_loc + warps_per_block - 1) / warps_per_block;
-  chunk_sum_kernel<<<blocks, threads, 0, st>>>(g, lam2, Lam2, A);
+  const int blocks = (g.m_loc * g.Hkv + warps_per_block - 1) / warps_per_block;
+  chunk_sum_kernel<<<blocks, threads, 0, st>>>(g, lam2, Lam2, Apart);
   return cudaGetLastError();
 }
 

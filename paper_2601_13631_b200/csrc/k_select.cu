@@ -13,10 +13,19 @@ namespace {
 
 constexpr int NT = 1024;
 
-__global__ void __launch_bounds__(NT) topk_scores_kernel(const float* __restrict__ A, int m, int k, int id_offset,
+__global__ void __launch_bounds__(NT) topk_scores_kernel(float* __restrict__ A, const float* __restrict__ Apart,
+                                                         int nparts, int m, int k, int id_offset,
                                                          int32_t* __restrict__ ids, uint64_t* __restrict__ cand,
                                                          int n_cand_out, int32_t* __restrict__ n_out) {
   __shared__ SelectSmem ss;
+  if (Apart) {  // A_j = sum over KV heads of the chunk-sum partials, fixed order
+    for (int j = threadIdx.x; j < m; j += NT) {
+      float a = 0.f;
+      for (int h = 0; h < nparts; ++h) a += Apart[(size_t)h * m + j];
+      A[j] = a;
+    }
+    __syncthreads();
+  }
   auto key = [&](int j) -> uint64_t {
     return ((uint64_t)__float_as_uint(A[j]) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j + id_offset));
   };
@@ -75,9 +84,9 @@ __global__ void __launch_bounds__(NT) topk_merge_kernel(const uint64_t* __restri
 
 }  // namespace
 
-cudaError_t launch_topk_scores(const float* A, int m, int k, int id_offset, int32_t* ids, uint64_t* cand_out,
-                               int n_cand_out, int32_t* n_out, cudaStream_t st) {
-  topk_scores_kernel<<<1, NT, 0, st>>>(A, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, int k, int id_offset, int32_t* ids,
+                               uint64_t* cand_out, int n_cand_out, int32_t* n_out, cudaStream_t st) {
+  topk_scores_kernel<<<1, NT, 0, st>>>(A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
   return cudaGetLastError();
 }
 
