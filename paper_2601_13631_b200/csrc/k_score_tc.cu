@@ -36,7 +36,7 @@ struct TcParams {
   LayerGeom g;
   float* lam2;
   float* lampart;
-  int nsplit;   // = NKT
+  int nsplit;   // = kColSplit * NKT (one partial normaliser per row, key tile and column quarter)
   int NKT;      // key tiles per kv head
   int MT;       // row tiles per kv head
   int R_pad;
@@ -152,7 +152,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* acc_full = bars + 8;
   uint64_t* acc_empty = bars + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
-  __shared__ float2 xchg[2 * kColSplit * 128];  // [unit parity][column quarter][row]: (max, sum)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
@@ -279,28 +278,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           epilogue_group<C, NP>(p, v[gi], kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
         }
       }
-      // the four column quarters of a row combine into one partial normaliser per key tile
-      float2* xb = xchg + (acount & 1) * (kColSplit * 128);
-      xb[half * 128 + row_in_tile] = make_float2(HM, HS);
-      ptx::named_bar_sync(1 + quad, 32 * kColSplit);
-      if (half == 0) {
-        float M = -INFINITY, S = 0.f;
-#pragma unroll
-        for (int w = 0; w < kColSplit; ++w) {
-          const float2 pc = xb[w * 128 + row_in_tile];
-          if (pc.y > 0.f) {
-            if (S == 0.f) {
-              M = pc.x;
-              S = pc.y;
-            } else {
-              const float nm = fmaxf(M, pc.x);
-              S = S * fast_exp2(M - nm) + pc.y * fast_exp2(pc.x - nm);
-              M = nm;
-            }
-          }
-        }
-        if (row_ok) p.lampart[((size_t)kvh * p.nsplit + kt) * p.g.R + rho] = (S > 0.f) ? M + fast_log2(S) : -INFINITY;
-      }
+      if (row_ok)
+        p.lampart[((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho] =
+            (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
       ++acount;
     }
   }
@@ -379,7 +359,7 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
 int score_tc_nsplit(const LayerGeom& g) {
   if (g.d != D) return 0;
   if (g.c < 1 || g.c > BN / kColSplit || ((BN / kColSplit) % g.c) != 0) return 0;
-  return (g.n_loc + BN - 1) / BN;  // one partial normaliser per (row, key tile)
+  return kColSplit * ((g.n_loc + BN - 1) / BN);
 }
 
 size_t score_tc_qpack_elems(int Hkv, int R_max) { return (size_t)Hkv * ((R_max + BM - 1) / BM) * BM * D; }
@@ -392,7 +372,7 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   p.lam2 = lam2;
   p.lampart = lampart;
   p.nsplit = nsplit;
-  p.NKT = nsplit;
+  p.NKT = nsplit / kColSplit;
   p.MT = (g.R + BM - 1) / BM;
   p.R_pad = p.MT * BM;
   p.n_units = g.Hkv * p.NKT * p.MT;
