@@ -69,11 +69,11 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
 }
 
-template <int C, int NP>
+template <int C, int NP, bool MASK>
 __device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32], int key0, int kvh, int rho,
                                                bool row_ok, float& HM, float& HS, float& CM, float& CS) {
   const float sc = p.scale;
-  if (key0 + 32 > p.g.n_loc) {  // only the shard's last key tile (warp-uniform)
+  if constexpr (MASK) {  // only the shard's last key tile (a separate instantiation)
 #pragma unroll
     for (int j = 0; j < 32; ++j)
       if (key0 + j >= p.g.n_loc) v[j] = -INFINITY;
@@ -274,8 +274,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           HS += 1.f;
         } else if constexpr (NP == 10) {  // tuning: TMEM drain only
           HS += v[gi][0] + v[gi][31];
+        } else if (kt * BN + BN > p.g.n_loc) {  // warp-uniform: the last key tile only
+          epilogue_group<C, NP, true>(p, v[gi], kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
         } else {
-          epilogue_group<C, NP>(p, v[gi], kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
+          epilogue_group<C, NP, false>(p, v[gi], kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
         }
       }
       if (row_ok)
