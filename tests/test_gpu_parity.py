@@ -200,6 +200,34 @@ def test_periods_intra_period_prefetch(period, sub):
     assert st["total_spec_loads"] > 0
 
 
+@pytest.mark.parametrize("c,bp", [(4, 200), (16, 2500), (64, 5000), (16, 200)])
+def test_c5_chunk_and_budget_sweep_reduced(c, bp):
+    """C5 (32B shape: 40 Q / 8 KV heads) chunk-size x budget sweep at a reduced prefix."""
+    cfg = CONFIGS["c5_32b"].replace(num_layers=2, prefix_len=8192, chunk_size=c, suffix_len=64, budget_bp=bp)
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg, prefetch=k)
+    res = run_layers(ctx, cfg, prefix, range(cfg.num_layers))
+    _check_all(ctx, cfg, prefix, res, k)
+
+
+def test_c4_shape_reduced():
+    """C4 (14B shape: 40 Q / 8 KV heads, c = 32, n_s = 256, 5% budget) at a reduced prefix."""
+    cfg = CONFIGS["c4_14b"].replace(num_layers=2, prefix_len=16384)
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg, prefetch=k)
+    res = run_layers(ctx, cfg, prefix, range(cfg.num_layers))
+    _check_all(ctx, cfg, prefix, res, k)
+
+
+def test_probe_config_ns8():
+    """Supplementary HBM-probe config (C3 shape, n_s = 8: 56 rows per KV head, one row tile)."""
+    cfg = CONFIGS["probe_7b_ns8"].replace(num_layers=1)
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg)
+    res = run_layers(ctx, cfg, prefix, [0])
+    _check_all(ctx, cfg, prefix, res, k)
+
+
 # ---------------------------------------------------------------- top-k (bit exact)
 @pytest.mark.parametrize("m", [1, 7, 300, 2048, 32768])
 def test_topk_exact_with_ties(m):
