@@ -167,11 +167,14 @@ def run_ckv(args, rank, world):
     from paper_2601_13631_b200.sharded import ShardedReprefill
     from synth import CONFIGS, make_prefix, make_request
 
-    local_rank = int(os.environ.get("LOCAL_RANK", rank))
+    local_rank = int(os.environ.get("LOCAL_RANK", rank)) if args.local_gpu is None else args.local_gpu
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # functional check of the sharded path (e.g. several ranks sharing one GPU)
+            dist.init_process_group("gloo")
     cfg = CONFIGS[CFG_NAME]
     k = ckv.ckv_budget_chunks(cfg.prefix_len, cfg.chunk_size, cfg.budget_bp)
     quota = k if args.prefetch else 0
@@ -221,8 +224,8 @@ def run_ckv(args, rank, world):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t = torch.tensor([ms], device=dev if args.backend == "nccl" else "cpu")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks
             ms = float(t.item())
         return ms
 
@@ -398,6 +401,8 @@ def main():
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--local-gpu", type=int, default=None, help="pin every rank to this GPU (functional runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ckv" else args.warmup
     rank = int(os.environ.get("RANK", 0))

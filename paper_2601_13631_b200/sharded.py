@@ -73,16 +73,28 @@ class _TorchComm:
     def __init__(self, group=None):
         self.group = group
 
+    def _nccl(self):
+        return dist.get_backend(self.group) == "nccl"
+
     def all_gather(self, out, inp):
-        if dist.get_backend(self.group) == "nccl":
+        if self._nccl():
             dist.all_gather_into_tensor(out, inp, group=self.group)
-        else:  # gloo (CPU tests): list form
-            parts = list(out.chunk(dist.get_world_size(self.group)))
-            dist.all_gather(parts, inp, group=self.group)
-            out.copy_(torch.cat(parts))
+            return
+        # gloo (CPU tests, or a functional multi-rank run on one GPU): CPU staging, list form
+        parts = [torch.empty_like(inp, device="cpu") for _ in range(dist.get_world_size(self.group))]
+        dist.all_gather(parts, inp.cpu(), group=self.group)
+        out.copy_(torch.cat(parts))
+
+    def _all_reduce(self, t, op):
+        if self._nccl():
+            dist.all_reduce(t, op=op, group=self.group)
+            return
+        c = t.cpu()
+        dist.all_reduce(c, op=op, group=self.group)
+        t.copy_(c)
 
     def all_reduce_max(self, t):
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        self._all_reduce(t, dist.ReduceOp.MAX)
 
     def all_reduce_sum(self, t):
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        self._all_reduce(t, dist.ReduceOp.SUM)
