@@ -180,6 +180,11 @@ ckv_status ckv_lse_merge_prepare(ckv_ctx* ctx, const float* o_part, const float*
 ckv_status ckv_lse_merge_finish(ckv_ctx* ctx, const float* merge_buf, int32_t n_suffix,
                                 void* out, void* stream);
 
+/* Change the Period p and subperiod sp (same meaning and limits as ckv_config.period /
+ * .subperiod) between requests (before the next layer-0 call).  CKV_EINVAL / CKV_EUNSUPPORTED
+ * as in ckv_create. */
+ckv_status ckv_set_period(ckv_ctx* ctx, int32_t period, int32_t subperiod);
+
 /* Cache control / introspection. */
 ckv_status ckv_reset_cache(ckv_ctx* ctx, void* stream); /* empty every slot; keep (I, F) */
 ckv_status ckv_get_stats(ckv_ctx* ctx, ckv_stats* out);  /* synchronises the library's streams */

@@ -63,6 +63,7 @@ SIGNATURES = {
     "ckv_lse_merge_prepare": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P]),
     "ckv_lse_merge_finish": (ctypes.c_int, [_P, _P, _I32, _P, _P]),
     "ckv_reset_cache": (ctypes.c_int, [_P, _P]),
+    "ckv_set_period": (ctypes.c_int, [_P, _I32, _I32]),
     "ckv_get_stats": (ctypes.c_int, [_P, ctypes.POINTER(ckv_stats)]),
     "ckv_reset_stats": (ctypes.c_int, [_P]),
     "ckv_num_chunks": (_I32, [_P]),
@@ -197,6 +198,9 @@ class Context:
     def lse_merge_finish(self, merge_buf, n_suffix, out, stream=None):
         self._check(self.lib.ckv_lse_merge_finish(self.h, _ptr(merge_buf), n_suffix, _ptr(out), _stream(stream)),
                     "ckv_lse_merge_finish")
+
+    def set_period(self, period, subperiod=1):
+        self._check(self.lib.ckv_set_period(self.h, period, subperiod), "ckv_set_period")
 
     def reset_cache(self, stream=None):
         self._check(self.lib.ckv_reset_cache(self.h, _stream(stream)), "ckv_reset_cache")

@@ -677,6 +677,17 @@ ckv_status ckv_lse_merge_finish(ckv_ctx* ctx, const float* merge_buf, int32_t n_
   return CKV_OK;
 }
 
+ckv_status ckv_set_period(ckv_ctx* ctx, int32_t period, int32_t subperiod) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  const int p = period > 0 ? period : 1, sp = subperiod > 0 ? subperiod : 1;
+  if (sp > p) return fail(ctx, CKV_EINVAL, "subperiod > period");
+  if (p > 1 && ctx->W > 1) return fail(ctx, CKV_EUNSUPPORTED, "period > 1 needs num_shards == 1");
+  ctx->period = p;
+  ctx->subperiod = sp;
+  return CKV_OK;
+}
+
 ckv_status ckv_reset_cache(ckv_ctx* ctx, void* stream) {
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
