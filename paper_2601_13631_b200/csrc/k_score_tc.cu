@@ -154,9 +154,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // row-tile order rotated per CTA: the ~37 CTAs working on one KV head at a time would
-  // otherwise all fetch the same Q tile from L2 at once
-  const int rot = blockIdx.x % p.MT;
+  // units: (kv head, key tile) pairs x row tiles; the row-tile order is rotated by the pair index
+  // (a bijection inside every pair, whichever CTAs share it) so the CTAs working on one KV head
+  // at a time do not all fetch the same Q tile from L2 at once
   const int u0 = (int)((int64_t)blockIdx.x * p.n_units / gridDim.x);
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * p.n_units / gridDim.x);
 
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tma_prefetch_desc(&tmQ);
       int kcount = 0, qcount = 0, cur = -1;
       for (int u = u0; u < u1; ++u) {
-        const int pr = u / p.MT, mt = (u % p.MT + rot) % p.MT;
+        const int pr = u / p.MT, mt = (u % p.MT + pr) % p.MT;
         const int kvh = pr / p.NKT, kt = pr % p.NKT;
         if (pr != cur) {
           const int kb = kcount & 1;
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row_in_tile = quad * 32 + lane;
     int acount = 0;
     for (int u = u0; u < u1; ++u) {
-      const int pr = u / p.MT, mt = (u % p.MT + rot) % p.MT;
+      const int pr = u / p.MT, mt = (u % p.MT + pr) % p.MT;
       const int kvh = pr / p.NKT, kt = pr % p.NKT;
       const int ab = acount & 1;
       ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
