@@ -30,7 +30,8 @@ constexpr int kColSplit = kEpiWarps / 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kKBytes = BN * D * 2;  // 65536
 constexpr uint32_t kQBytes = BM * D * 2;  // 32768
-constexpr size_t kSmem = 2 * kKBytes + 2 * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int kQStages = 3;  // TMA latency of a Q tile (~2 us) spans more than one unit's MMAs
+constexpr size_t kSmem = 2 * kKBytes + kQStages * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
 
 struct TcParams {
   LayerGeom g;
@@ -144,14 +145,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* kbuf0 = smem;
   uint8_t* qbuf0 = smem + 2 * kKBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kKBytes + 2 * kQBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kKBytes + kQStages * kQBytes);
   uint64_t* k_full = bars + 0;
   uint64_t* k_empty = bars + 2;
-  uint64_t* q_full = bars + 4;
-  uint64_t* q_empty = bars + 6;
-  uint64_t* acc_full = bars + 8;
-  uint64_t* acc_empty = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+  uint64_t* acc_full = bars + 4;
+  uint64_t* acc_empty = bars + 6;
+  uint64_t* q_full = bars + 8;              // [kQStages]
+  uint64_t* q_empty = bars + 8 + kQStages;  // [kQStages]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kQStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // units: (kv head, key tile) pairs x row tiles; the row-tile order is rotated by the pair index
@@ -164,10 +165,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
-      ptx::mbar_init(&q_full[i], 1);
-      ptx::mbar_init(&q_empty[i], 1);
       ptx::mbar_init(&acc_full[i], 1);
       ptx::mbar_init(&acc_empty[i], kEpiWarps);
+    }
+    for (int i = 0; i < kQStages; ++i) {
+      ptx::mbar_init(&q_full[i], 1);
+      ptx::mbar_init(&q_empty[i], 1);
     }
     ptx::fence_mbar_init();
   }
@@ -196,8 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           cur = pr;
           ++kcount;
         }
-        const int qs = qcount & 1;
-        ptx::mbar_wait(&q_empty[qs], ((qcount >> 1) & 1) ^ 1);
+        const int qs = qcount % kQStages;
+        ptx::mbar_wait(&q_empty[qs], ((qcount / kQStages) & 1) ^ 1);
         ptx::mbar_expect_tx(&q_full[qs], kQBytes);
         const int yq = kvh * p.R_pad + mt * BM;
         uint8_t* dq = qbuf0 + qs * kQBytes;
@@ -218,8 +221,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++kcount;
           cur = pr;
         }
-        const int qs = qcount & 1;
-        ptx::mbar_wait(&q_full[qs], (qcount >> 1) & 1);
+        const int qs = qcount % kQStages;
+        ptx::mbar_wait(&q_full[qs], (qcount / kQStages) & 1);
         const int ab = acount & 1;
         ptx::mbar_wait(&acc_empty[ab], ((acount >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
