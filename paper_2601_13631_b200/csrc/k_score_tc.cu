@@ -70,73 +70,75 @@ __device__ __forceinline__ float exp2_poly(float x) {
   return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
 }
 
+// One warp's 64 key columns of one row tile (this thread: one suffix row): a single max over
+// the 64 scores is the reference for every exponential (no running rescale), so the MUFU pipe
+// sees one ex2 per score plus one lg2 per chunk piece and one for the quarter normaliser.
 template <int C, int NP, bool MASK>
-__device__ __forceinline__ void epilogue_group(const TcParams& p, float (&v)[32], int key0, int kvh, int rho,
-                                               bool row_ok, float& HM, float& HS, float& CM, float& CS) {
+__device__ __forceinline__ void epilogue_unit(const TcParams& p, float (&v)[64], int key0, float* lamrow,
+                                              float* lampart_out, bool row_ok) {
   const float sc = p.scale;
   if constexpr (MASK) {  // only the shard's last key tile (a separate instantiation)
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
+    for (int j = 0; j < 64; ++j)
       if (key0 + j >= p.g.n_loc) v[j] = -INFINITY;
   }
-  float m[16];
+  float m[22];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) m[i] = fmaxf(v[2 * i], v[2 * i + 1]);
+  for (int i = 0; i < 21; ++i) m[i] = fmaxf(fmaxf(v[3 * i], v[3 * i + 1]), v[3 * i + 2]);
+  m[21] = v[63];
 #pragma unroll
-  for (int n = 8; n >= 1; n >>= 1)
+  for (int i = 0; i < 7; ++i) m[i] = fmaxf(fmaxf(m[3 * i], m[3 * i + 1]), m[3 * i + 2]);
+  m[0] = fmaxf(fmaxf(m[0], m[1]), m[2]);
+  m[3] = fmaxf(fmaxf(m[3], m[4]), m[5]);
+  m[6] = fmaxf(m[6], m[21]);
+  const float gm = fmaxf(fmaxf(m[0], m[3]), m[6]);
+  const float ms = (gm == -INFINITY) ? 0.f : gm * sc;
 #pragma unroll
-    for (int i = 0; i < n; ++i) m[i] = fmaxf(m[2 * i], m[2 * i + 1]);
-  const float gm = m[0];
-  const float gms = (gm == -INFINITY) ? 0.f : gm * sc;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const float t = fmaf(v[j], sc, -gms);
-    v[j] = ((j & 7) < NP) ? exp2_poly(t) : fast_exp2(t);  // NP of every 8 on the FMA pipe
+  for (int j = 0; j < 64; ++j) {
+    const float t = fmaf(v[j], sc, -ms);
+    v[j] = (NP < 8 && (j & 7) < NP) ? exp2_poly(t) : fast_exp2(t);  // NP of every 8 on the FMA pipe
   }
-  constexpr int CG = C < 32 ? C : 32;  // chunk piece inside this group
-  tree_sum<32, CG>(v);                 // v[0 .. 32/CG) = chunk (piece) sums
-  float cs[32 / CG];
+  constexpr int CG = C < 64 ? C : 64;  // keys per chunk piece inside these 64 columns
+  tree_sum<64, CG>(v);                 // v[0 .. 64/CG) = chunk (piece) sums
+  float cs[64 / CG];
 #pragma unroll
-  for (int i = 0; i < 32 / CG; ++i) cs[i] = v[i];
-  tree_sum<32 / CG, 32 / CG>(v);
-  const float gs = v[0];
-  if (gs > 0.f) {  // running LSE of this warp's 64-key quarter tile
-    if (HS == 0.f) {
-      HM = gms;
-      HS = gs;
-    } else {
-      const float nm = fmaxf(HM, gms);
-      HS = HS * fast_exp2(HM - nm) + gs * fast_exp2(gms - nm);
-      HM = nm;
-    }
+  for (int i = 0; i < 64 / CG; ++i) cs[i] = v[i];
+  tree_sum<64 / CG, 64 / CG>(v);
+  const float total = v[0];
+  if (!row_ok) return;
+#pragma unroll
+  for (int i = 0; i < 64 / CG; ++i) {
+    if (MASK && key0 / C + i >= p.g.m_loc) break;
+    lamrow[(size_t)i * p.g.R] = (cs[i] > 0.f) ? ms + fast_log2(cs[i]) : -INFINITY;
   }
-  float* lam = p.lam2 + (size_t)kvh * p.g.m_loc * p.g.R + rho;
-  if constexpr (C <= 32) {
-#pragma unroll
-    for (int i = 0; i < 32 / C; ++i) {
-      const int chunk = key0 / C + i;
-      if (row_ok && chunk < p.g.m_loc)
-        lam[(size_t)chunk * p.g.R] = (cs[i] > 0.f) ? gms + fast_log2(cs[i]) : -INFINITY;
-    }
-  } else {
-    if (gs > 0.f) {
-      if (CS == 0.f) {
-        CM = gms;
-        CS = gs;
-      } else {
-        const float nm = fmaxf(CM, gms);
-        CS = CS * fast_exp2(CM - nm) + gs * fast_exp2(gms - nm);
-        CM = nm;
+  *lampart_out = (total > 0.f) ? ms + fast_log2(total) : -INFINITY;
+}
+
+// Unit index bookkeeping without integer division in the loops: unit u = pr * MT + r covers
+// (kv head, key tile) pair pr = kvh * NKT + kt and row tile mt = (r + pr) mod MT.
+struct UnitIter {
+  int r, pr, prm, kvh, kt;
+  __device__ __forceinline__ UnitIter(int u, int MT, int NKT) {
+    pr = u / MT;
+    r = u - pr * MT;
+    prm = pr % MT;
+    kvh = pr / NKT;
+    kt = pr - kvh * NKT;
+  }
+  __device__ __forceinline__ int mt(int MT) const { return r + prm >= MT ? r + prm - MT : r + prm; }
+  __device__ __forceinline__ bool last_of_pair(int MT) const { return r + 1 == MT; }
+  __device__ __forceinline__ void next(int MT, int NKT) {
+    if (++r == MT) {
+      r = 0;
+      ++pr;
+      if (++prm == MT) prm = 0;
+      if (++kt == NKT) {
+        kt = 0;
+        ++kvh;
       }
     }
-    if (((key0 + 32) % C) == 0) {
-      const int chunk = key0 / C;
-      if (row_ok && chunk < p.g.m_loc) lam[(size_t)chunk * p.g.R] = (CS > 0.f) ? CM + fast_log2(CS) : -INFINITY;
-      CM = -INFINITY;
-      CS = 0.f;
-    }
   }
-}
+};
 
 template <int C, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -185,27 +187,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tma_prefetch_desc(&tmK);
       ptx::tma_prefetch_desc(&tmQ);
       int kcount = 0, qcount = 0, cur = -1;
-      for (int u = u0; u < u1; ++u) {
-        const int pr = u / p.MT, mt = (u % p.MT + pr) % p.MT;
-        const int kvh = pr / p.NKT, kt = pr % p.NKT;
+      UnitIter it(u0, p.MT, p.NKT);
+      for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT)) {
+        const int pr = it.pr, mt = it.mt(p.MT), kvh = it.kvh, kt = it.kt;
         if (pr != cur) {
           const int kb = kcount & 1;
           ptx::mbar_wait(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
-          ptx::mbar_expect_tx(&k_full[kb], kKBytes);
-          const int y = kvh * p.g.n_pad + kt * BN;
-          uint8_t* dst = kbuf0 + kb * kKBytes;
-          ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
-          ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
+          if constexpr (NP >= 13) {  // tuning: no K traffic
+            ptx::mbar_arrive(&k_full[kb]);
+          } else {
+            ptx::mbar_expect_tx(&k_full[kb], kKBytes);
+            const int y = kvh * p.g.n_pad + kt * BN;
+            uint8_t* dst = kbuf0 + kb * kKBytes;
+            ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
+            ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
+          }
           cur = pr;
           ++kcount;
         }
         const int qs = qcount % kQStages;
         ptx::mbar_wait(&q_empty[qs], ((qcount / kQStages) & 1) ^ 1);
-        ptx::mbar_expect_tx(&q_full[qs], kQBytes);
-        const int yq = kvh * p.R_pad + mt * BM;
-        uint8_t* dq = qbuf0 + qs * kQBytes;
-        ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
-        ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
+        if constexpr (NP >= 12) {  // tuning: no Q traffic
+          ptx::mbar_arrive(&q_full[qs]);
+        } else {
+          ptx::mbar_expect_tx(&q_full[qs], kQBytes);
+          const int yq = kvh * p.R_pad + mt * BM;
+          uint8_t* dq = qbuf0 + qs * kQBytes;
+          ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
+          ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
+        }
         ++qcount;
       }
     }
@@ -213,8 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
       int kcount = 0, qcount = 0, acount = 0, cur = -1, kb = 0;
-      for (int u = u0; u < u1; ++u) {
-        const int pr = u / p.MT;
+      UnitIter it(u0, p.MT, p.NKT);
+      for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT)) {
+        const int pr = it.pr;
         if (pr != cur) {
           kb = kcount & 1;
           ptx::mbar_wait(&k_full[kb], (kcount >> 1) & 1);
@@ -230,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t qa = ptx::smem_u32(qbuf0 + qs * kQBytes);
         const uint32_t ka = ptx::smem_u32(kbuf0 + kb * kKBytes);
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
+        for (int k = 0; k < (NP == 14 ? 0 : D / 16); ++k) {  // 14: tuning, epilogue alone
           const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
           const uint32_t off_k = (k >> 2) * (kKBytes / 2) + (k & 3) * 32;
           ptx::mma_bf16(d_tmem, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k), idesc,
@@ -238,7 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::mma_commit(&q_empty[qs]);
         ptx::mma_commit(&acc_full[ab]);
-        const bool last_of_pair = (u + 1 == u1) || ((u + 1) / p.MT != pr);
+        const bool last_of_pair = (u + 1 == u1) || it.last_of_pair(p.MT);
         if (last_of_pair) ptx::mma_commit(&k_empty[kb]);
         ++qcount;
         ++acount;
@@ -249,46 +260,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;
     const int half = e >> 2;  // column quarter
     const int row_in_tile = quad * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const int nfull = p.g.n_loc / BN;  // key tiles without a ragged tail
     int acount = 0;
-    for (int u = u0; u < u1; ++u) {
-      const int pr = u / p.MT, mt = (u % p.MT + pr) % p.MT;
-      const int kvh = pr / p.NKT, kt = pr % p.NKT;
+    UnitIter it(u0, p.MT, p.NKT);
+    for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT)) {
+      const int mt = it.mt(p.MT), kvh = it.kvh, kt = it.kt;
       const int ab = acount & 1;
       ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
       ptx::tc_fence_after();
       const int rho = mt * BM + row_in_tile;
       const bool row_ok = rho < p.g.R;
-      float HM = -INFINITY, HS = 0.f, CM = -INFINITY, CS = 0.f;
-      // both 32-key groups are read from TMEM first (the accumulator is then released early)
-      // and processed in one unrolled block, so the compiler can overlap the two groups'
-      // exponentials with their reductions
-      float v[BN / kColSplit / 32][32];
-      if constexpr (NP != 11) {
+      // both 32-key groups are read from TMEM, then the accumulator is released at once
+      float v[64];
+      if constexpr (NP < 11 || NP == 14) {
+        uint32_t r0[32], r1[32];
+        const uint32_t ta = tmem_base + (uint32_t)(ab * BN + half * (BN / kColSplit)) + lane_off;
+        ptx::tmem_ld32_nowait(ta, r0);
+        ptx::tmem_ld32_nowait(ta + 32, r1);
+        ptx::tmem_wait_ld_tied(r0);
+        ptx::tmem_wait_ld_tied(r1);
 #pragma unroll
-        for (int gi = 0; gi < BN / kColSplit / 32; ++gi)
-          ptx::tmem_ld32(tmem_base + (uint32_t)(ab * BN + half * (BN / kColSplit) + gi * 32) +
-                             ((uint32_t)(quad * 32) << 16),
-                         v[gi]);
+        for (int j = 0; j < 32; ++j) {
+          v[j] = __uint_as_float(r0[j]);
+          v[32 + j] = __uint_as_float(r1[j]);
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
-#pragma unroll
-      for (int gi = 0; gi < BN / kColSplit / 32; ++gi) {
-        const int col0 = half * (BN / kColSplit) + gi * 32;
-        if constexpr (NP == 11) {  // tuning skeleton: pipeline only
-          HS += 1.f;
-        } else if constexpr (NP == 10) {  // tuning: TMEM drain only
-          HS += v[gi][0] + v[gi][31];
-        } else if (kt * BN + BN > p.g.n_loc) {  // warp-uniform: the last key tile only
-          epilogue_group<C, NP, true>(p, v[gi], kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
-        } else {
-          epilogue_group<C, NP, false>(p, v[gi], kt * BN + col0, kvh, rho, row_ok, HM, HS, CM, CS);
-        }
+      const int key0 = kt * BN + half * (BN / kColSplit);
+      float* lamrow = p.lam2 + ((size_t)kvh * p.g.m_loc + key0 / C) * p.g.R + rho;
+      float* lp = p.lampart + ((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho;
+      if constexpr (NP >= 11 && NP <= 13) {  // tuning skeleton: pipeline only
+        if (row_ok) *lp = 0.f;
+      } else if constexpr (NP == 10) {  // tuning: TMEM drain only
+        if (row_ok) *lp = v[0] + v[63];
+      } else if (kt >= nfull) {  // warp-uniform: the last key tile only
+        epilogue_unit<C, NP, true>(p, v, key0, lamrow, lp, row_ok);
+      } else {
+        epilogue_unit<C, NP, false>(p, v, key0, lamrow, lp, row_ok);
       }
-      if (row_ok)
-        p.lampart[((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho] =
-            (HS > 0.f) ? HM + fast_log2(HS) : -INFINITY;
       ++acount;
     }
   }
@@ -346,7 +358,7 @@ int poly_share() {
   if (np < 0) {
     const char* e = getenv("CKV_SCORE_POLY");
     np = e ? atoi(e) : 0;  // measured on B200: the MUFU-only path is fastest (no FMA offload)
-    if (np != 0 && np != 2 && np != 3 && np != 10 && np != 11) np = 0;
+    if (np < 0 || (np > 3 && np < 10) || np > 14) np = 0;
   }
   return np;
 }
@@ -357,7 +369,11 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
     case 3: return launch_cp<C, 3>(tmK, tmQ, p, grid, st);
     case 10: return launch_cp<C, 10>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
     case 11: return launch_cp<C, 11>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
+    case 12: return launch_cp<C, 12>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
+    case 14: return launch_cp<C, 14>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
+    case 13: return launch_cp<C, 13>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
     case 2: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
+    case 1: return launch_cp<C, 1>(tmK, tmQ, p, grid, st);
     default: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
   }
 }
