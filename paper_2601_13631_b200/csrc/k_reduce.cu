@@ -34,61 +34,57 @@ __device__ __forceinline__ void lse2_merge(float& M, float& S, float m, float s)
 }
 
 constexpr int kRowsPerBlock = 32;
-constexpr int kRowGroups = kRowsPerBlock / 4;  // 8 threads x 4 rows
-constexpr int kSplitGroups = 256 / kRowGroups;  // 32 split groups
+constexpr int kSplitWarps = 32;  // 1024 threads: lane = row, warp = split group
 
-// Block = 256 threads over 32 flattened rows (idx = kvh * R + row = h * ns + r): thread t owns
-// rows 4*(t % 8) .. +3 and splits t/8, t/8 + 32, ...  (4 independent accumulators, coalesced
-// 128-byte row segments per split); the 32 split-group partials are merged in a fixed order.
+// Block = 32 warps over 32 flattened rows (idx = kvh * R + row = h * ns + r): lane l owns row
+// idx0 + l, warp w the splits w, w + 32, ... (each warp load is one coalesced 128-byte row
+// segment; sixteen loads in flight per thread); the 32 split-group partials are merged in a fixed
+// order by warp 0.
 template <typename T>
-__global__ void __launch_bounds__(256) row_lse_kernel(LayerGeom g, const float* __restrict__ lampart, int nsplit,
-                                                      const T* __restrict__ q, const T* __restrict__ ks, int fullrow,
-                                                      const float* __restrict__ lam_all, int W,
-                                                      float* __restrict__ Lam2, float* __restrict__ lam_local_out) {
-  __shared__ float sM[kSplitGroups][kRowsPerBlock + 1], sS[kSplitGroups][kRowsPerBlock + 1];
+__global__ void __launch_bounds__(1024) row_lse_kernel(LayerGeom g, const float* __restrict__ lampart, int nsplit,
+                                                       const T* __restrict__ q, const T* __restrict__ ks, int fullrow,
+                                                       const float* __restrict__ lam_all, int W,
+                                                       float* __restrict__ Lam2, float* __restrict__ lam_local_out) {
+  __shared__ float sM[kSplitWarps][kRowsPerBlock + 1], sS[kSplitWarps][kRowsPerBlock + 1];
   const int nrows = g.Hkv * g.R;
-  const int rg = threadIdx.x % kRowGroups, sg = threadIdx.x / kRowGroups;
-  const int idx0 = blockIdx.x * kRowsPerBlock + rg * 4;
-  float M[4], S[4];
-  const float* base[4];
-  int stride = 0, nparts = 0;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int idx = min(blockIdx.x * kRowsPerBlock + lane, nrows - 1);
+  const float* base;
+  int stride, nparts;
   if (lam_all == nullptr) {
+    const int kvh = idx / g.R, row = idx - kvh * g.R;
+    base = lampart + (size_t)kvh * nsplit * g.R + row;
     stride = g.R;
     nparts = nsplit;
   } else {
+    base = lam_all + idx;
     stride = nrows;
     nparts = W;
   }
+  // up to 16 loads in flight per thread (the whole split range of c3_7b in one round)
+  float M = -INFINITY, S = 0.f;
+  for (int sp0 = w; sp0 < nparts; sp0 += 16 * kSplitWarps) {
+    float v[16];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    M[i] = -INFINITY;
-    S[i] = 0.f;
-    const int idx = min(idx0 + i, nrows - 1);
-    const int kvh = idx / g.R, row = idx % g.R;
-    base[i] = lam_all ? lam_all + idx : lampart + (size_t)kvh * nsplit * g.R + row;
+    for (int i = 0; i < 16; ++i) {
+      const int sp = sp0 + i * kSplitWarps;
+      v[i] = sp < nparts ? base[(size_t)sp * stride] : -INFINITY;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) lse2_acc(M, S, v[i]);
   }
-  for (int sp = sg; sp < nparts; sp += kSplitGroups) {
-    float v[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) v[i] = base[i][(size_t)sp * stride];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) lse2_acc(M[i], S[i], v[i]);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    sM[sg][rg * 4 + i] = M[i];
-    sS[sg][rg * 4 + i] = S[i];
-  }
+  sM[w][lane] = M;
+  sS[w][lane] = S;
   __syncthreads();
-  if (threadIdx.x >= kRowsPerBlock) return;
-  const int idx = blockIdx.x * kRowsPerBlock + threadIdx.x;
-  if (idx >= nrows) return;
+  if (w != 0) return;
+  const int row_idx = blockIdx.x * kRowsPerBlock + lane;
+  if (row_idx >= nrows) return;
   float Mt = -INFINITY, St = 0.f;
-  for (int w = 0; w < kSplitGroups; ++w) lse2_merge(Mt, St, sM[w][threadIdx.x], sS[w][threadIdx.x]);
-  if (lam_all == nullptr && lam_local_out) lam_local_out[idx] = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
+  for (int i = 0; i < kSplitWarps; ++i) lse2_merge(Mt, St, sM[i][lane], sS[i][lane]);
+  if (lam_all == nullptr && lam_local_out) lam_local_out[row_idx] = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
   if (fullrow) {
     // causal suffix keys t <= r of the same KV head (Q1 FULLROW, Q9)
-    const int kvh = idx / g.R, row = idx % g.R;
+    const int kvh = row_idx / g.R, row = row_idx % g.R;
     const int gq = row / g.ns, r = row % g.ns, h = kvh * g.G + gq;
     const float scale = kLog2e * rsqrtf((float)g.d);
     const T* qr = q + ((size_t)r * g.Hq + h) * g.d;
@@ -99,7 +95,7 @@ __global__ void __launch_bounds__(256) row_lse_kernel(LayerGeom g, const float* 
       lse2_acc(Mt, St, acc * scale);
     }
   }
-  Lam2[idx] = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
+  Lam2[row_idx] = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
 }
 
 // One warp per (kv head, chunk j): lanes take 4 consecutive rows at a time (float4 when
@@ -115,6 +111,7 @@ __global__ void chunk_sum_kernel(LayerGeom g, const float* __restrict__ lam2, co
   const float* src = lam2 + ((size_t)kvh * g.m_loc + j) * g.R;
   const float* L = Lam2 + (size_t)kvh * g.R;
   if ((g.R & 3) == 0) {
+#pragma unroll 4
     for (int row = lane * 4; row < g.R; row += 128) {
       const float4 a = *reinterpret_cast<const float4*>(src + row);
       const float4 b = *reinterpret_cast<const float4*>(L + row);
@@ -139,7 +136,7 @@ cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit,
                            int fullrow, const float* lam_all, int W, float* Lam2, float* lam_local_out,
                            cudaStream_t st) {
   const int n = g.Hkv * g.R;
-  row_lse_kernel<T><<<(n + kRowsPerBlock - 1) / kRowsPerBlock, 256, 0, st>>>(g, lampart, nsplit, q, k_suf, fullrow,
+  row_lse_kernel<T><<<(n + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kSplitWarps, 0, st>>>(g, lampart, nsplit, q, k_suf, fullrow,
                                                                              lam_all, W, Lam2, lam_local_out);
   return cudaGetLastError();
 }

@@ -43,6 +43,7 @@ struct TcParams {
   int R_pad;
   int n_units;  // Hkv * NKT * MT
   float scale;  // log2(e) / sqrt(d)
+  int dephase;  // tuning: start delay (cycles) of odd column-quarter warps
 };
 
 // In-place pairwise tree: after the call a[0..N/G) hold sums of consecutive groups of G.
@@ -263,6 +264,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const int nfull = p.g.n_loc / BN;  // key tiles without a ragged tail
     int acount = 0;
+    if (p.dephase > 0 && (half & 1)) {  // start half of the warps of every SMSP later (de-phase)
+      const long long t0 = clock64();
+      while (clock64() - t0 < p.dephase) {
+      }
+    }
     UnitIter it(u0, p.MT, p.NKT);
     for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT)) {
       const int mt = it.mt(p.MT), kvh = it.kvh, kt = it.kt;
@@ -357,7 +363,7 @@ int poly_share() {
   static int np = -1;
   if (np < 0) {
     const char* e = getenv("CKV_SCORE_POLY");
-    np = e ? atoi(e) : 0;  // measured on B200: the MUFU-only path is fastest (no FMA offload)
+    np = e ? atoi(e) : 1;  // measured on B200: 1 of 8 exponentials on the FMA pipe is fastest
     if (np < 0 || (np > 3 && np < 10) || np > 14) np = 0;
   }
   return np;
@@ -401,6 +407,14 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   p.R_pad = p.MT * BM;
   p.n_units = g.Hkv * p.NKT * p.MT;
   p.scale = kLog2e / sqrtf((float)g.d);
+  {
+    static int dp = -1;
+    if (dp < 0) {
+      const char* e = getenv("CKV_SCORE_DEPHASE");
+      dp = e ? atoi(e) : 0;
+    }
+    p.dephase = dp;
+  }
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
   pack_q_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
   cudaError_t e = cudaGetLastError();
