@@ -48,6 +48,8 @@ def _compile(src):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
+    with open(obj[:-2] + ".ptxas.log", "w") as f:  # register / spill report of this object
+        f.write(r.stderr)
     return obj, r.stderr
 
 
@@ -61,8 +63,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
         results = list(ex.map(_compile, srcs))
     objs = [o for o, _ in results]
     log = "".join(e for _, e in results)
-    with open(os.path.join(BUILD, "ptxas.log"), "a") as f:
-        f.write(log)
     if verbose and log:
         print(log)
     if force or _stale(LIB, objs):

@@ -31,7 +31,6 @@ struct ckv_ctx {
   int nsplit_score_max = 1, nsplit_attn_max = 1;
   int score_kind = 0;  // 0 SIMT, 1 tcgen05
   int rec_swz = 0;     // chunk-record layout (rec_elem)
-  int qpack_ns = 0;    // n_s of the GQA-packed Q the tcgen05 score kernel left in tmap_cache (0: none)
   int attn_kind = 0;   // 0 SIMT, 1 tcgen05
 
   void* probe = nullptr;
@@ -51,6 +50,7 @@ struct ckv_ctx {
   int64_t* stats = nullptr;  // [16]
   int32_t* epoch_dev = nullptr;  // request counter on the device (graph-safe)
   void* tmap_cache = nullptr;
+  void* dense_kv = nullptr;  // tcgen05 attention: dense K/V tiles of the current layer
 
   cudaStream_t side = nullptr;
   cudaEvent_t ev_ids = nullptr;
@@ -184,7 +184,6 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
   int nsplit = 0;
   cudaError_t e = cudaErrorNotSupported;
   PROF_BEGIN(0);
-  ctx->qpack_ns = 0;
   if (ctx->score_kind == 1) {
     nsplit = score_tc_nsplit(g);
     e = launch_score_tc(g, static_cast<const __nv_bfloat16*>(q),
@@ -192,7 +191,6 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
                         ctx->tmap_cache, st);
     if (e == cudaSuccess) {
       ctx->launches += 1;  // + the Q pack kernel
-      ctx->qpack_ns = ns;
     }
   }
   if (e == cudaErrorNotSupported) {
@@ -273,11 +271,9 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
       if (nsplit > ctx->nsplit_attn_max) nsplit = ctx->nsplit_attn_max;  // o_part / lse_part capacity
       e = launch_attn_tc(g, static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(ks),
                          static_cast<const __nv_bfloat16*>(vs),
-                         reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->P, ctx->kept_slots, ids,
-                         n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->tmap_cache,
-                         ctx->qpack_ns == ns, st);
-      if (e == cudaSuccess && ctx->qpack_ns != ns) ctx->launches += 1;  // + the Q pack kernel
-      ctx->qpack_ns = 0;
+                         reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->kept_slots, ids,
+                         n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->dense_kv, st);
+      if (e == cudaSuccess) ctx->launches += 1;  // + the dense K/V compaction kernel
     }
     if (e == cudaErrorNotSupported) {
       nsplit = attn_nsplit(ctx, ns, ctx->k);
@@ -313,7 +309,7 @@ void free_all(ckv_ctx* ctx) {
                       ctx->lampart, ctx->Lam2, ctx->A, ctx->Apart, ctx->ids_buf[0], ctx->ids_buf[1], ctx->n_ids_buf[0],
                       ctx->n_ids_buf[1], ctx->kept_slots, ctx->ids_glob, ctx->flag, ctx->scratch_main,
                       ctx->scratch_side, ctx->gl_main, ctx->gl_side, ctx->nload_main, ctx->nload_side, ctx->counts,
-                      ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache, ctx->epoch_dev};
+                      ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache, ctx->dense_kv, ctx->epoch_dev};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (ctx->host_store) cudaFreeHost(ctx->host_store);
@@ -479,8 +475,13 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
     LayerGeom g = geom(ctx, ctx->max_ns);
     ctx->attn_kind = (ctx->dtype == CKV_BF16 && attn_tc_supported(g) && !(c.flags & CKV_FLAG_SIMT_ATTN)) ? 1 : 0;
   }
-  if (ctx->score_kind == 1 || ctx->attn_kind == 1)
+  if (ctx->score_kind == 1)
     CKC(cudaMalloc(&ctx->tmap_cache, score_tc_qpack_elems(ctx->Hkv, R_max) * sizeof(__nv_bfloat16)));
+  if (ctx->attn_kind == 1) {
+    const size_t nb = attn_tc_dense_bytes(geom(ctx, ctx->max_ns), ctx->k, ctx->max_ns);
+    CKC(cudaMalloc(&ctx->dense_kv, nb));
+    CKC(cudaMemset(ctx->dense_kv, 0, nb));
+  }
   CKC(cudaDeviceSynchronize());
 #undef CKC
   (void)st;

@@ -119,11 +119,13 @@ cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, con
                              cudaStream_t st);
 bool attn_tc_supported(const LayerGeom& g);
 int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix);
+// tcgen05 attention = dense K/V compaction + attention kernel; dense_ws holds
+// attn_tc_dense_bytes(g, k_cap, max_ns) bytes, zero-initialised once (padding keys stay finite)
+size_t attn_tc_dense_bytes(const LayerGeom& g, int k_cap, int max_ns);
 cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* k_suf,
-                           const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, int P_slots,
-                           const int32_t* kept_slots, const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap,
-                           int include_suffix, int nsplit, float* o_part, float* lse_part, void* qpack_ws,
-                           bool qpack_ready, cudaStream_t st);
+                           const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
+                           const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
+                           int nsplit, float* o_part, float* lse_part, void* dense_ws, cudaStream_t st);
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit,
                                 T* out, float* o_f32, float* lse_nat, cudaStream_t st);

@@ -1,24 +1,30 @@
-// A7 split-K exact attention on tcgen05 (bf16, d = 128), flash-attention style.
+// A7 split-K exact attention on tcgen05 (bf16, d = 128), flash-attention style, in two kernels.
 //
 // Same contract as attn_simt_kernel (k_attn.cu): for every GQA-packed suffix row and every
 // key split, a normalised partial O and its base-2 LSE over the kept prefix chunks (all
 // visible, partial-chunk padding masked) and the causal suffix keys t <= r
 // (Q6, Q9).  A8 (attn_combine) merges the splits.
 //
-// Per work item (kv head, 128-row tile, key split), 1 CTA per SM, 576 threads:
-//   warp 0      producer: Q tile by TMA (the GQA-packed [Hkv][R_pad][128] Q left by the score
-//               kernel); per 128-key tile the K and V halves of up to 128/c kept chunks straight
-//               from their HBM cache slots, one 1-D bulk copy per (chunk, K|V, half) issued by
-//               many lanes at once (records are stored pre-swizzled, rec_elem), or the suffix
-//               tile through a 3-D TMA map over k_suf / v_suf.  Two 64 KB stages; K and V of a
-//               stage have separate barriers (K(j+2) lands as soon as S(j) is done).
-//   warp 1      TMEM alloc + MMA issue: S = Q K^T (M 128, N 128, K 128; K-major / K-major) into one
-//               of two TMEM S buffers, then O += P V (P K-major from smem, V MN-major) into the TMEM
-//               O accumulator, software-pipelined one tile behind S.
-//   warps 2..17 softmax: one row per thread, four warps per TMEM lane quadrant (32 key columns
-//               and 32 O columns each); row max exchanged through shared memory; lazy O rescale
-//               (only when the running max grows by > 8 in log2 units) via tcgen05.ld/st;
-//               P = 2^(s - m) written as bf16 in the 128-byte-swizzled K-major layout.
+// 1. compact_kv_kernel: the kept chunks' K / V (from their HBM cache slots, records stored
+//    pre-swizzled, rec_elem) and the suffix K / V are copied into a dense per-layer tile image
+//    dense[kvh][tile][K|V][half][128 keys][64] (128-byte swizzle), one warp per 2 KB piece.
+//    Measured on B200: the per-copy issue cost of the bulk-copy engine (~55 ns per copy) made
+//    gathering 2 KB pieces inside the attention kernel (32 copies per tile, for each of the
+//    7 row tiles that reuse a tile) the attention's bound; tensor-core MMAs cost >= ~60 cycles
+//    each whatever N, so per-chunk N = c MMAs are no way around it.
+// 2. attn_tc_kernel: per work item (kv head, 128-row tile, key split), 1 CTA per SM, 576 threads.
+//    TMEM: S0 [0,128) S1 [128,256) (P(j) is written over S(j) as bf16 pairs), O [256,384),
+//    Q [384,448).
+//   warp 0      producer: one 64 KB bulk copy per key tile from the dense image, 3 stages.
+//   warp 1      TMEM alloc + MMA issue: S = Q K^T (M 128, N 128, K 128) with Q (A) from TMEM,
+//               then O += P V with P (A) from TMEM and V (B) MN-major from smem, software-
+//               pipelined one tile behind S.  tcgen05 MMAs execute in issue order, so S(j+2)
+//               (same TMEM buffer) follows PV(j).
+//   warps 2..17 softmax: one row per thread, four warps per TMEM lane quadrant (32 key
+//               columns and 32 O columns each); row max exchanged through shared memory; lazy O
+//               rescale (only when the running max grows by > 8 in log2 units); P = 2^(s - m)
+//               as bf16 into TMEM.  They also load each item's Q rows from q into TMEM.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -33,38 +39,38 @@ constexpr int kSoftWarps = 16;
 constexpr int NWQ = kSoftWarps / 4;  // softmax warps per TMEM lane quadrant
 constexpr int CPW = BN / NWQ;        // key / O columns per softmax warp
 constexpr int kThreads = 64 + 32 * kSoftWarps;
-constexpr uint32_t kQBytes = BM * D * 2;           // 32 KB
-constexpr uint32_t kKVBytes = 2 * BN * D * 2;      // K + V = 64 KB
-constexpr uint32_t kPBytes = BM * BN * 2;          // 32 KB
-constexpr size_t kSmem = kQBytes + 2 * kKVBytes + kPBytes + 4096 + 1024;
-constexpr float kRescaleThresh = 8.f;
-constexpr int kSlotBuf = 1024;              // log2 units
+constexpr int kStages = 3;
+constexpr uint32_t kKVBytes = 2 * BN * D * 2;   // K + V of a 128-key tile = 64 KB
+constexpr uint32_t kPartBytes = kKVBytes / 4;   // one (K|V, half) block: 128 rows x 128 B
+constexpr size_t kSmem = kStages * kKVBytes + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t kOBlockBytes = BM * 32 * 4;  // O staging: [128 rows][32 floats], 128-byte swizzle
+constexpr float kRescaleThresh = 8.f;  // log2 units
+constexpr uint32_t kColO = 256, kColQ = 384;
 
 struct AttnParams {
   LayerGeom g;
-  const int32_t* kept_slots;
+  const __nv_bfloat16* q;  // [ns][Hq][128]
   const int32_t* kept_ids;
   const int32_t* n_kept_dev;
-  int k_cap;
   int include_suffix;
   int nsplit;
-  int MT, R_pad;
+  int MT;
   int NTp_cap, NTs, T_cap;
-  const char* pool;      // this layer's slot pool (swizzled records, rec_elem)
-  int64_t rec_bytes;
-  uint32_t chunk_bytes;  // one (chunk, kv head) K+V block = 4 * c * 128 bytes
+  const char* dense;  // [Hkv][T_cap][64 KB]
   int n_items;
   float scale;
   float* o_part;
   float* lse_part;
-  unsigned long long* trace;  // debug: per-event %globaltimer of CTA 0 (CKV_ATTN_TRACE=1), else null
+  unsigned long long* trace;  // debug: %globaltimer events of CTA 0 (CKV_ATTN_TRACE=1), else null
 };
 
-__device__ __forceinline__ void trace_ev(const AttnParams& p, int ev, int i) {
-  if (p.trace && blockIdx.x == 0 && i < 64) {
+// debug timeline: event e (0 start, 1 q_full seen by MMA, 2 kv_full seen by MMA, 3 s_full seen by
+// softmax, 4 p_full arrived, 5 o_full seen by softmax, 6 epilogue stored), occurrence i
+__device__ __forceinline__ void trace_ev(const AttnParams& p, int e, int i) {
+  if (p.trace && blockIdx.x == 0 && i < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.trace[ev * 64 + i] = t;
+    p.trace[e * 32 + i] = t;
   }
 }
 
@@ -85,76 +91,100 @@ __device__ __forceinline__ bool tile_present(const AttnParams& p, const Tiles& t
   return (t < p.NTp_cap) ? (t < tl.NTp) : (p.include_suffix != 0);
 }
 
-// O += P V for the tile that was scored one step earlier (MMA thread).  Prefix tiles hold
-// `nv` chunk blocks [K h0|K h1|V h0|V h1] of c rows each; suffix tiles hold [K h0|K h1|V h0|V h1]
-// of 128 rows each.  V is the MN-major B operand (d contiguous), P the K-major A operand.
-__device__ __forceinline__ void issue_pv(const AttnParams& p, uint32_t tmem_O, uint32_t pa, uint8_t* kvbuf0,
-                                         uint64_t* p_full, uint64_t* p_empty, uint64_t* o_empty, uint64_t* kv_empty,
-                                         uint64_t* v_full, uint32_t idesc_o, int jj, int stage, int stage_use,
-                                         bool prefix, int nv, int icount, int& pcount) {
-  ptx::mbar_wait(&v_full[stage], (stage_use >> 1) & 1);
+// Dense tile image of the kept chunks and the suffix (see the file comment).  Warp items:
+// prefix (kvh, kept chunk i, part = K h0 | K h1 | V h0 | V h1): c rows of 128 B copied as is
+// (record rows are swizzled by (row & 7) and c % 8 == 0, so they land swizzled);
+// suffix (kvh, key t, K|V): one 256 B row of k_suf / v_suf, 16-byte units swizzled on the way.
+__global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, const char* __restrict__ pool,
+                                                         int64_t rec_bytes, const int32_t* __restrict__ kept_slots,
+                                                         const int32_t* __restrict__ n_kept_dev, int k_cap,
+                                                         const __nv_bfloat16* __restrict__ k_suf,
+                                                         const __nv_bfloat16* __restrict__ v_suf, int include_suffix,
+                                                         int NTp_cap, int T_cap, char* __restrict__ dense) {
+  const int n_kept = *n_kept_dev;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t n_pre = (int64_t)g.Hkv * k_cap * 4;
+  const int64_t n_suf = include_suffix ? (int64_t)g.Hkv * g.ns * 2 : 0;
+  const uint32_t piece = (uint32_t)g.c * 128u;  // bytes of one (K|V, half) block of a chunk
+  for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n_pre + n_suf; w += nwarps) {
+    if (w < n_pre) {
+      const int part = (int)(w & 3);
+      const int64_t ci = w >> 2;
+      const int kvh = (int)(ci / k_cap), i = (int)(ci % k_cap);
+      if (i >= n_kept) continue;
+      const uint4* src = reinterpret_cast<const uint4*>(pool + (int64_t)kept_slots[i] * rec_bytes +
+                                                        (int64_t)kvh * 4 * piece + part * piece);
+      const int key = i * g.c;
+      uint4* dst = reinterpret_cast<uint4*>(dense + ((int64_t)kvh * T_cap + key / BN) * kKVBytes +
+                                            part * kPartBytes + (key % BN) * 128);
+      for (int u = lane; u < (int)(piece / 16); u += 32) dst[u] = src[u];
+    } else {
+      const int64_t si = w - n_pre;
+      const int kv = (int)(si & 1);
+      const int64_t rt = si >> 1;
+      const int kvh = (int)(rt / g.ns), t = (int)(rt % g.ns);
+      if (lane >= 16) continue;
+      const __nv_bfloat16* row = (kv ? v_suf : k_suf) + ((int64_t)t * g.Hkv + kvh) * D;
+      const uint4 val = reinterpret_cast<const uint4*>(row)[lane];
+      const int tile = NTp_cap + t / BN, r = t % BN, half = lane >> 3, u = (lane & 7) ^ (r & 7);
+      uint4* dst = reinterpret_cast<uint4*>(dense + ((int64_t)kvh * T_cap + tile) * kKVBytes +
+                                            (kv * 2 + half) * kPartBytes + r * 128 + u * 16);
+      *dst = val;
+    }
+  }
+}
+
+// O += P V for the tile that was scored one step earlier (MMA thread): P (A) from the tile's
+// S buffer in TMEM, V (B) the MN-major [half][128 keys][64] block of the stage.
+__device__ __forceinline__ void issue_pv(uint32_t tmem, uint8_t* kvbuf0, uint64_t* p_full, uint64_t* pv_done,
+                                         uint64_t* o_empty, uint64_t* kv_empty, uint32_t idesc_o, int jj, int stage,
+                                         int sbuf, int nkeys, int icount, int& pcount) {
   ptx::mbar_wait(p_full, pcount & 1);
   if (jj == 0) ptx::mbar_wait(o_empty, (icount & 1) ^ 1);
   ptx::tc_fence_after();
-  const uint32_t sa = ptx::smem_u32(kvbuf0 + stage * kKVBytes);
-  uint32_t acc = jj > 0 ? 1u : 0u;
-  const int ksteps = prefix ? (nv * p.g.c + 15) / 16 : BN / 16;  // keys of absent chunks are skipped
-  for (int k = 0; k < ksteps; ++k) {
-    const uint64_t adesc = ptx::umma_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32);
-    const uint64_t bdesc = ptx::umma_desc_sw128_mn(sa + kKVBytes / 2 + k * 16 * 128, kKVBytes / 4);
-    ptx::mma_bf16(tmem_O, adesc, bdesc, idesc_o, acc);
-    acc = 1u;
-  }
-  ptx::mma_commit(p_empty);
+  const uint32_t va0 = ptx::smem_u32(kvbuf0 + stage * kKVBytes + 2 * kPartBytes);
+  const int ksteps = (nkeys + 15) / 16;  // key steps past the tile's valid keys are skipped
+  for (int k = 0; k < ksteps; ++k)
+    ptx::mma_bf16_ts(tmem + kColO, tmem + sbuf * BN + k * 8, ptx::umma_desc_sw128_mn(va0 + k * 16 * 128, kPartBytes),
+                     idesc_o, k > 0 || jj > 0 ? 1u : 0u);
+  ptx::mma_commit(pv_done);
   ptx::mma_commit(&kv_empty[stage]);
   ++pcount;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKs,
-                   const __grid_constant__ CUtensorMap tmVs, AttnParams p) {
+__global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmO, AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* qbuf = smem;
-  uint8_t* kvbuf0 = smem + kQBytes;
-  uint8_t* pbuf = kvbuf0 + 2 * kKVBytes;
+  uint8_t* kvbuf0 = smem;
   __shared__ float red_m[NWQ * 128], red_l[NWQ * 128];  // [warp of a quadrant][128 rows]
-  __shared__ int slot_of_pos[16];          // producer: slot of each chunk position of a tile
-  __shared__ int slot_buf[kSlotBuf];       // producer: slot ids of the current item
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pbuf + kPBytes);
-  uint64_t* q_full = bars + 0;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;    // [2] K half of a stage landed
-  uint64_t* k_empty = bars + 14;  // [2] S(j) done with K of the stage
-  uint64_t* v_full = bars + 18;   // [2] V half landed
-  uint64_t* kv_empty = bars + 4;  // [2] PV(j) done with V of the stage
-  uint64_t* s_full = bars + 6;    // [2]
-  uint64_t* s_empty = bars + 8;   // [2]
-  uint64_t* p_full = bars + 10;
-  uint64_t* p_empty = bars + 11;
-  uint64_t* o_full = bars + 12;
-  uint64_t* o_empty = bars + 13;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);  // bars 16, 17 hold the slot
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kKVBytes);
+  uint64_t* kv_full = bars + 0;             // [kStages]
+  uint64_t* kv_empty = bars + kStages;      // [kStages]
+  uint64_t* s_full = bars + 2 * kStages;    // [2]
+  uint64_t* p_full = s_full + 2;
+  uint64_t* pv_done = p_full + 1;
+  uint64_t* o_full = pv_done + 1;
+  uint64_t* o_empty = o_full + 1;
+  uint64_t* q_full = o_empty + 1;
+  uint64_t* epi_done = q_full + 1;  // the item's O staging (in stage 0) has been stored
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_kept = *p.n_kept_dev;
-  if (threadIdx.x == 0) trace_ev(p, 5, 0);
+  if (threadIdx.x == 0) trace_ev(p, 0, 0);
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, 1);
-    ptx::mbar_init(q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(&k_full[i], 1);
-      ptx::mbar_init(&k_empty[i], 1);
-      ptx::mbar_init(&v_full[i], 1);
+    for (int i = 0; i < kStages; ++i) {
+      ptx::mbar_init(&kv_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
-      ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&s_empty[i], kSoftWarps);
     }
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(&s_full[i], 1);
     ptx::mbar_init(p_full, kSoftWarps);
-    ptx::mbar_init(p_empty, 1);
+    ptx::mbar_init(pv_done, 1);
     ptx::mbar_init(o_full, 1);
     ptx::mbar_init(o_empty, kSoftWarps);
+    ptx::mbar_init(q_full, kSoftWarps);
+    ptx::mbar_init(epi_done, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc<512>(tmem_slot);
@@ -162,152 +192,117 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_O = tmem + 256;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer (whole warp:
-    // lanes fetch the tile's slot ids in parallel, lane 0 issues the copies)
+    // ------------------------------------------------------------ bulk-copy producer
     if (lane == 0) {
-      ptx::tma_prefetch_desc(&tmQ);
-    }
-    int icount = 0, kvcount = 0;
-    const int cpt = BN / p.g.c;  // chunks per key tile (<= 16)
-    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
-      const int sp = it % p.nsplit, mt = (it / p.nsplit) % p.MT, kvh = it / (p.nsplit * p.MT);
-      const Tiles tl = item_tiles(p, sp, n_kept);
-      if (lane == 0) {
-        ptx::mbar_wait(q_empty, (icount & 1) ^ 1);
-        ptx::mbar_expect_tx(q_full, kQBytes);
-        const int yq = kvh * p.R_pad + mt * BM;
-        ptx::tma_load_2d(qbuf, &tmQ, q_full, 0, yq);
-        ptx::tma_load_2d(qbuf + kQBytes / 2, &tmQ, q_full, 64, yq);
-      }
-      // all slot ids of the item's kept chunks, staged in shared memory once per item
-      const int c_beg = min(tl.t0, p.NTp_cap) * cpt;
-      const int c_end = min(min(tl.t1, p.NTp_cap) * cpt, n_kept);
-      for (int i = c_beg + lane; i < c_end && i - c_beg < kSlotBuf; i += 32) slot_buf[i - c_beg] = p.kept_slots[i];
-      __syncwarp();
-      for (int t = tl.t0; t < tl.t1; ++t) {
-        if (!tile_present(p, tl, t)) continue;
-        const int st = kvcount & 1;
-        uint8_t* kb = kvbuf0 + st * kKVBytes;
-        const bool prefix = t < p.NTp_cap;
-        const int nv = prefix ? min(cpt, n_kept - t * cpt) : 0;
-        // c = 8 with an odd chunk count: the last 16-key MMA step also spans the next (absent)
-        // chunk position, so fill it with a duplicate (finite V; its P is masked to 0)
-        const int ncopy = (prefix && (nv * p.g.c) % 16) ? nv + 1 : nv;
-        // K and V of a stage have separate barriers: K(j+2) may land as soon as S(j) is done,
-        // V(j+2) once PV(j) is done
-        const uint32_t hb = p.g.c * 128u;  // bytes of one (K|V, half) block
-        if (prefix && lane < cpt && lane < nv) {
-          const int ci = t * cpt + lane;
-          slot_of_pos[lane] = (ci - c_beg < kSlotBuf) ? slot_buf[ci - c_beg] : p.kept_slots[ci];
+      const int n_kept = *p.n_kept_dev;
+      int kvcount = 0, icount = 0;
+      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
+        const int sp = it % p.nsplit, kvh = it / (p.nsplit * p.MT);
+        const Tiles tl = item_tiles(p, sp, n_kept);
+        // stage 0 doubles as the previous item's O staging buffer
+        if (icount > 0) ptx::mbar_wait(epi_done, (icount - 1) & 1);
+        for (int t = tl.t0; t < tl.t1; ++t) {
+          if (!tile_present(p, tl, t)) continue;
+          const int st = kvcount % kStages;
+          ptx::mbar_wait(&kv_empty[st], ((kvcount / kStages) & 1) ^ 1);
+          ptx::mbar_expect_tx(&kv_full[st], kKVBytes);
+          ptx::bulk_g2s(kvbuf0 + st * kKVBytes, p.dense + ((int64_t)kvh * p.T_cap + t) * kKVBytes, kKVBytes,
+                        &kv_full[st]);
+          ++kvcount;
         }
-        for (int kv = 0; kv < 2; ++kv) {
-          uint64_t* full = kv == 0 ? &k_full[st] : &v_full[st];
-          if (lane == 0) {
-            ptx::mbar_wait(kv == 0 ? &k_empty[st] : &kv_empty[st], ((kvcount >> 1) & 1) ^ 1);
-            ptx::mbar_expect_tx(full, prefix ? ncopy * 2 * hb : kKVBytes / 2);
-            if (kv == 0) trace_ev(p, 0, kvcount);
-          }
-          __syncwarp();  // slot ids visible; expect_tx precedes every complete_tx of this phase
-          uint8_t* dstb = kb + kv * (kKVBytes / 2);
-          if (prefix) {
-            // two contiguous bulk copies per kept chunk and operand (h0, h1 of the swizzled
-            // record image, rec_elem) into rows [q c, (q+1) c) of the [half][128 keys][128 B]
-            // tile; issued by many lanes at once (one issuing thread serialises them)
-            for (int w = lane; w < ncopy * 2; w += 32) {
-              const int q = w >> 1, hh = w & 1;
-              const int sl = slot_of_pos[q < nv ? q : nv - 1];
-              const char* src = p.pool + (int64_t)sl * p.rec_bytes + (int64_t)kvh * p.chunk_bytes + (kv * 2 + hh) * hb;
-              ptx::bulk_g2s(dstb + hh * (kKVBytes / 4) + q * hb, src, hb, full);
-            }
-          } else if (lane == 0) {
-            const int ts0 = (t - p.NTp_cap) * BN;
-            const CUtensorMap* m = kv == 0 ? &tmKs : &tmVs;
-            ptx::tma_load_3d(dstb, m, full, 0, kvh, ts0);
-            ptx::tma_load_3d(dstb + kKVBytes / 4, m, full, 64, kvh, ts0);
-          }
-        }
-        __syncwarp();
-        ++kvcount;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
+      const int n_kept = *p.n_kept_dev;
+      int n_valid_prefix = 0;  // keys of the kept prefix (the last kept chunk may be partial)
+      if (n_kept > 0)
+        n_valid_prefix = (n_kept - 1) * p.g.c + min(p.g.c, p.g.n_loc - p.kept_ids[n_kept - 1] * p.g.c);
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);
       constexpr uint32_t idesc_o = ptx::idesc_bf16_f32(BM, D, true);
-      const int cpt = BN / p.g.c;
       int icount = 0, kvcount = 0, scount = 0, pcount = 0;
-      const uint32_t qa = ptx::smem_u32(qbuf);
-      const uint32_t pa = ptx::smem_u32(pbuf);
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
         const int sp = it % p.nsplit;
         const Tiles tl = item_tiles(p, sp, n_kept);
         ptx::mbar_wait(q_full, icount & 1);
-        int j = 0, prev_stage = 0, prev_nv = 0, prev_use = 0;
-        bool prev_prefix = false;
+        trace_ev(p, 1, icount);
+        int j = 0, prev_stage = 0, prev_sb = 0, prev_keys = 0;
         for (int t = tl.t0; t < tl.t1; ++t) {
           if (!tile_present(p, tl, t)) continue;
-          const int st = kvcount & 1;
-          ptx::mbar_wait(&k_full[st], (kvcount >> 1) & 1);
-          trace_ev(p, 1, kvcount);
-          const int sb = scount & 1;
-          ptx::mbar_wait(&s_empty[sb], ((scount >> 1) & 1) ^ 1);
+          const int st = kvcount % kStages;
+          ptx::mbar_wait(&kv_full[st], (kvcount / kStages) & 1);
+          trace_ev(p, 2, kvcount);
           ptx::tc_fence_after();
+          const int sb = scount & 1;
           const uint32_t ka = ptx::smem_u32(kvbuf0 + st * kKVBytes);
-          const bool prefix = t < p.NTp_cap;
-          const int nv = prefix ? min(cpt, n_kept - t * cpt) : 0;
 #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
-            const uint32_t off_k = (k >> 2) * (kKVBytes / 4) + (k & 3) * 32;
-            ptx::mma_bf16(tmem + sb * BN, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k),
-                          idesc_s, k > 0 ? 1u : 0u);
-          }
+          for (int k = 0; k < D / 16; ++k)
+            ptx::mma_bf16_ts(tmem + sb * BN, tmem + kColQ + k * 8,
+                             ptx::umma_desc_sw128(ka + (k >> 2) * kPartBytes + (k & 3) * 32), idesc_s, k > 0 ? 1u : 0u);
           ptx::mma_commit(&s_full[sb]);
-          ptx::mma_commit(&k_empty[st]);
-          trace_ev(p, 2, scount);
           ++scount;
           if (j > 0)
-            issue_pv(p, tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, v_full, idesc_o, j - 1, prev_stage,
-                     prev_use, prev_prefix, prev_nv, icount, pcount);
+            issue_pv(tmem, kvbuf0, p_full, pv_done, o_empty, kv_empty, idesc_o, j - 1, prev_stage, prev_sb, prev_keys,
+                     icount, pcount);
           prev_stage = st;
-          prev_use = kvcount;
-          prev_prefix = prefix;
-          prev_nv = nv;
+          prev_sb = sb;
+          prev_keys = (t < p.NTp_cap) ? min(BN, n_valid_prefix - t * BN) : min(BN, p.g.ns - (t - p.NTp_cap) * BN);
           ++kvcount;
           ++j;
         }
         if (j > 0)
-          issue_pv(p, tmem_O, pa, kvbuf0, p_full, p_empty, o_empty, kv_empty, v_full, idesc_o, j - 1, prev_stage,
-                   prev_use, prev_prefix, prev_nv, icount, pcount);
-        ptx::mma_commit(q_empty);
+          issue_pv(tmem, kvbuf0, p_full, pv_done, o_empty, kv_empty, idesc_o, j - 1, prev_stage, prev_sb, prev_keys,
+                   icount, pcount);
         ptx::mma_commit(o_full);
       }
     }
   } else {
     // ------------------------------------------------------------ softmax / epilogue
     // kSoftWarps = 16: four warps per TMEM lane quadrant, each owning CPW = 32 key columns
-    // of S, the same 32 columns of O, and 32 keys (64 bytes) of every P row.
+    // of S (= 16 P columns), the same 32 columns of O and 32 elements (16 columns) of Q.
     const int e = warp - 2, quad = warp & 3, h = e >> 2;
     const int rit = quad * 32 + lane;  // row in tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t bar_id = 1 + quad;  // named barrier of the quadrant's NWQ warps
     int icount = 0, scount = 0, pcount = 0;
+    int n_kept = -1, n_valid_prefix = 0;
     const float sc = p.scale;
-    int n_valid_prefix = 0;
-    if (n_kept > 0) {
-      const int last = p.kept_ids[n_kept - 1];
-      n_valid_prefix = (n_kept - 1) * p.g.c + min(p.g.c, p.g.n_loc - last * p.g.c);
-    }
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
       const int sp = it % p.nsplit, mt = (it / p.nsplit) % p.MT, kvh = it / (p.nsplit * p.MT);
-      const Tiles tl = item_tiles(p, sp, n_kept);
       const int rho = mt * BM + rit;
       const bool row_ok = rho < p.g.R;
-      const int r = rho % p.g.ns;
+      const int gq = rho / p.g.ns, r = rho - gq * p.g.ns;
+      {  // Q rows of this item -> TMEM (the previous item's MMAs are all complete: o_full)
+        uint32_t qv[16];
+        if (row_ok) {
+          const uint4* src = reinterpret_cast<const uint4*>(p.q + ((size_t)r * p.g.Hq + kvh * p.g.G + gq) * D + h * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint4 u = src[i];
+            qv[4 * i] = u.x;
+            qv[4 * i + 1] = u.y;
+            qv[4 * i + 2] = u.z;
+            qv[4 * i + 3] = u.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) qv[i] = 0u;
+        }
+        if (n_kept < 0) {  // first item: issued while the Q loads are in flight
+          n_kept = *p.n_kept_dev;
+          if (n_kept > 0)
+            n_valid_prefix = (n_kept - 1) * p.g.c + min(p.g.c, p.g.n_loc - p.kept_ids[n_kept - 1] * p.g.c);
+        }
+        ptx::tmem_st16_nowait(tmem + kColQ + h * 16 + lane_off, qv);
+        ptx::tmem_wait_st();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(q_full);
+      }
+      const Tiles tl = item_tiles(p, sp, n_kept);
       float m_ref = -INFINITY, l = 0.f;
       int j = 0;
       for (int t = tl.t0; t < tl.t1; ++t) {
@@ -318,9 +313,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         float x[CPW];
         ptx::tmem_ld32p(tmem + sb * BN + h * CPW + lane_off, x);
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&s_empty[sb]);  // S buffer consumed into registers
         ++scount;
         const bool pre = t < p.NTp_cap;
         const int b0 = (pre ? t * BN : (t - p.NTp_cap) * BN) + h * CPW;
@@ -338,6 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int i = 0; i < n; ++i) mx[i] = fmaxf(mx[i], mx[i + n]);
         red_m[h * 128 + rit] = mx[0];
+        // after this barrier every warp of the quadrant holds its S columns in registers, so
+        // P may be written over the S buffer
         ptx::named_bar_sync(bar_id, 32 * NWQ);
         float tmax = red_m[rit];
 #pragma unroll
@@ -362,26 +356,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float lsum = (ls[0] + ls[1]) + (ls[2] + ls[3]);
         if (__any_sync(0xffffffffu, resc)) {
           // lazy rescale: O must hold PV(j-1) before it is multiplied by 2^(m_old - m_new)
-          ptx::mbar_wait(p_empty, (pcount - 1) & 1);
+          ptx::mbar_wait(pv_done, (pcount - 1) & 1);
           ptx::tc_fence_after();
           float o[32];
-          const uint32_t ta = tmem_O + h * CPW + lane_off;
+          const uint32_t ta = tmem + kColO + h * CPW + lane_off;
           ptx::tmem_ld32(ta, o);
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] *= f;
           ptx::tmem_st32(ta, o);
         }
         l = l * f + lsum;
-        // P buffer free (PV(j-1) done reading it)?  keys [h*32, h*32+32) = half h/2, units
-        // 4*(h&1) .. 4*(h&1)+3 of the 128-byte row, swizzled by (row & 7)
-        ptx::mbar_wait(p_empty, (pcount & 1) ^ 1);
-        const uint32_t prow = ptx::smem_u32(pbuf) + (h >> 1) * (kPBytes / 2) + rit * 128;
-#pragma unroll
-        for (int c16 = 0; c16 < CPW / 8; ++c16) {
-          const uint32_t phys = (uint32_t)(((h & 1) * 4 + c16) ^ (rit & 7));
-          ptx::st_shared_v4(prow + phys * 16, pk[4 * c16], pk[4 * c16 + 1], pk[4 * c16 + 2], pk[4 * c16 + 3]);
-        }
-        ptx::fence_proxy_async_smem();
+        // P(j) over S(j): keys [h*32, h*32+32) -> columns [h*16, h*16+16) of the S buffer
+        ptx::tmem_st16_nowait(tmem + sb * BN + h * (CPW / 2) + lane_off, pk);
+        ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(p_full);
@@ -391,6 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       // final O of this item
       ptx::mbar_wait(o_full, icount & 1);
+      if (warp == 2 && lane == 0) trace_ev(p, 5, icount);
       ptx::tc_fence_after();
       red_l[h * 128 + rit] = l;
       ptx::named_bar_sync(bar_id, 32 * NWQ);
@@ -399,45 +387,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int w = 0; w < NWQ; ++w) ltot += red_l[w * 128 + rit];
       ptx::named_bar_sync(bar_id, 32 * NWQ);
       float o[32];
-      if (j > 0) ptx::tmem_ld32(tmem_O + h * CPW + lane_off, o);
+      if (j > 0) ptx::tmem_ld32(tmem + kColO + h * CPW + lane_off, o);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(o_empty);
-      if (row_ok) {
+      // O rows -> swizzled staging in stage 0 (free: every MMA of the item is complete and the
+      // producer waits epi_done before the next item) -> four TMA box stores (rows >= R clipped)
+      {
         const float inv = (j > 0 && ltot > 0.f) ? 1.f / ltot : 0.f;
-        float* dst = p.o_part + (((size_t)sp * p.g.Hkv + kvh) * p.g.R + rho) * D + h * CPW;
+        const uint32_t srow = ptx::smem_u32(kvbuf0) + h * kOBlockBytes + rit * 128;
 #pragma unroll
-        for (int i = 0; i < CPW; i += 4)
-          *reinterpret_cast<float4*>(dst + i) =
-              (j > 0) ? make_float4(o[i] * inv, o[i + 1] * inv, o[i + 2] * inv, o[i + 3] * inv)
-                      : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (h == 0)
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t a = srow + (uint32_t)((u ^ (rit & 7)) * 16);
+          if (j > 0)
+            ptx::st_shared_v4(a, __float_as_uint(o[4 * u] * inv), __float_as_uint(o[4 * u + 1] * inv),
+                              __float_as_uint(o[4 * u + 2] * inv), __float_as_uint(o[4 * u + 3] * inv));
+          else
+            ptx::st_shared_v4(a, 0u, 0u, 0u, 0u);
+        }
+        if (row_ok && h == 0)
           p.lse_part[((size_t)sp * p.g.Hkv + kvh) * p.g.R + rho] =
               (j > 0 && ltot > 0.f) ? m_ref + fast_log2(ltot) : -INFINITY;
       }
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(5, 32 * kSoftWarps);
+      if (warp == 2 && lane == 0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          ptx::tma_store_3d(&tmO, kvbuf0 + b * kOBlockBytes, b * 32, mt * BM, sp * p.g.Hkv + kvh);
+        ptx::bulk_commit();
+        ptx::bulk_wait_read0();
+        ptx::mbar_arrive(epi_done);
+      }
+      if (warp == 2 && lane == 0) trace_ev(p, 6, icount);
     }
   }
+  if (warp == 2 && lane == 0) ptx::bulk_wait0();
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem);
-  }
-}
-
-__global__ void pack_q_attn_kernel(LayerGeom g, int R_pad, const __nv_bfloat16* __restrict__ q,
-                                   __nv_bfloat16* __restrict__ qpack) {
-  const int64_t total = (int64_t)g.Hkv * R_pad * (D / 8);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-    const int x8 = (int)(i % (D / 8));
-    const int64_t row = i / (D / 8);
-    const int kvh = (int)(row / R_pad), rho = (int)(row % R_pad);
-    uint4 val = make_uint4(0, 0, 0, 0);
-    if (rho < g.R) {
-      const int gq = rho / g.ns, r = rho % g.ns;
-      val = *reinterpret_cast<const uint4*>(q + ((int64_t)r * g.Hq + kvh * g.G + gq) * D + x8 * 8);
-    }
-    *reinterpret_cast<uint4*>(qpack + row * D + x8 * 8) = val;
   }
 }
 
@@ -468,44 +458,40 @@ int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix) {
   return s < 1 ? 1 : s;
 }
 
+size_t attn_tc_dense_bytes(const LayerGeom& g, int k_cap, int max_ns) {
+  const int T_cap = (k_cap * g.c + BN - 1) / BN + (max_ns + BN - 1) / BN;
+  return (size_t)g.Hkv * T_cap * kKVBytes;
+}
+
 cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* k_suf,
-                           const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, int P_slots,
-                           const int32_t* kept_slots, const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap,
-                           int include_suffix, int nsplit, float* o_part, float* lse_part, void* qpack_ws,
-                           bool qpack_ready, cudaStream_t st) {
-  if (!attn_tc_supported(g) || !qpack_ws) return cudaErrorNotSupported;
+                           const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
+                           const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
+                           int nsplit, float* o_part, float* lse_part, void* dense_ws, cudaStream_t st) {
+  if (!attn_tc_supported(g) || !dense_ws) return cudaErrorNotSupported;
   AttnParams p;
   p.g = g;
-  p.kept_slots = kept_slots;
+  p.q = q;
   p.kept_ids = kept_ids;
   p.n_kept_dev = n_kept_dev;
-  p.k_cap = k_cap;
   p.include_suffix = include_suffix;
   p.nsplit = nsplit;
   p.MT = (g.R + BM - 1) / BM;
-  p.R_pad = p.MT * BM;
   p.NTp_cap = (k_cap * g.c + BN - 1) / BN;
   p.NTs = (g.ns + BN - 1) / BN;
   p.T_cap = p.NTp_cap + (include_suffix ? p.NTs : 0);
-  p.pool = reinterpret_cast<const char*>(pool_layer);
-  p.rec_bytes = (int64_t)2 * g.Hkv * g.c * D * 2;
-  p.chunk_bytes = 4u * g.c * 128u;
-  (void)P_slots;
+  p.dense = static_cast<const char*>(dense_ws);
   p.n_items = g.Hkv * p.MT * nsplit;
   p.scale = kLog2e / sqrtf((float)g.d);
   p.o_part = o_part;
   p.lse_part = lse_part;
-  auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
-  cudaError_t e = cudaSuccess;
-  if (!qpack_ready) {  // the tcgen05 score kernel already packed this layer's Q otherwise
-    pack_q_attn_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  CUtensorMap tmQ, tmKs, tmVs;
-  if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_3d(&tmKs, k_suf, D, g.Hkv, g.ns, BN)) return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_3d(&tmVs, v_suf, D, g.Hkv, g.ns, BN)) return cudaErrorInvalidValue;
+  const int64_t rec_bytes = (int64_t)2 * g.Hkv * g.c * D * 2;
+  const int64_t n_warps = (int64_t)g.Hkv * k_cap * 4 + (include_suffix ? (int64_t)g.Hkv * g.ns * 2 : 0);
+  const int cblocks = (int)std::min<int64_t>((n_warps + 7) / 8, 8 * sm_count());
+  compact_kv_kernel<<<cblocks, 256, 0, st>>>(g, reinterpret_cast<const char*>(pool_layer), rec_bytes, kept_slots,
+                                             n_kept_dev, k_cap, k_suf, v_suf, include_suffix, p.NTp_cap, p.T_cap,
+                                             static_cast<char*>(dense_ws));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   static bool attr = false;
   if (!attr) {
     e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
@@ -518,20 +504,22 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   if (trace_mode < 0) {
     const char* ev = getenv("CKV_ATTN_TRACE");
     trace_mode = (ev && ev[0] == '1') ? 1 : 0;
-    if (trace_mode) cudaMalloc(&trace_buf, 6 * 64 * sizeof(unsigned long long));
+    if (trace_mode) cudaMalloc(&trace_buf, 7 * 32 * sizeof(unsigned long long));
   }
   p.trace = trace_buf;
-  if (trace_buf) cudaMemsetAsync(trace_buf, 0, 6 * 64 * sizeof(unsigned long long), st);
-  attn_tc_kernel<<<grid, kThreads, kSmem, st>>>(tmQ, tmKs, tmVs, p);
-  if (trace_buf) {  // debug only: synchronous dump of CTA 0's event times (ns since kernel start)
-    unsigned long long h[6 * 64];
+  if (trace_buf) cudaMemsetAsync(trace_buf, 0, 7 * 32 * sizeof(unsigned long long), st);
+  CUtensorMap tmO;
+  if (!make_tmap_f32_3d_store(&tmO, o_part, D, (uint64_t)g.R, (uint64_t)nsplit * g.Hkv, BM))
+    return cudaErrorInvalidValue;
+  attn_tc_kernel<<<grid, kThreads, kSmem, st>>>(tmO, p);
+  if (trace_buf) {  // debug only: synchronous dump of CTA 0's event times (us since kernel start)
+    unsigned long long h[7 * 32];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, trace_buf, sizeof h, cudaMemcpyDeviceToHost);
-    const unsigned long long t0 = h[5 * 64];
-    const char* nm[5] = {"tma_issue", "kv_full", "s_commit", "s_full@sm", "p_full@sm"};
-    for (int e = 0; e < 5; ++e) {
-      fprintf(stderr, "[attn trace] %-10s", nm[e]);
-      for (int i = 0; i < 12; ++i) fprintf(stderr, " %7.2f", h[e * 64 + i] ? (h[e * 64 + i] - t0) * 1e-3 : -1.0);
+    const char* nm[7] = {"start", "q_full", "kv_full", "s_full", "p_full", "o_full", "stored"};
+    for (int e = 1; e < 7; ++e) {
+      fprintf(stderr, "[attn trace] %-8s", nm[e]);
+      for (int i = 0; i < 10; ++i) fprintf(stderr, " %6.2f", h[e * 32 + i] ? (h[e * 32 + i] - h[0]) * 1e-3 : -1.0);
       fprintf(stderr, "\n");
     }
   }

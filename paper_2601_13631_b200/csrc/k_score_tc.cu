@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pr = it.pr, mt = it.mt(p.MT), kvh = it.kvh, kt = it.kt;
         if (pr != cur) {
           const int kb = kcount & 1;
-          ptx::mbar_wait(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
+          ptx::mbar_wait_sleep(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
           if constexpr (NP >= 13) {  // tuning: no K traffic
             ptx::mbar_arrive(&k_full[kb]);
           } else {
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           ++kcount;
         }
         const int qs = qcount % kQStages;
-        ptx::mbar_wait(&q_empty[qs], ((qcount / kQStages) & 1) ^ 1);
+        ptx::mbar_wait_sleep(&q_empty[qs], ((qcount / kQStages) & 1) ^ 1);
         if constexpr (NP >= 12) {  // tuning: no Q traffic
           ptx::mbar_arrive(&q_full[qs]);
         } else {
@@ -229,14 +229,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pr = it.pr;
         if (pr != cur) {
           kb = kcount & 1;
-          ptx::mbar_wait(&k_full[kb], (kcount >> 1) & 1);
+          ptx::mbar_wait_sleep(&k_full[kb], (kcount >> 1) & 1);
           ++kcount;
           cur = pr;
         }
         const int qs = qcount % kQStages;
-        ptx::mbar_wait(&q_full[qs], (qcount / kQStages) & 1);
+        ptx::mbar_wait_sleep(&q_full[qs], (qcount / kQStages) & 1);
         const int ab = acount & 1;
-        ptx::mbar_wait(&acc_empty[ab], ((acount >> 1) & 1) ^ 1);
+        ptx::mbar_wait_sleep(&acc_empty[ab], ((acount >> 1) & 1) ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + ab * BN;
         const uint32_t qa = ptx::smem_u32(qbuf0 + qs * kQBytes);

@@ -12,7 +12,7 @@
 
 using namespace ckv;
 
-template <int N>
+template <int N, bool TS = false>
 __global__ void __launch_bounds__(576, 1) mma_kernel(int units, int mode, long long* cyc) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -48,12 +48,34 @@ __global__ void __launch_bounds__(576, 1) mma_kernel(int units, int mode, long l
       if (mode == 1 && u >= 2) ptx::mbar_wait(&acc_full[ab], ((u - 2) >> 1) & 1);
       if (mode == 2) ptx::mbar_wait(&acc_empty[ab], ((u >> 1) & 1) ^ 1);
       ptx::tc_fence_after();
+      if (mode == 3) {  // 128 / N independent N-wide accumulators, K-step outer (interleaved)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+          for (int c = 0; c < 128 / N; ++c)
+            ptx::mma_bf16_ts(tmem + ab * 128 + c * N, tmem + 384 + k * 8,
+                             ptx::umma_desc_sw128(ptx::smem_u32(B) + (k >> 2) * (N * 128) + (k & 3) * 32), idesc, k > 0);
+        continue;
+      }
+      if (mode == 4) {  // same, chunk outer (dependent accumulations back to back)
+#pragma unroll
+        for (int c = 0; c < 128 / N; ++c)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::mma_bf16_ts(tmem + ab * 128 + c * N, tmem + 384 + k * 8,
+                             ptx::umma_desc_sw128(ptx::smem_u32(B) + (k >> 2) * (N * 128) + (k & 3) * 32), idesc, k > 0);
+        continue;
+      }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         const uint32_t oa = (k >> 2) * 16384 + (k & 3) * 32;
         const uint32_t ob = (k >> 2) * (N * 128) + (k & 3) * 32;
-        ptx::mma_bf16(tmem + ab * 256, ptx::umma_desc_sw128(ptx::smem_u32(A) + oa),
-                      ptx::umma_desc_sw128(ptx::smem_u32(B) + ob), idesc, k > 0);
+        if constexpr (TS)
+          ptx::mma_bf16_ts(tmem + ab * 128, tmem + 384 + k * 8, ptx::umma_desc_sw128(ptx::smem_u32(B) + ob), idesc,
+                           k > 0);
+        else
+          ptx::mma_bf16(tmem + ab * 256, ptx::umma_desc_sw128(ptx::smem_u32(A) + oa),
+                        ptx::umma_desc_sw128(ptx::smem_u32(B) + ob), idesc, k > 0);
       }
       if (mode >= 1) ptx::mma_commit(&acc_full[ab]);
     }
@@ -75,18 +97,18 @@ __global__ void __launch_bounds__(576, 1) mma_kernel(int units, int mode, long l
   if (warp == 1) ptx::tmem_dealloc<512>(tmem);
 }
 
-template <int N>
+template <int N, bool TS = false>
 void run(int units, int mode) {
   const size_t smem = 1024 + 32768 + N * 256 + 128;
-  cudaFuncSetAttribute(mma_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(mma_kernel<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   long long* cyc;
   cudaMalloc(&cyc, 148 * sizeof(long long));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  mma_kernel<N><<<148, 576, smem>>>(units, mode, cyc);
+  mma_kernel<N, TS><<<148, 576, smem>>>(units, mode, cyc);
   cudaEventRecord(e0);
-  mma_kernel<N><<<148, 576, smem>>>(units, mode, cyc);
+  mma_kernel<N, TS><<<148, 576, smem>>>(units, mode, cyc);
   cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -99,17 +121,25 @@ void run(int units, int mode) {
   cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
   double avg = 0;
   for (int i = 0; i < 148; ++i) avg += h[i] / 148.0;
-  const double flops = 2.0 * 128 * N * 128 * (double)units * 148;
-  printf("N=%d mode=%d units=%d: %.1f cyc/unit (floor %d), kernel %.2f us, %.0f TFLOP/s\n", N, mode, units,
+  const double flops = 2.0 * 128 * (mode >= 3 ? 128 : N) * 128 * (double)units * 148;
+  printf("%s N=%d mode=%d units=%d: %.1f cyc/unit (floor %d), kernel %.2f us, %.0f TFLOP/s\n", TS ? "TS" : "SS", N,
+         mode, units,
          avg / units, 8 * 128 * N / 256, ms * 1e3, flops / (ms * 1e-3) / 1e12);
   cudaFree(cyc);
 }
 
 int main() {
-  for (int mode = 0; mode < 3; ++mode) {
-    run<256>(256, mode);
-    run<128>(256, mode);
-  }
-  run<256>(24, 2);
+  run<256>(256, 0);
+  run<128>(256, 0);
+  run<16>(256, 0);
+  run<128, true>(256, 0);
+  run<64, true>(256, 0);
+  run<32, true>(256, 0);
+  run<16, true>(256, 0);
+  run<8, true>(256, 0);
+  run<16, true>(256, 3);
+  run<16, true>(256, 4);
+  run<8, true>(256, 3);
+  run<32, true>(256, 3);
   return 0;
 }

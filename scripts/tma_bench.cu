@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(32) gather_kernel(const __grid_constant__ CUte
       for (int q = 0; q < 32; ++q) bulk1d(dst + q * 2048, base + (size_t)r[t * 32 + q] * 256, 2048, &bar[s]);
     } else if (mode == 2) {
       for (int q = 0; q < 8; ++q) bulk1d(dst + q * 8192, base + (size_t)r[t * 32 + q] * 256, 8192, &bar[s]);
+    } else if (mode == 4) {
+      for (int q = 0; q < 16; ++q) bulk1d(dst + q * 4096, base + (size_t)r[t * 32 + q] * 256, 4096, &bar[s]);
     } else {
       for (int q = 0; q < 4; ++q) tma2d(dst + q * 16384, &m128, &bar[s], (q & 1) * 64, (r[t * 32] / 128) * 128);
     }
@@ -100,8 +102,8 @@ int main() {
   enc(&m128, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, b128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 65536);
-  const char* names[4] = {"tma2d 32x2KB", "bulk 32x2KB", "bulk 8x8KB", "tma2d 4x16KB contiguous"};
-  for (int mode = 0; mode < 4; ++mode) {
+  const char* names[5] = {"tma2d 32x2KB", "bulk 32x2KB", "bulk 8x8KB", "tma2d 4x16KB contiguous", "bulk 16x4KB"};
+  for (int mode = 0; mode < 5; ++mode) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
