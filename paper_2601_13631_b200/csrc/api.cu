@@ -225,6 +225,7 @@ ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int
   if (ctx->quota <= 0 || layer >= ctx->L) return CKV_OK;
   CK(cudaEventRecord(ctx->ev_ids, st));
   CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ids, 0));
+  pdl_mark_event_wait(ctx->side);
   PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)(layer * 2 + 1) * 4, ctx->stats,
              nullptr, ctx->epoch_dev};
   LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 1, ctx->quota, ctx->epoch, ctx->rec_bytes, nullptr,
@@ -242,7 +243,10 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
                       const void* ks, const void* vs, int ns, int include_suffix, void* out, float* o_f32,
                       float* lse_nat, cudaStream_t st) {
   const bool pf = ctx->pf_issued[layer] == ctx->epoch;
-  if (pf) CK(cudaStreamWaitEvent(st, ctx->ev_pplan[layer], 0));
+  if (pf) {
+    CK(cudaStreamWaitEvent(st, ctx->ev_pplan[layer], 0));
+    pdl_mark_event_wait(st);
+  }
   PlanOut po{ctx->gl_main, ctx->nload_main, ctx->kept_slots, nullptr, ctx->counts + (size_t)(layer * 2) * 4,
              ctx->stats, ctx->A, ctx->epoch_dev};
   PROF_BEGIN(3);
@@ -253,7 +257,10 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
   LK(launch_gather(ctx->gl_main, ctx->nload_main, host_layer_dev(ctx, layer), pool_layer(ctx, layer), ctx->rec_bytes,
                    st));
   PROF_END(4);
-  if (pf) CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
+  if (pf) {
+    CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
+    pdl_mark_event_wait(st);
+  }
   LayerGeom g = geom(ctx, ns);
   int nsplit = attn_nsplit(ctx, ns, ctx->k);
   PROF_BEGIN(5);
@@ -582,7 +589,10 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
       if ((s = issue_prefetch(ctx, lp, ids, nids, st)) != CKV_OK) return s;
     // subperiod gate: attention of the first layer waits for sp layers' chunks
     for (int lp = layer + 1; lp < layer + ctx->subperiod && lp < pend; ++lp)
-      if (ctx->pf_issued[lp] == ctx->epoch) CK(cudaStreamWaitEvent(st, ctx->ev_pf[lp], 0));
+      if (ctx->pf_issued[lp] == ctx->epoch) {
+        CK(cudaStreamWaitEvent(st, ctx->ev_pf[lp], 0));
+        pdl_mark_event_wait(st);
+      }
   }
   if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, st)) != CKV_OK)
     return s;
@@ -807,3 +817,49 @@ void ckv_destroy(ckv_ctx* ctx) {
 }
 
 }  // extern "C"
+
+namespace ckv {
+static cudaStream_t g_pdl_marked[8];
+static int g_pdl_n_marked = 0;
+void pdl_mark_event_wait(cudaStream_t st) {
+  for (int i = 0; i < g_pdl_n_marked; ++i)
+    if (g_pdl_marked[i] == st) return;
+  if (g_pdl_n_marked < 8) g_pdl_marked[g_pdl_n_marked++] = st;
+}
+bool pdl_take_event_wait(cudaStream_t st) {
+  for (int i = 0; i < g_pdl_n_marked; ++i)
+    if (g_pdl_marked[i] == st) {
+      g_pdl_marked[i] = g_pdl_marked[--g_pdl_n_marked];
+      return true;
+    }
+  return false;
+}
+bool pdl_skip_kernel(const void* kern) {
+  static const bool dbg = getenv("CKV_PDL_DEBUG") != nullptr;
+  if (dbg) fprintf(stderr, "[pdl] launch %p\n", kern);
+  static const char* skip = getenv("CKV_PDL_SKIP");
+  if (!skip || !*skip) return false;
+  const char* name = nullptr;
+  const cudaError_t e = cudaFuncGetName(&name, kern);
+  if (getenv("CKV_PDL_DEBUG")) fprintf(stderr, "[pdl] %s -> %s\n", cudaGetErrorString(e), name ? name : "(null)");
+  if (e != cudaSuccess || !name) return false;
+  std::string list(skip);
+  size_t pos = 0;
+  while (pos <= list.size()) {
+    size_t e = list.find(',', pos);
+    if (e == std::string::npos) e = list.size();
+    const std::string tok = list.substr(pos, e - pos);
+    if (!tok.empty() && strstr(name, tok.c_str())) return true;
+    pos = e + 1;
+  }
+  return false;
+}
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CKV_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+}  // namespace ckv

@@ -7,6 +7,44 @@
 
 namespace ckv {
 
+// ---- programmatic dependent launch (PDL) ----
+// Every kernel of libckv is launched with programmatic stream serialization (launch_kernel), so
+// it may be scheduled while its stream predecessor is still running.  Each kernel calls
+// pdl_wait() before its first access to memory another kernel of the stream writes or reads
+// (griddepcontrol.wait: the predecessor grid has completed and its writes are visible), and
+// pdl_trigger() only AFTER its own pdl_wait(): its successor is then scheduled no earlier than
+// the completion of its predecessor, so at most two kernels of a stream overlap and every
+// kernel older than the predecessor has completed.  (Triggering before the wait let three-
+// kernel chains -- plan, gather, attention -- read stale data: measured on B200.)  Only
+// constant inputs (q, k_suf, v_suf, the probe keys), TMEM / shared-memory setup and tensor-map
+// prefetches may precede pdl_wait().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();  // CKV_PDL=0 disables the launch attribute (A/B measurements)
+// A kernel that follows a cross-stream event wait is launched without the attribute (the
+// programmatic relaxation must not weaken the event dependency); api.cu marks such streams.
+void pdl_mark_event_wait(cudaStream_t st);
+bool pdl_take_event_wait(cudaStream_t st);  // true (and cleared) if st was marked
+bool pdl_skip_kernel(const void* kern);     // debug: CKV_PDL_SKIP=name,name,... (substring match)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                 Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  const bool after_wait = pdl_take_event_wait(st);
+  attr[0].val.programmaticStreamSerializationAllowed =
+      (pdl_enabled() && !after_wait && !pdl_skip_kernel(reinterpret_cast<const void*>(kern))) ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+}
+
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 

@@ -23,6 +23,8 @@ __global__ void __launch_bounds__(NT) attn_simt_kernel(LayerGeom g, const T* __r
                                                        const int32_t* __restrict__ n_kept_dev, int k_cap,
                                                        int include_suffix, int nsplit, float* __restrict__ o_part,
                                                        float* __restrict__ lse_part) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   const int d = g.d;
   float* Qt = sm;               // [d][RB]
@@ -192,6 +194,8 @@ template <typename T>
 __global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_part, const float* __restrict__ lse_part,
                                     int nsplit, T* __restrict__ out, float* __restrict__ o_f32,
                                     float* __restrict__ lse_nat) {
+  pdl_wait();
+  pdl_trigger();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // kvh * R + rho
   const int lane = threadIdx.x & 31;
   const int64_t nrow = (int64_t)g.Hkv * g.R;
@@ -246,6 +250,8 @@ __global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_par
 
 __global__ void lse_merge_prepare_kernel(int rows, int d, const float* __restrict__ o, const float* __restrict__ lse,
                                          const float* __restrict__ lse_max, float* __restrict__ buf) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x;
   if (i >= rows) return;
   const float l = lse[i], M = lse_max[i];
@@ -256,6 +262,8 @@ __global__ void lse_merge_prepare_kernel(int rows, int d, const float* __restric
 
 template <typename T>
 __global__ void lse_merge_finish_kernel(int rows, int d, const float* __restrict__ buf, T* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x;
   if (i >= rows) return;
   const float den = buf[(int64_t)i * (d + 1) + d];
@@ -281,27 +289,27 @@ cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, con
     attr_done = 1;
   }
   dim3 grid((g.R + RB - 1) / RB, nsplit, g.Hkv);
-  kfn<<<grid, NT, smem, st>>>(g, q, k_suf, v_suf, pool_layer, rec_elems, kept_slots, kept_ids, n_kept_dev, k_cap,
-                              include_suffix, nsplit, o_part, lse_part);
+  if (cudaError_t e_ = launch_kernel(kfn, grid, NT, smem, st, g, q, k_suf, v_suf, pool_layer, rec_elems, kept_slots, kept_ids, n_kept_dev, k_cap,
+                              include_suffix, nsplit, o_part, lse_part)) return e_;
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit, T* out,
                                 float* o_f32, float* lse_nat, cudaStream_t st) {
-  attn_combine_kernel<T><<<(g.Hkv * g.R + 7) / 8, 256, 0, st>>>(g, o_part, lse_part, nsplit, out, o_f32, lse_nat);
+  if (cudaError_t e_ = launch_kernel(attn_combine_kernel<T>, (g.Hkv * g.R + 7) / 8, 256, 0, st, g, o_part, lse_part, nsplit, out, o_f32, lse_nat)) return e_;
   return cudaGetLastError();
 }
 
 cudaError_t launch_lse_merge_prepare(int rows, int d, const float* o, const float* lse, const float* lse_max,
                                      float* buf, cudaStream_t st) {
-  lse_merge_prepare_kernel<<<rows, 128, 0, st>>>(rows, d, o, lse, lse_max, buf);
+  if (cudaError_t e_ = launch_kernel(lse_merge_prepare_kernel, rows, 128, 0, st, rows, d, o, lse, lse_max, buf)) return e_;
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_lse_merge_finish(int rows, int d, const float* buf, T* out, cudaStream_t st) {
-  lse_merge_finish_kernel<T><<<rows, 128, 0, st>>>(rows, d, buf, out);
+  if (cudaError_t e_ = launch_kernel(lse_merge_finish_kernel<T>, rows, 128, 0, st, rows, d, buf, out)) return e_;
   return cudaGetLastError();
 }
 

@@ -101,6 +101,8 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, const char
                                                          const __nv_bfloat16* __restrict__ k_suf,
                                                          const __nv_bfloat16* __restrict__ v_suf, int include_suffix,
                                                          int NTp_cap, int T_cap, char* __restrict__ dense) {
+  pdl_wait();
+  pdl_trigger();
   const int n_kept = *n_kept_dev;
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -196,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   if (warp == 0) {
     // ------------------------------------------------------------ bulk-copy producer
     if (lane == 0) {
+      pdl_wait();
       const int n_kept = *p.n_kept_dev;
       int kvcount = 0, icount = 0;
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
@@ -217,6 +220,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
+      pdl_wait();
+      pdl_trigger();  // after this CTA's own dependency is resolved (see common.cuh)
       const int n_kept = *p.n_kept_dev;
       int n_valid_prefix = 0;  // keys of the kept prefix (the last kept chunk may be partial)
       if (n_kept > 0)
@@ -292,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           for (int i = 0; i < 16; ++i) qv[i] = 0u;
         }
         if (n_kept < 0) {  // first item: issued while the Q loads are in flight
+          pdl_wait();
           n_kept = *p.n_kept_dev;
           if (n_kept > 0)
             n_valid_prefix = (n_kept - 1) * p.g.c + min(p.g.c, p.g.n_loc - p.kept_ids[n_kept - 1] * p.g.c);
@@ -487,9 +493,9 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   const int64_t rec_bytes = (int64_t)2 * g.Hkv * g.c * D * 2;
   const int64_t n_warps = (int64_t)g.Hkv * k_cap * 4 + (include_suffix ? (int64_t)g.Hkv * g.ns * 2 : 0);
   const int cblocks = (int)std::min<int64_t>((n_warps + 7) / 8, 8 * sm_count());
-  compact_kv_kernel<<<cblocks, 256, 0, st>>>(g, reinterpret_cast<const char*>(pool_layer), rec_bytes, kept_slots,
+  if (cudaError_t e_ = launch_kernel(compact_kv_kernel, cblocks, 256, 0, st, g, reinterpret_cast<const char*>(pool_layer), rec_bytes, kept_slots,
                                              n_kept_dev, k_cap, k_suf, v_suf, include_suffix, p.NTp_cap, p.T_cap,
-                                             static_cast<char*>(dense_ws));
+                                             static_cast<char*>(dense_ws))) return e_;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static bool attr = false;
@@ -511,7 +517,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   CUtensorMap tmO;
   if (!make_tmap_f32_3d_store(&tmO, o_part, D, (uint64_t)g.R, (uint64_t)nsplit * g.Hkv, BM))
     return cudaErrorInvalidValue;
-  attn_tc_kernel<<<grid, kThreads, kSmem, st>>>(tmO, p);
+  if (cudaError_t e_ = launch_kernel(attn_tc_kernel, grid, kThreads, kSmem, st, tmO, p)) return e_;
   if (trace_buf) {  // debug only: synchronous dump of CTA 0's event times (us since kernel start)
     unsigned long long h[7 * 32];
     cudaStreamSynchronize(st);

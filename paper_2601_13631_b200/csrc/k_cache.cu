@@ -32,6 +32,8 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
                                                         const int32_t* __restrict__ n_ids_dev, int n_ids_host,
                                                         int prefetch, int quota, int epoch, int64_t rec_bytes,
                                                         int32_t* __restrict__ scratch, PlanOut out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ SelectSmem ss;
   __shared__ int s_hits, s_spec_used;
   const int n_ids = n_ids_dev ? *n_ids_dev : n_ids_host;
@@ -170,6 +172,8 @@ __global__ void __launch_bounds__(GATHER_THREADS) gather_kernel(const int32_t* _
                                                                 const int32_t* __restrict__ n_load,
                                                                 const char* __restrict__ host_layer,
                                                                 char* __restrict__ pool_layer, int64_t rec_bytes) {
+  pdl_wait();
+  pdl_trigger();
   const int n = *n_load;
   if (n == 0) return;
   const int nseg = (int)((rec_bytes + GATHER_SEG - 1) / GATHER_SEG);
@@ -200,6 +204,8 @@ __global__ void __launch_bounds__(GATHER_THREADS) gather_kernel(const int32_t* _
 
 __global__ void cache_update_kernel(CacheLayer cl, const int32_t* __restrict__ ids, const int32_t* n_ids_dev,
                                     const float* __restrict__ A) {
+  pdl_wait();
+  pdl_trigger();
   const int n = *n_ids_dev;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int j = ids[t];
@@ -211,6 +217,8 @@ __global__ void cache_update_kernel(CacheLayer cl, const int32_t* __restrict__ i
 template <typename T>
 __global__ void pack_probe_kernel(const T* __restrict__ k, int64_t t0, int n_loc, int n_pad, int Hkv, int d,
                                   T* __restrict__ probe) {
+  pdl_wait();
+  pdl_trigger();
   // probe[kvh][i][x] = k[t0 + i][kvh][x]
   const int64_t total = (int64_t)Hkv * n_loc * d;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -224,6 +232,8 @@ __global__ void pack_probe_kernel(const T* __restrict__ k, int64_t t0, int n_loc
 template <typename T>
 __global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t t0, int n_loc,
                                     int m_loc, int c, int Hkv, int d, int swz, T* __restrict__ rec) {
+  pdl_wait();
+  pdl_trigger();
   // one record per chunk j (layout: rec_elem), zero padding past n_loc
   const int64_t per = (int64_t)2 * Hkv * c * d;
   const int64_t total = (int64_t)m_loc * per;
@@ -241,45 +251,47 @@ __global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict
   }
 }
 
-__global__ void epoch_inc_kernel(int32_t* e) { *e += 1; }
+__global__ void epoch_inc_kernel(int32_t* e) {
+  pdl_wait();
+  pdl_trigger(); *e += 1; }
 
 }  // namespace
 
 cudaError_t launch_epoch_inc(int32_t* epoch_dev, cudaStream_t st) {
-  epoch_inc_kernel<<<1, 1, 0, st>>>(epoch_dev);
+  if (cudaError_t e_ = launch_kernel(epoch_inc_kernel, 1, 1, 0, st, epoch_dev)) return e_;
   return cudaGetLastError();
 }
 
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t*,
                               int32_t* scratch32, PlanOut out, cudaStream_t st) {
-  cache_plan_kernel<<<1, NT, 0, st>>>(cl, ids, n_ids_dev, n_ids_host, prefetch, quota, epoch, rec_bytes, scratch32,
-                                      out);
+  if (cudaError_t e_ = launch_kernel(cache_plan_kernel, 1, NT, 0, st, cl, ids, n_ids_dev, n_ids_host, prefetch, quota, epoch, rec_bytes, scratch32,
+                                      out)) return e_;
   return cudaGetLastError();
 }
 
 cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
                           char* pool_layer, int64_t rec_bytes, cudaStream_t st) {
-  gather_kernel<<<GATHER_BLOCKS, GATHER_THREADS, 0, st>>>(gather_list, n_load, host_layer_dev, pool_layer, rec_bytes);
+  if (cudaError_t e_ = launch_kernel(gather_kernel, GATHER_BLOCKS, GATHER_THREADS, 0, st, gather_list, n_load, host_layer_dev, pool_layer, rec_bytes)) return e_;
   return cudaGetLastError();
 }
 
 cudaError_t launch_cache_update(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, const float* A,
                                 cudaStream_t st) {
-  cache_update_kernel<<<8, 256, 0, st>>>(cl, ids, n_ids_dev, A);
+  if (cudaError_t e_ = launch_kernel(cache_update_kernel, 8, 256, 0, st, cl, ids, n_ids_dev, A)) return e_;
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t launch_pack_probe(const T* k, int64_t t0, int n_loc, int n_pad, int Hkv, int d, T* probe_layer,
                               cudaStream_t st) {
-  pack_probe_kernel<T><<<1184, 256, 0, st>>>(k, t0, n_loc, n_pad, Hkv, d, probe_layer);
+  if (cudaError_t e_ = launch_kernel(pack_probe_kernel<T>, 1184, 256, 0, st, k, t0, n_loc, n_pad, Hkv, d, probe_layer)) return e_;
   return cudaGetLastError();
 }
 template <typename T>
 cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int n_loc, int m_loc, int c, int Hkv, int d,
                                 int swz, T* staging, cudaStream_t st) {
-  pack_records_kernel<T><<<1184, 256, 0, st>>>(k, v, t0, n_loc, m_loc, c, Hkv, d, swz, staging);
+  if (cudaError_t e_ = launch_kernel(pack_records_kernel<T>, 1184, 256, 0, st, k, v, t0, n_loc, m_loc, c, Hkv, d, swz, staging)) return e_;
   return cudaGetLastError();
 }
 template cudaError_t launch_pack_probe<float>(const float*, int64_t, int, int, int, int, float*, cudaStream_t);

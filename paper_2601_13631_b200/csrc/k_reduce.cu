@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(1024) row_lse_kernel(LayerGeom g, const float*
                                                        const T* __restrict__ q, const T* __restrict__ ks, int fullrow,
                                                        const float* __restrict__ lam_all, int W,
                                                        float* __restrict__ Lam2, float* __restrict__ lam_local_out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sM[kSplitWarps][kRowsPerBlock + 1], sS[kSplitWarps][kRowsPerBlock + 1];
   const int nrows = g.Hkv * g.R;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -103,6 +105,8 @@ __global__ void __launch_bounds__(1024) row_lse_kernel(LayerGeom g, const float*
 // partial Apart[kvh][j]; the top-k kernel adds the Hkv partials in a fixed order.
 __global__ void chunk_sum_kernel(LayerGeom g, const float* __restrict__ lam2, const float* __restrict__ Lam2,
                                  float* __restrict__ Apart) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= g.m_loc * g.Hkv) return;
@@ -136,8 +140,8 @@ cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit,
                            int fullrow, const float* lam_all, int W, float* Lam2, float* lam_local_out,
                            cudaStream_t st) {
   const int n = g.Hkv * g.R;
-  row_lse_kernel<T><<<(n + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kSplitWarps, 0, st>>>(g, lampart, nsplit, q, k_suf, fullrow,
-                                                                             lam_all, W, Lam2, lam_local_out);
+  if (cudaError_t e_ = launch_kernel(row_lse_kernel<T>, (n + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kSplitWarps, 0, st, g, lampart, nsplit, q, k_suf, fullrow,
+                                                                             lam_all, W, Lam2, lam_local_out)) return e_;
   return cudaGetLastError();
 }
 template cudaError_t launch_row_lse<float>(const LayerGeom&, const float*, int, const float*, const float*, int,
@@ -150,7 +154,7 @@ cudaError_t launch_chunk_sum(const LayerGeom& g, const float* lam2, const float*
                              cudaStream_t st) {
   const int threads = 256, warps_per_block = threads / 32;
   const int blocks = (g.m_loc * g.Hkv + warps_per_block - 1) / warps_per_block;
-  chunk_sum_kernel<<<blocks, threads, 0, st>>>(g, lam2, Lam2, Apart);
+  if (cudaError_t e_ = launch_kernel(chunk_sum_kernel, blocks, threads, 0, st, g, lam2, Lam2, Apart)) return e_;
   return cudaGetLastError();
 }
 

@@ -19,6 +19,8 @@ template <typename T>
 __global__ void __launch_bounds__(NT) score_simt_kernel(LayerGeom g, const T* __restrict__ q,
                                                         const T* __restrict__ probe, float* __restrict__ lam2,
                                                         float* __restrict__ lampart, int nsplit) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ float sm[];
   const int d = g.d;
   float* Qt = sm;                 // [d][RB]
@@ -124,7 +126,7 @@ cudaError_t launch_score_simt(const LayerGeom& g, const T* q, const T* probe_lay
     attr_done = 1;
   }
   dim3 grid((g.R + RB - 1) / RB, nsplit, g.Hkv);
-  kfn<<<grid, NT, smem, st>>>(g, q, probe_layer, lam2, lampart, nsplit);
+  if (cudaError_t e_ = launch_kernel(kfn, grid, NT, smem, st, g, q, probe_layer, lam2, lampart, nsplit)) return e_;
   return cudaGetLastError();
 }
 

@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int qs = qcount % kQStages;
         ptx::mbar_wait_sleep(&q_empty[qs], ((qcount / kQStages) & 1) ^ 1);
+        if (qcount == 0) pdl_wait();  // Q is the previous kernel's output (the probe keys are not)
         if constexpr (NP >= 12) {  // tuning: no Q traffic
           ptx::mbar_arrive(&q_full[qs]);
         } else {
@@ -257,6 +258,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
+    pdl_wait();
+    pdl_trigger();  // after this CTA's own dependency is resolved (see common.cuh)
     const int e = warp - 2;
     const int quad = warp & 3;
     const int half = e >> 2;  // column quarter
@@ -321,6 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // GQA row packing: qpack[kvh][rho][x] = q[r][kvh*G + g][x], rho = g*ns + r, zero rows past R.
 __global__ void pack_q_kernel(LayerGeom g, int R_pad, const __nv_bfloat16* __restrict__ q,
                               __nv_bfloat16* __restrict__ qpack) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t total = (int64_t)g.Hkv * R_pad * (D / 8);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int x8 = (int)(i % (D / 8));
@@ -354,7 +359,7 @@ cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPa
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  score_tc_kernel<C, NP><<<grid, kThreads, kSmem, st>>>(tmK, tmQ, p);
+  if (cudaError_t e_ = launch_kernel(score_tc_kernel<C, NP>, grid, kThreads, kSmem, st, tmK, tmQ, p)) return e_;
   return cudaGetLastError();
 }
 
@@ -416,7 +421,7 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
     p.dephase = dp;
   }
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
-  pack_q_kernel<<<256, 256, 0, st>>>(g, p.R_pad, q, qpack);
+  if (cudaError_t e_ = launch_kernel(pack_q_kernel, 256, 256, 0, st, g, p.R_pad, q, qpack)) return e_;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap tmK, tmQ;

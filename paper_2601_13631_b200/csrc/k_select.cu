@@ -17,6 +17,8 @@ __global__ void __launch_bounds__(NT) topk_scores_kernel(float* __restrict__ A, 
                                                          int nparts, int m, int k, int id_offset,
                                                          int32_t* __restrict__ ids, uint64_t* __restrict__ cand,
                                                          int n_cand_out, int32_t* __restrict__ n_out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ SelectSmem ss;
   if (Apart) {  // A_j = sum over KV heads of the chunk-sum partials, fixed order
     for (int j = threadIdx.x; j < m; j += NT) {
@@ -55,6 +57,8 @@ __global__ void __launch_bounds__(NT) topk_merge_kernel(const uint64_t* __restri
                                                         int m_glob, int j0, int j1, int32_t* __restrict__ flag,
                                                         int32_t* __restrict__ ids_glob, int32_t* __restrict__ ids_local,
                                                         int32_t* __restrict__ n_local) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ SelectSmem ss;
   for (int j = threadIdx.x; j < m_glob; j += NT) flag[j] = 0;
   auto key = [&](int i) -> uint64_t { return cand_all[i]; };
@@ -86,15 +90,15 @@ __global__ void __launch_bounds__(NT) topk_merge_kernel(const uint64_t* __restri
 
 cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, int k, int id_offset, int32_t* ids,
                                uint64_t* cand_out, int n_cand_out, int32_t* n_out, cudaStream_t st) {
-  topk_scores_kernel<<<1, NT, 0, st>>>(A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+  if (cudaError_t e_ = launch_kernel(topk_scores_kernel, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out)) return e_;
   return cudaGetLastError();
 }
 
 cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1,
                               int32_t* flag_scratch, int32_t* ids_glob, int32_t* ids_local, int32_t* n_local,
                               cudaStream_t st) {
-  topk_merge_kernel<<<1, NT, 0, st>>>(cand_all, n_cand, k, m_glob, j0, j1, flag_scratch, ids_glob, ids_local,
-                                      n_local);
+  if (cudaError_t e_ = launch_kernel(topk_merge_kernel, 1, NT, 0, st, cand_all, n_cand, k, m_glob, j0, j1, flag_scratch, ids_glob, ids_local,
+                                      n_local)) return e_;
   return cudaGetLastError();
 }
 
