@@ -265,6 +265,11 @@ def run_ckv(args, rank, world):
     ms_step = ms / args.steps
     bpl = bytes_per_layer(cfg, k)
     value = bpl * L / (ms_step * 1e-3) / 1e9
+    if args.quick:  # tuning runs: the warm graph-replayed step only
+        if rank == 0:
+            print(json.dumps({"us_per_layer": ms_step * 1e3 / L, "value": value, "eager_us_per_layer":
+                              ms_eager * 1e3 / L, "clocks": clk.summary()}))
+        return
 
     # stage profile pass (eager; CUDA events on the launching stream, inside the library)
     ctx.profile(True)
@@ -427,6 +432,7 @@ def main():
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
+    ap.add_argument("--quick", action="store_true", help="tuning: print only the warm graph-step time")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--local-gpu", type=int, default=None, help="pin every rank to this GPU (functional runs)")
     args = ap.parse_args()

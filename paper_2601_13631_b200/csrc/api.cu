@@ -16,6 +16,10 @@
 #include "../../include/ckv.h"
 #include "common.cuh"
 
+namespace ckv {
+void timeline_dump();  // debug (CKV_TIMELINE=1), defined at the end of this file
+}
+
 using namespace ckv;
 
 struct ckv_ctx {
@@ -574,6 +578,14 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
   int32_t* ids = ctx->ids_buf[pid & 1];  // double-buffered by period: side-stream plans may still read it
   int32_t* nids = ctx->n_ids_buf[pid & 1];
   if (first) {  // identification: A1 -> A2 -> A3
+    // The persistent score kernel needs every SM: side-stream prefetch work for this layer must
+    // not still be resident when it starts (one late CTA delays the whole statically partitioned
+    // launch), so the prefetch is joined here rather than only before the attention.
+    static const bool side_sync = !(getenv("CKV_SIDE_SYNC") && getenv("CKV_SIDE_SYNC")[0] == '0');
+    if (side_sync && ctx->pf_issued[layer] == ctx->epoch) {
+      CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
+      pdl_mark_event_wait(st);
+    }
     int nsplit = 0;
     if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
     LayerGeom g = geom(ctx, n_suffix);
@@ -811,6 +823,7 @@ ckv_status ckv_test_cache_step(ckv_ctx* ctx, int32_t layer, const int32_t* ids, 
 const char* ckv_last_error(const ckv_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 void ckv_destroy(ckv_ctx* ctx) {
+  ckv::timeline_dump();
   if (!ctx) return;
   free_all(ctx);
   delete ctx;
@@ -834,16 +847,11 @@ bool pdl_take_event_wait(cudaStream_t st) {
     }
   return false;
 }
-bool pdl_skip_kernel(const void* kern) {
-  static const bool dbg = getenv("CKV_PDL_DEBUG") != nullptr;
-  if (dbg) fprintf(stderr, "[pdl] launch %p\n", kern);
-  static const char* skip = getenv("CKV_PDL_SKIP");
-  if (!skip || !*skip) return false;
+static bool name_listed(const void* kern, const char* list_env) {
+  if (!list_env || !*list_env) return false;
   const char* name = nullptr;
-  const cudaError_t e = cudaFuncGetName(&name, kern);
-  if (getenv("CKV_PDL_DEBUG")) fprintf(stderr, "[pdl] %s -> %s\n", cudaGetErrorString(e), name ? name : "(null)");
-  if (e != cudaSuccess || !name) return false;
-  std::string list(skip);
+  if (cudaFuncGetName(&name, kern) != cudaSuccess || !name) return false;
+  std::string list(list_env);
   size_t pos = 0;
   while (pos <= list.size()) {
     size_t e = list.find(',', pos);
@@ -853,6 +861,58 @@ bool pdl_skip_kernel(const void* kern) {
     pos = e + 1;
   }
   return false;
+}
+bool pdl_skip_kernel(const void* kern) {
+  static const char* skip = getenv("CKV_PDL_SKIP");
+  return name_listed(kern, skip);
+}
+bool knocked_out(const void* kern) {
+  static const char* ko = getenv("CKV_KNOCKOUT");
+  return name_listed(kern, ko);
+}
+// Debug timeline (CKV_TIMELINE=1): an event after every kernel launch (also inside graph capture,
+// as event-record nodes -- they break the programmatic edges, so this measures a PDL-free
+// schedule); ckv_destroy prints the last 400 entries (end time of each kernel, us, relative).
+struct TlEntry {
+  const void* kern;
+  cudaStream_t st;
+  cudaEvent_t ev;
+};
+static std::vector<TlEntry> g_tl;
+static size_t g_tl_pos = 0;
+void timeline_mark(const void* kern, cudaStream_t st) {
+  static const bool on = getenv("CKV_TIMELINE") && getenv("CKV_TIMELINE")[0] == '1';
+  if (!on) return;
+  if (g_tl.empty()) {
+    g_tl.resize(400);
+    for (auto& t : g_tl) cudaEventCreate(&t.ev);
+  }
+  TlEntry& t = g_tl[g_tl_pos++ % g_tl.size()];
+  t.kern = kern;
+  t.st = st;
+  cudaEventRecord(t.ev, st);
+}
+void timeline_dump() {
+  if (g_tl.empty() || g_tl_pos < g_tl.size()) return;
+  cudaDeviceSynchronize();
+  const size_t n = g_tl.size(), first = g_tl_pos % n;
+  float prev = 0.f;
+  for (size_t i = 0; i < n; ++i) {
+    const TlEntry& t = g_tl[(first + i) % n];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_tl[first].ev, t.ev);
+    const char* name = nullptr;
+    cudaFuncGetName(&name, t.kern);
+    std::string nm = name ? name : "?";
+    const size_t k = nm.find("kernel");
+    if (k != std::string::npos) nm = nm.substr(0, k + 6);
+    const size_t b = nm.rfind("_N_");
+    if (b != std::string::npos) nm = nm.substr(b);
+    fprintf(stderr, "[tl] %8.2f us  +%7.2f  %s %s\n", ms * 1e3, (ms - prev) * 1e3, nm.c_str(),
+            t.st == nullptr ? "" : "");
+    fprintf(stderr, "[tl-stream] %p\n", (void*)t.st);
+    prev = ms;
+  }
 }
 bool pdl_enabled() {
   static int v = -1;

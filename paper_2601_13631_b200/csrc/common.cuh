@@ -26,10 +26,13 @@ bool pdl_enabled();  // CKV_PDL=0 disables the launch attribute (A/B measurement
 void pdl_mark_event_wait(cudaStream_t st);
 bool pdl_take_event_wait(cudaStream_t st);  // true (and cleared) if st was marked
 bool pdl_skip_kernel(const void* kern);     // debug: CKV_PDL_SKIP=name,name,... (substring match)
+bool knocked_out(const void* kern);         // timing experiments only: CKV_KNOCKOUT=name,... not launched
+void timeline_mark(const void* kern, cudaStream_t st);  // debug: CKV_TIMELINE=1 event after each launch
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                                  Args&&... args) {
+  if (knocked_out(reinterpret_cast<const void*>(kern))) return cudaSuccess;  // results invalid (timing only)
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   const bool after_wait = pdl_take_event_wait(st);
@@ -42,7 +45,9 @@ inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, 
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
+  timeline_mark(reinterpret_cast<const void*>(kern), st);
+  return e;
 }
 
 constexpr float kLog2e = 1.4426950408889634f;

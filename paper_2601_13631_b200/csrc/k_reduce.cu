@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(1024) row_lse_kernel(LayerGeom g, const float*
     stride = nrows;
     nparts = W;
   }
-  // up to 16 loads in flight per thread (the whole split range of c3_7b in one round)
+  // up to 16 loads in flight per thread (the whole split range of c3_7b in one round); two-pass
+  // LSE per round (max, then independent exponentials) so no exp2 chain is serial
   float M = -INFINITY, S = 0.f;
   for (int sp0 = w; sp0 < nparts; sp0 += 16 * kSplitWarps) {
     float v[16];
@@ -72,8 +73,14 @@ __global__ void __launch_bounds__(1024) row_lse_kernel(LayerGeom g, const float*
       const int sp = sp0 + i * kSplitWarps;
       v[i] = sp < nparts ? base[(size_t)sp * stride] : -INFINITY;
     }
+    float m = v[0];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) lse2_acc(M, S, v[i]);
+    for (int i = 1; i < 16; ++i) m = fmaxf(m, v[i]);
+    if (m == -INFINITY) continue;
+    float t[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i & 3] += fast_exp2(v[i] - m);
+    lse2_merge(M, S, m, (t[0] + t[1]) + (t[2] + t[3]));
   }
   sM[w][lane] = M;
   sS[w][lane] = S;
@@ -81,8 +88,20 @@ __global__ void __launch_bounds__(1024) row_lse_kernel(LayerGeom g, const float*
   if (w != 0) return;
   const int row_idx = blockIdx.x * kRowsPerBlock + lane;
   if (row_idx >= nrows) return;
-  float Mt = -INFINITY, St = 0.f;
-  for (int i = 0; i < kSplitWarps; ++i) lse2_merge(Mt, St, sM[i][lane], sS[i][lane]);
+  // merge the 32 split-warp partials of this row: max first, then independent rescales (fixed order)
+  float Mt = -INFINITY;
+#pragma unroll 8
+  for (int i = 0; i < kSplitWarps; ++i) Mt = fmaxf(Mt, sS[i][lane] > 0.f ? sM[i][lane] : -INFINITY);
+  float St = 0.f;
+  if (Mt != -INFINITY) {
+    float t[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
+    for (int i = 0; i < kSplitWarps; ++i) {
+      const float si = sS[i][lane];
+      if (si > 0.f) t[i & 3] += si * fast_exp2(sM[i][lane] - Mt);
+    }
+    St = (t[0] + t[1]) + (t[2] + t[3]);
+  }
   if (lam_all == nullptr && lam_local_out) lam_local_out[row_idx] = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
   if (fullrow) {
     // causal suffix keys t <= r of the same KV head (Q1 FULLROW, Q9)

@@ -30,6 +30,11 @@ __global__ void __launch_bounds__(512, 1) k(int iters, float* out, long long* cy
       if (MODE == 1) v[i] = fmaf(v[i], 0.999f, -1e-7f);
       if (MODE == 2) v[i] = ex2(v[i]);         // MUFU only (value converges to a fixed point)
       if (MODE == 3) v[i] = __uint_as_float(ex2h2(__float_as_uint(v[i])));  // 2 exps per lane-op
+      if (MODE == 4 && (i & 1) == 0) {  // FFMA2: 2 fp32 FMAs per lane-op (counted as 2 ops)
+        float2 r = __ffma2_rn(make_float2(v[i], v[i + 1]), make_float2(0.999f, 0.999f), make_float2(-1e-7f, -1e-7f));
+        v[i] = r.x;
+        v[i + 1] = r.y;
+      }
     }
   }
   __syncthreads();
@@ -63,5 +68,6 @@ int main() {
   run<2>("ex2");
   run<1>("ffma");
   run<3>("ex2.f16x2 (lane-ops)");
+  run<4>("ffma2 (fp32 FMAs)");
   return 0;
 }
