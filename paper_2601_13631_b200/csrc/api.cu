@@ -194,7 +194,7 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
                         static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)), ctx->lam2, ctx->lampart, nsplit,
                         ctx->tmap_cache, st);
     if (e == cudaSuccess) {
-      ctx->launches += 1;  // + the Q pack kernel
+      ctx->launches += score_tc_packs_q(g);  // + the Q pack kernel
     }
   }
   if (e == cudaErrorNotSupported) {

@@ -105,6 +105,7 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
                             float* lam2, float* lampart, int nsplit, void* qpack_ws, cudaStream_t st);
 int score_tc_nsplit(const LayerGeom& g);   // 0 if the shape is outside the tcgen05 kernel
 size_t score_tc_qpack_elems(int Hkv, int R_max);
+int score_tc_packs_q(const LayerGeom& g);  // 1 if the launch includes the Q pack kernel (n_s % 128 != 0)
 // A2: Lambda2[kvh][R] = LSE2 over splits (+ causal suffix if fullrow) ; also writes row LSE for shards
 template <typename T>
 cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit, const T* q, const T* k_suf,

@@ -41,6 +41,7 @@ struct TcParams {
   int NKT;      // key tiles per kv head
   int MT;       // row tiles per kv head
   int R_pad;
+  int q_direct;  // 1: Q tiles straight from q [ns][Hq][128] by a 3-D map (n_s % 128 == 0), no pack
   int n_units;  // Hkv * NKT * MT
   float scale;  // log2(e) / sqrt(d)
   int dephase;  // tuning: start delay (cycles) of odd column-quarter warps
@@ -213,10 +214,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mbar_arrive(&q_full[qs]);
         } else {
           ptx::mbar_expect_tx(&q_full[qs], kQBytes);
-          const int yq = kvh * p.R_pad + mt * BM;
           uint8_t* dq = qbuf0 + qs * kQBytes;
-          ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
-          ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
+          if (p.q_direct) {  // a 128-row tile is 128 consecutive tokens of one query head
+            const int rho0 = mt * BM, gq = rho0 / p.g.ns, r0 = rho0 - gq * p.g.ns, head = kvh * p.g.G + gq;
+            ptx::tma_load_3d(dq, &tmQ, &q_full[qs], 0, head, r0);
+            ptx::tma_load_3d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, head, r0);
+          } else {
+            const int yq = kvh * p.R_pad + mt * BM;
+            ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
+            ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
+          }
         }
         ++qcount;
       }
@@ -397,6 +404,8 @@ int score_tc_nsplit(const LayerGeom& g) {
   return kColSplit * ((g.n_loc + BN - 1) / BN);
 }
 
+int score_tc_packs_q(const LayerGeom& g) { return (g.ns % BM) != 0; }
+
 size_t score_tc_qpack_elems(int Hkv, int R_max) { return (size_t)Hkv * ((R_max + BM - 1) / BM) * BM * D; }
 
 cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* probe_layer, float* lam2,
@@ -421,12 +430,18 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
     p.dephase = dp;
   }
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
-  if (cudaError_t e_ = launch_kernel(pack_q_kernel, 256, 256, 0, st, g, p.R_pad, q, qpack)) return e_;
+  p.q_direct = (g.ns % BM) == 0 ? 1 : 0;
+  if (!p.q_direct)
+    if (cudaError_t e_ = launch_kernel(pack_q_kernel, 256, 256, 0, st, g, p.R_pad, q, qpack)) return e_;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap tmK, tmQ;
   if (!make_tmap_bf16_2d(&tmK, probe_layer, D, (uint64_t)g.Hkv * g.n_pad, BN)) return cudaErrorInvalidValue;
-  if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) return cudaErrorInvalidValue;
+  if (p.q_direct) {
+    if (!make_tmap_bf16_3d(&tmQ, q, D, g.Hq, g.ns, BM)) return cudaErrorInvalidValue;
+  } else if (!make_tmap_bf16_2d(&tmQ, qpack, D, (uint64_t)g.Hkv * p.R_pad, BM)) {
+    return cudaErrorInvalidValue;
+  }
   const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
   switch (g.c) {
     case 1: return launch_c<1>(tmK, tmQ, p, grid, st);
