@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* kvbuf0 = smem;
-  __shared__ float red_m[NWQ * 128], red_l[NWQ * 128];  // [warp of a quadrant][128 rows]
+  __shared__ float red_m[2][NWQ * 128];  // [tile parity][warp of a quadrant][128 rows]
+  __shared__ float red_l[NWQ * 128];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kKVBytes);
   uint64_t* kv_full = bars + 0;             // [kStages]
   uint64_t* kv_empty = bars + kStages;      // [kStages]
@@ -335,15 +336,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         for (int n = CPW / 4; n >= 1; n >>= 1)
 #pragma unroll
           for (int i = 0; i < n; ++i) mx[i] = fmaxf(mx[i], mx[i + n]);
-        red_m[h * 128 + rit] = mx[0];
+        // red_m is double-buffered by tile parity: a warp can only overwrite a buffer two tiles
+        // later, after the next barrier, which every reader of this tile's values has passed
+        float* rm = red_m[j & 1];
+        rm[h * 128 + rit] = mx[0];
         // after this barrier every warp of the quadrant holds its S columns in registers, so
         // P may be written over the S buffer
         ptx::named_bar_sync(bar_id, 32 * NWQ);
-        float tmax = red_m[rit];
+        float tmax = rm[rit];
 #pragma unroll
-        for (int w = 1; w < NWQ; ++w) tmax = fmaxf(tmax, red_m[w * 128 + rit]);
+        for (int w = 1; w < NWQ; ++w) tmax = fmaxf(tmax, rm[w * 128 + rit]);
         tmax *= sc;
-        ptx::named_bar_sync(bar_id, 32 * NWQ);  // red_m reusable
         const float m_new = fmaxf(m_ref, tmax);
         const bool resc = (j > 0) && (m_ref != -INFINITY) && (m_new > m_ref + kRescaleThresh);
         const float f = resc ? fast_exp2(m_ref - m_new) : 1.f;
@@ -353,8 +356,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         uint32_t pk[CPW / 2];
 #pragma unroll
         for (int i = 0; i < CPW / 2; ++i) {
-          const float p0 = fast_exp2(fmaf(x[2 * i], sc, -msub));
-          const float p1 = fast_exp2(fmaf(x[2 * i + 1], sc, -msub));
+          // 1 pair in 8 on the FMA pipe (polynomial exp2), the rest on MUFU
+          const float a0 = fmaf(x[2 * i], sc, -msub), a1 = fmaf(x[2 * i + 1], sc, -msub);
+          const float p0 = (i & 7) == 0 ? exp2_poly(a0) : fast_exp2(a0);
+          const float p1 = (i & 7) == 0 ? exp2_poly(a1) : fast_exp2(a1);
           ls[i & 3] += p0 + p1;
           __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
           pk[i] = *reinterpret_cast<uint32_t*>(&b2);

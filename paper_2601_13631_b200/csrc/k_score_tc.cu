@@ -57,24 +57,6 @@ __device__ __forceinline__ void tree_sum(float* a) {
   }
 }
 
-// 2^x on the FMA/ALU pipes (x <= 0): round-to-nearest split x = i + f with the 1.5*2^23 trick,
-// degree-5 Taylor of 2^f on [-0.5, 0.5] (rel. error < 3e-6), exponent added in the integer
-// domain.  Used for part of the exponentials so the MUFU (ex2) pipe is not the only bound.
-__device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -125.f);
-  const float r = x + 12582912.f;
-  const float f = x - (r - 12582912.f);
-  float p = fmaf(f, 1.3333558e-3f, 9.6181291e-3f);
-  p = fmaf(p, f, 5.5504109e-2f);
-  p = fmaf(p, f, 2.4022651e-1f);
-  p = fmaf(p, f, 6.9314718e-1f);
-  p = fmaf(p, f, 1.0f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(r) - 0x4B400000) << 23));
-}
-
-// One warp's 64 key columns of one row tile (this thread: one suffix row): a single max over
-// the 64 scores is the reference for every exponential (no running rescale), so the MUFU pipe
-// sees one ex2 per score plus one lg2 per chunk piece and one for the quarter normaliser.
 template <int C, int NP, bool MASK>
 __device__ __forceinline__ void epilogue_unit(const TcParams& p, float (&v)[64], int key0, float* lamrow,
                                               float* lampart_out, bool row_ok) {
