@@ -11,6 +11,15 @@
 
 using namespace ckv;
 
+template <int N, int G>
+__device__ __forceinline__ void tsum(float* a) {
+  if constexpr (G > 1) {
+    tsum<N, G / 2>(a);
+#pragma unroll
+    for (int i = 0; i < N / G; ++i) a[i] = a[2 * i] + a[2 * i + 1];
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(512, 1) tmem_kernel(int iters, float* out, long long* cyc) {
   __shared__ uint32_t slot;
@@ -27,6 +36,29 @@ __global__ void __launch_bounds__(512, 1) tmem_kernel(int iters, float* out, lon
   for (int i = 0; i < 32; ++i) v[i] = -0.01f * i;
   __syncthreads();
   const long long t0 = clock64();
+  if (MODE >= 4) {  // score epilogue: 64 columns, one max, C = 16 chunk sums, lg2 per chunk (+ stores)
+    for (int it = 0; it < iters; ++it) {
+      float w[64];
+      ptx::tmem_ld32p(tmem + (it & 1) * 256 + part * 64 + ((uint32_t)(quad * 32) << 16), w);
+      ptx::tmem_ld32p(tmem + (it & 1) * 256 + part * 64 + 32 + ((uint32_t)(quad * 32) << 16), w + 32);
+      float m = w[0];
+#pragma unroll
+      for (int i = 1; i < 64; ++i) m = fmaxf(m, w[i]);
+      const float ms = m * 0.127f;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) w[i] = fast_exp2(fmaf(w[i], 0.127f, -ms) - 1.f);
+      tsum<64, 16>(w);
+      float tot = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float l = ms + fast_log2(w[i]);
+        tot += w[i];
+        if (MODE == 5) out[(size_t)148 * 512 * (1 + (it & 63) * 4 + i) + blockIdx.x * 512 + threadIdx.x] = l;
+        else acc += l;
+      }
+      acc += fast_log2(tot);
+    }
+  } else
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int g = 0; g < 2; ++g) {
@@ -61,7 +93,7 @@ template <int MODE>
 void run(const char* name) {
   float* out;
   long long* cyc;
-  cudaMalloc(&out, 148 * 512 * 4);
+  cudaMalloc(&out, (size_t)148 * 512 * 4 * 260);
   cudaMalloc(&cyc, 148 * 8);
   const int iters = 512;
   tmem_kernel<MODE><<<148, 512>>>(iters, out, cyc);
@@ -83,5 +115,7 @@ int main() {
   run<1>("ldtm + ex2 + sum");
   run<2>("ex2 + sum (no ldtm)");
   run<3>("ldtm + max + ex2 + sum");
+  run<4>("score epilogue (64 cols, C=16, lg2), no stores");
+  run<5>("score epilogue + coalesced lam stores");
   return 0;
 }
