@@ -185,6 +185,19 @@ ckv_status ckv_lse_merge_finish(ckv_ctx* ctx, const float* merge_buf, int32_t n_
  * as in ckv_create. */
 ckv_status ckv_set_period(ckv_ctx* ctx, int32_t period, int32_t subperiod);
 
+/* Eviction score of the HBM chunk cache (A4).  CKV_CACHE_ATTN is the paper's
+ * attention-guided policy S_j = I_j * F_j (Eq. 2); CKV_CACHE_LFU
+ * (S_j = F_j) and CKV_CACHE_LRU (S_j = request index of the last selection) are the
+ * ablation baselines of PAPER.md:610-613 ("w/o AC": "LFU as the cache policy").
+ * Victims are always the lowest (S, j) residents that are not requested and not pinned. */
+typedef enum { CKV_CACHE_ATTN = 0, CKV_CACHE_LFU = 1, CKV_CACHE_LRU = 2 } ckv_cache_policy;
+
+/* Select the eviction policy.  Synchronises the device, empties every slot and zeroes
+ * the (I, F, last-use) tables of every layer, so each policy starts from the same cold
+ * state (performance only: results never depend on the cache).  Call between requests.
+ * Errors: CKV_EINVAL (unknown policy), CKV_ECUDA. */
+ckv_status ckv_set_cache_policy(ckv_ctx* ctx, int32_t policy, void* stream);
+
 /* Cache control / introspection. */
 ckv_status ckv_reset_cache(ckv_ctx* ctx, void* stream); /* empty every slot; keep (I, F) */
 ckv_status ckv_get_stats(ckv_ctx* ctx, ckv_stats* out);  /* synchronises the library's streams */

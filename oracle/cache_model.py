@@ -12,6 +12,11 @@ B200 design of SURVEY §8(a) A4/A6/A9 (per-layer slot partitions)
   low-scored ContiguousChunks", PAPER.md:452; ties by (S, l, j), SPEC.md:414);
 * after the layer: I_j += A_j, F_j += 1 for the selected ids.
 
+Ablation policies ("w/o AC: ContiguousKV using LFU as the cache
+policy"): policy="lfu" ranks residents by S_j = F_j alone,
+policy="lru" by the request index of the chunk's last selection (the `tick` passed to
+update); the victim rule (lowest (S, j), never a requested chunk) is the same.
+
 Pure integer/slot bookkeeping plus the float compare of S; the GPU planner must
 reproduce this exactly when S values are exact (integers), and the tests use such.
 """
@@ -21,15 +26,24 @@ import numpy as np
 
 
 class CacheModel:
-    def __init__(self, num_layers: int, num_chunks: int, slots_per_layer: int):
+    POLICIES = ("attn", "lfu", "lru")
+
+    def __init__(self, num_layers: int, num_chunks: int, slots_per_layer: int, policy: str = "attn"):
+        assert policy in self.POLICIES, policy
+        self.policy = policy
         self.L, self.m, self.P = num_layers, num_chunks, slots_per_layer
         self.slot_of = np.full((num_layers, num_chunks), -1, dtype=np.int64)
         self.owner = np.full((num_layers, slots_per_layer), -1, dtype=np.int64)
         self.I = np.zeros((num_layers, num_chunks))
         self.F = np.zeros((num_layers, num_chunks), dtype=np.int64)
+        self.T = np.zeros((num_layers, num_chunks), dtype=np.int64)  # last-selection tick
 
     def score(self, layer: int) -> np.ndarray:
-        """S_j = I_j x F_j  (Eq. 2)."""
+        """S_j = I_j x F_j  (Eq. 2); F_j (LFU) or the last-use tick (LRU) for the ablations."""
+        if self.policy == "lfu":
+            return self.F[layer].astype(np.float64)
+        if self.policy == "lru":
+            return self.T[layer].astype(np.float64)
         return self.I[layer] * self.F[layer]
 
     def plan(self, layer: int, ids, limit: int | None = None):
@@ -65,8 +79,9 @@ class CacheModel:
             loads.append((j, s))
         return hits, loads, victims
 
-    def update(self, layer: int, ids, A) -> None:
-        """I_j += A_j, F_j += 1 for every selected chunk."""
+    def update(self, layer: int, ids, A, tick: int = 0) -> None:
+        """I_j += A_j, F_j += 1 for every selected chunk; T_j = tick."""
         for j in ids:
             self.I[layer, int(j)] += float(A[int(j)])
             self.F[layer, int(j)] += 1
+            self.T[layer, int(j)] = tick

@@ -64,6 +64,7 @@ SIGNATURES = {
     "ckv_lse_merge_finish": (ctypes.c_int, [_P, _P, _I32, _P, _P]),
     "ckv_reset_cache": (ctypes.c_int, [_P, _P]),
     "ckv_set_period": (ctypes.c_int, [_P, _I32, _I32]),
+    "ckv_set_cache_policy": (ctypes.c_int, [_P, _I32, _P]),
     "ckv_get_stats": (ctypes.c_int, [_P, ctypes.POINTER(ckv_stats)]),
     "ckv_reset_stats": (ctypes.c_int, [_P]),
     "ckv_num_chunks": (_I32, [_P]),
@@ -201,6 +202,13 @@ class Context:
 
     def set_period(self, period, subperiod=1):
         self._check(self.lib.ckv_set_period(self.h, period, subperiod), "ckv_set_period")
+
+    CACHE_POLICIES = {"attn": 0, "lfu": 1, "lru": 2}
+
+    def set_cache_policy(self, policy, stream=None):
+        """Eviction score: "attn" (S = I*F, Eq. 2), "lfu" (S = F) or "lru"; empties the cache."""
+        pol = self.CACHE_POLICIES[policy] if isinstance(policy, str) else int(policy)
+        self._check(self.lib.ckv_set_cache_policy(self.h, pol, _stream(stream)), "ckv_set_cache_policy")
 
     def reset_cache(self, stream=None):
         self._check(self.lib.ckv_reset_cache(self.h, _stream(stream)), "ckv_reset_cache")

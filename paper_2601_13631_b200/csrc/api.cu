@@ -41,7 +41,8 @@ struct ckv_ctx {
   char* host_store = nullptr;
   char* host_store_dev = nullptr;
   char* pool = nullptr;
-  int32_t *slot_of = nullptr, *owner = nullptr, *pf_epoch = nullptr, *F = nullptr;
+  int32_t *slot_of = nullptr, *owner = nullptr, *pf_epoch = nullptr, *F = nullptr, *T = nullptr;
+  int cache_policy = 0;  // ckv_cache_policy
   float* I = nullptr;
   float *lam2 = nullptr, *lampart = nullptr, *Lam2 = nullptr, *A = nullptr, *Apart = nullptr;
   int32_t* ids_buf[2] = {nullptr, nullptr};
@@ -168,8 +169,10 @@ CacheLayer cache_layer(const ckv_ctx* ctx, int layer) {
   cl.pf_epoch = ctx->pf_epoch + (size_t)layer * ctx->P;
   cl.I = ctx->I + (size_t)layer * ctx->m_loc;
   cl.F = ctx->F + (size_t)layer * ctx->m_loc;
+  cl.T = ctx->T + (size_t)layer * ctx->m_loc;
   cl.m_loc = ctx->m_loc;
   cl.P = ctx->P;
+  cl.policy = ctx->cache_policy;
   return cl;
 }
 
@@ -316,7 +319,7 @@ void free_all(ckv_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->cfg.device);
   cudaDeviceSynchronize();
-  void* dev_ptrs[] = {ctx->probe, ctx->pool, ctx->slot_of, ctx->owner, ctx->pf_epoch, ctx->F, ctx->I, ctx->lam2,
+  void* dev_ptrs[] = {ctx->probe, ctx->pool, ctx->slot_of, ctx->owner, ctx->pf_epoch, ctx->F, ctx->T, ctx->I, ctx->lam2,
                       ctx->lampart, ctx->Lam2, ctx->A, ctx->Apart, ctx->ids_buf[0], ctx->ids_buf[1], ctx->n_ids_buf[0],
                       ctx->n_ids_buf[1], ctx->kept_slots, ctx->ids_glob, ctx->flag, ctx->scratch_main,
                       ctx->scratch_side, ctx->gl_main, ctx->gl_side, ctx->nload_main, ctx->nload_side, ctx->counts,
@@ -433,11 +436,13 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   CKC(dalloc(&ctx->owner, (size_t)ctx->L * ctx->P));
   CKC(dalloc(&ctx->pf_epoch, (size_t)ctx->L * ctx->P));
   CKC(dalloc(&ctx->F, (size_t)ctx->L * ctx->m_loc));
+  CKC(dalloc(&ctx->T, (size_t)ctx->L * ctx->m_loc));
   CKC(dalloc(&ctx->I, (size_t)ctx->L * ctx->m_loc));
   CKC(cudaMemset(ctx->slot_of, 0xFF, sizeof(int32_t) * ctx->L * ctx->m_loc));
   CKC(cudaMemset(ctx->owner, 0xFF, sizeof(int32_t) * ctx->L * ctx->P));
   CKC(cudaMemset(ctx->pf_epoch, 0xFF, sizeof(int32_t) * ctx->L * ctx->P));
   CKC(cudaMemset(ctx->F, 0, sizeof(int32_t) * ctx->L * ctx->m_loc));
+  CKC(cudaMemset(ctx->T, 0, sizeof(int32_t) * ctx->L * ctx->m_loc));
   CKC(cudaMemset(ctx->I, 0, sizeof(float) * ctx->L * ctx->m_loc));
   CKC(dalloc(&ctx->lam2, (size_t)ctx->Hkv * ctx->m_loc * R_max));
   CKC(dalloc(&ctx->lampart, (size_t)ctx->Hkv * ctx->nsplit_score_max * R_max));
@@ -549,6 +554,7 @@ ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const vo
   CK(cudaMemsetAsync(cl.pf_epoch, 0xFF, sizeof(int32_t) * ctx->P, st));
   CK(cudaMemsetAsync(cl.I, 0, sizeof(float) * ctx->m_loc, st));
   CK(cudaMemsetAsync(cl.F, 0, sizeof(int32_t) * ctx->m_loc, st));
+  CK(cudaMemsetAsync(cl.T, 0, sizeof(int32_t) * ctx->m_loc, st));
   CK(cudaStreamSynchronize(st));
   CK(cudaFree(staging));
   if (tmp) CK(cudaFree(tmp));
@@ -711,6 +717,24 @@ ckv_status ckv_set_period(ckv_ctx* ctx, int32_t period, int32_t subperiod) {
   return CKV_OK;
 }
 
+ckv_status ckv_set_cache_policy(ckv_ctx* ctx, int32_t policy, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (policy < CKV_CACHE_ATTN || policy > CKV_CACHE_LRU) return fail(ctx, CKV_EINVAL, "cache policy %d", policy);
+  CK(cudaSetDevice(ctx->cfg.device));
+  CK(cudaDeviceSynchronize());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CK(cudaMemsetAsync(ctx->slot_of, 0xFF, sizeof(int32_t) * ctx->L * ctx->m_loc, st));
+  CK(cudaMemsetAsync(ctx->owner, 0xFF, sizeof(int32_t) * ctx->L * ctx->P, st));
+  CK(cudaMemsetAsync(ctx->pf_epoch, 0xFF, sizeof(int32_t) * ctx->L * ctx->P, st));
+  CK(cudaMemsetAsync(ctx->I, 0, sizeof(float) * ctx->L * ctx->m_loc, st));
+  CK(cudaMemsetAsync(ctx->F, 0, sizeof(int32_t) * ctx->L * ctx->m_loc, st));
+  CK(cudaMemsetAsync(ctx->T, 0, sizeof(int32_t) * ctx->L * ctx->m_loc, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->cache_policy = policy;
+  return CKV_OK;
+}
+
 ckv_status ckv_reset_cache(ckv_ctx* ctx, void* stream) {
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
@@ -815,7 +839,7 @@ ckv_status ckv_test_cache_step(ckv_ctx* ctx, int32_t layer, const int32_t* ids, 
   if (A && !prefetch) {
     CK(cudaMemcpyAsync(ctx->n_ids_buf[0], &k, sizeof(int32_t), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
-    LK(launch_cache_update(cache_layer(ctx, layer), ids, ctx->n_ids_buf[0], A, st));
+    LK(launch_cache_update(cache_layer(ctx, layer), ids, ctx->n_ids_buf[0], A, ctx->epoch, st));
   }
   return CKV_OK;
 }

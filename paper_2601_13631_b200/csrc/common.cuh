@@ -146,7 +146,9 @@ struct CacheLayer {
   int32_t* pf_epoch;  // [P]
   float* I;           // [m_loc]
   int32_t* F;         // [m_loc]
+  int32_t* T;         // [m_loc] request tick of the last selection (LRU policy)
   int m_loc, P;
+  int policy;         // ckv_cache_policy: eviction score S (0: I*F, 1: F, 2: last-use tick)
 };
 struct PlanOut {
   int32_t* gather_list;  // [2 * cap]: (chunk, slot)
@@ -165,7 +167,7 @@ cudaError_t launch_epoch_inc(int32_t* epoch_dev, cudaStream_t st);
 cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
                           char* pool_layer, int64_t rec_bytes, cudaStream_t st);
 cudaError_t launch_cache_update(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev,
-                                const float* A, cudaStream_t st);
+                                const float* A, int tick, cudaStream_t st);
 // store
 template <typename T>
 cudaError_t launch_pack_probe(const T* k, int64_t t0, int n_loc, int n_pad, int Hkv, int d, T* probe_layer,

@@ -82,7 +82,8 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
       if (j < 0) return 0ull;
       if (bsearch_ids(ids, n_ids, j)) return 0ull;
       if (!prefetch && cl.pf_epoch[s] == epoch) return 0ull;
-      const float S = cl.I[j] * (float)cl.F[j];
+      // Eq. 2 by default; the ablation policies of PAPER.md:610-613
+      const float S = cl.policy == 0 ? cl.I[j] * (float)cl.F[j] : cl.policy == 1 ? (float)cl.F[j] : (float)cl.T[j];
       return ~(((uint64_t)__float_as_uint(S) << 32) | (uint64_t)(uint32_t)j);
     };
     // capacity guard (cannot trigger when P >= k + quota; kept as a loud failure, not a crash)
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
       const int j = ids[t];
       cl.I[j] += out.upd_A[j];
       cl.F[j] += 1;
+      cl.T[j] = epoch;
     }
   if (threadIdx.x == 0) {
     *out.n_load = n_miss;
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(GATHER_THREADS) gather_kernel(const int32_t* _
 }
 
 __global__ void cache_update_kernel(CacheLayer cl, const int32_t* __restrict__ ids, const int32_t* n_ids_dev,
-                                    const float* __restrict__ A) {
+                                    const float* __restrict__ A, int tick) {
   pdl_wait();
   pdl_trigger();
   const int n = *n_ids_dev;
@@ -211,6 +213,7 @@ __global__ void cache_update_kernel(CacheLayer cl, const int32_t* __restrict__ i
     const int j = ids[t];
     cl.I[j] += A[j];  // I_j = I_j + A_j
     cl.F[j] += 1;     // F_j: access count
+    cl.T[j] = tick;   // last use (LRU ablation policy)
   }
 }
 
@@ -277,8 +280,8 @@ cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, con
 }
 
 cudaError_t launch_cache_update(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, const float* A,
-                                cudaStream_t st) {
-  if (cudaError_t e_ = launch_kernel(cache_update_kernel, 8, 256, 0, st, cl, ids, n_ids_dev, A)) return e_;
+                                int tick, cudaStream_t st) {
+  if (cudaError_t e_ = launch_kernel(cache_update_kernel, 8, 256, 0, st, cl, ids, n_ids_dev, A, tick)) return e_;
   return cudaGetLastError();
 }
 

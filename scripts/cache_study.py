@@ -1,0 +1,96 @@
+"""NEXT-2 cache study: attention-guided retention vs LFU vs LRU, with and without
+speculative prefetch -- the ablation of PAPER.md:605-623 ("w/o AC": LFU as the cache policy;
+"w/o P": no prefetching) on a synthetic multi-request shared-prefix workload.
+
+Workload: the C3 shape (Qwen2.5-7B, 28 layers, 32K prefix, c = 16, n_s = 128, bf16); R = 16
+distinct requests (each its own topic mixture, synth.make_request) drawn 48 times with Zipf(1)
+popularity (seed 42); the first 16 draws warm the cache ("warm up one full pass"),
+the other 32 are measured.  Budgets 10% and 25% (the ablation's ratio); per-layer
+HBM cache of P = 2.5 k slots (prefetch quota k included when prefetch is on).  Per variant:
+hit rate, host-link MB per layer (critical-path delta and speculative), and the median eager
+us/layer over the measured requests (CUDA events on the launching stream).
+
+    python scripts/cache_study.py [--out gpurun_out/cache_study.json] [--draws 48]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2601_13631_b200 import Context, ckv_budget_chunks  # noqa: E402
+from synth import CONFIGS, make_prefix, make_request  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="gpurun_out/cache_study.json")
+    ap.add_argument("--draws", type=int, default=48)
+    ap.add_argument("--requests", type=int, default=16)
+    ap.add_argument("--budgets", default="1000,2500")
+    args = ap.parse_args()
+    base = CONFIGS["c3_7b"]
+    L, dev = base.num_layers, torch.device("cuda", 0)
+    prefix = []
+    for l in range(L):
+        kp, vp = make_prefix(base, l)
+        prefix.append((torch.from_numpy(kp).to(dev, torch.bfloat16), torch.from_numpy(vp).to(dev, torch.bfloat16)))
+    R = args.requests
+    reqs = [[[torch.from_numpy(x).to(dev, torch.bfloat16) for x in make_request(base, l, r)] for l in range(L)]
+            for r in range(R)]
+    g = np.random.default_rng(42)
+    pop = 1.0 / np.arange(1, R + 1)
+    draws = g.choice(R, size=args.draws, p=pop / pop.sum()).tolist()
+    warm = min(R, args.draws // 3)
+    outs = [torch.empty(base.suffix_len, base.num_q_heads, base.head_dim, dtype=torch.bfloat16, device=dev)
+            for _ in range(L)]
+    results = []
+    for bp in [int(b) for b in args.budgets.split(",")]:
+        k = ckv_budget_chunks(base.prefix_len, base.chunk_size, bp)
+        P = k * 5 // 2
+        ids = [torch.empty(k, dtype=torch.int32, device=dev) for _ in range(L)]
+        for prefetch in (True, False):
+            ctx = Context(L, base.num_q_heads, base.num_kv_heads, base.head_dim, base.chunk_size, base.prefix_len,
+                          base.suffix_len, dtype="bf16", budget_bp=bp, prefetch_chunks=k if prefetch else 0,
+                          cache_slots=P)
+            for l in range(L):
+                ctx.store_prefix(l, *prefix[l])
+            for policy in ("attn", "lfu", "lru"):
+                ctx.set_cache_policy(policy)
+                us = []
+                for i, r in enumerate(draws):
+                    if i == warm:
+                        torch.cuda.synchronize()
+                        ctx.reset_stats()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    for l in range(L):
+                        ctx.reprefill_layer(l, *reqs[r][l], out=outs[l], ids=ids[l])
+                    e1.record()
+                    torch.cuda.synchronize()
+                    if i >= warm:
+                        us.append(e0.elapsed_time(e1) * 1e3 / L)
+                st = ctx.get_stats()
+                nl = max(st["total_layers"], 1)
+                sel = st["total_hits"] + st["total_misses"]
+                row = {"budget_bp": bp, "k": k, "slots_per_layer": P, "prefetch": prefetch, "policy": policy,
+                       "hit_rate": st["total_hits"] / max(sel, 1),
+                       "delta_MB_per_layer": st["total_link_bytes_delta"] / nl / 1e6,
+                       "spec_MB_per_layer": st["total_link_bytes_spec"] / nl / 1e6,
+                       "spec_used_frac": st["total_spec_used"] / max(st["total_spec_loads"], 1),
+                       "us_per_layer_median": statistics.median(us), "us_per_layer_mean": statistics.mean(us)}
+                results.append(row)
+                print(json.dumps(row), flush=True)
+            ctx.close()
+    os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump({"workload": "c3_7b shape, R=%d requests, %d Zipf(1) draws (first %d warm-up), seed 42"
+                   % (R, args.draws, warm), "draws": draws, "rows": results}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()

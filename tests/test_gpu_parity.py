@@ -244,17 +244,19 @@ def test_topk_exact_with_ties(m):
 
 
 # ---------------------------------------------------------------- cache planner (A4/A9)
-def test_cache_plan_matches_model():
+@pytest.mark.parametrize("policy", ["attn", "lfu", "lru"])
+def test_cache_plan_matches_model(policy):
     m, P, k = 64, 20, 8
     ctx = Context(1, 1, 1, 64, 1, m, 1, dtype="fp32", budget_chunks=k, cache_slots=P)
     ctx.store_prefix(0, torch.zeros(m, 1, 64, device="cuda"), torch.zeros(m, 1, 64, device="cuda"))
-    model = O.CacheModel(1, m, P)
+    ctx.set_cache_policy(policy)
+    model = O.CacheModel(1, m, P, policy=policy)
     g = np.random.default_rng(7)
     for step in range(40):
         A = g.integers(0, 50, m).astype(np.float32)  # integer scores: S exact in fp32 and fp64
         ids = np.sort(g.choice(m // 2 if step % 3 else m, k, replace=False)).astype(np.int32)
         hits_m, loads_m, vict_m = model.plan(0, ids)
-        model.update(0, ids, A.astype(np.float64))
+        model.update(0, ids, A.astype(np.float64), tick=step + 1)  # the library counts one request per call
         loads, victims, counts = ctx.test_cache_step(0, torch.from_numpy(ids).cuda(), A=torch.from_numpy(A).cuda())
         counts = counts.cpu().numpy()
         loads = loads.cpu().numpy()[: 2 * counts[1]].reshape(-1, 2)

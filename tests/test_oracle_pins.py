@@ -306,6 +306,23 @@ def test_cache_heap_law_persistence_and_delta():
         assert cm.I[0, j] >= I and cm.F[0, j] >= F
 
 
+@pytest.mark.parametrize("policy,victim", [("attn", 0), ("lfu", 1), ("lru", 2)])
+def test_cache_policy_worked_example(policy, victim):
+    """Hand-worked ablation example (Eq. 2; LFU/LRU baselines PAPER.md:610-613).
+    P = 3 slots, requests (tick: ids, A on those ids): 1: {0,1,2} A=(0.1, 1, 10); 2: {2};
+    3: {0}; 4: {0}; 5: {1}; then 6: {3} needs one victim.
+      Eq. 2: I = (0.3, 2, 20), F = (3, 2, 2) -> S = (0.9, 4, 40)  -> evict chunk 0
+      LFU:   F = (3, 2, 2), tie on 1 and 2 broken by the lower id  -> evict chunk 1
+      LRU:   last use = (4, 5, 2)                                 -> evict chunk 2"""
+    cm = O.CacheModel(1, 4, 3, policy=policy)
+    A = np.array([0.1, 1.0, 10.0, 5.0])
+    for tick, ids in enumerate([[0, 1, 2], [2], [0], [0], [1]], start=1):
+        cm.plan(0, ids)
+        cm.update(0, ids, A, tick=tick)
+    hits, loads, victims = cm.plan(0, [3])
+    assert hits == [] and victims == [victim] and loads == [(3, victim)]  # slot s holds chunk s
+
+
 # ------------------------------------------------------------ synthetic inputs
 def test_synth_bf16_rounding_matches_torch():
     x = np.random.default_rng(0).standard_normal(10000).astype(np.float32) * 7
