@@ -220,6 +220,24 @@ ckv_status ckv_profile_read(ckv_ctx* ctx, double* ms, int64_t* count);
 /* Number of CUDA kernels this ctx has launched since creation (all streams). */
 int64_t ckv_kernel_launches(const ckv_ctx* ctx);
 
+/* ---- granularity accounting ----
+ * ckv_block_cover: the blocks of a coarse store of block_tokens-token blocks (e.g. the 64-token
+ *   chunks of IMPRESS / AttentionStore) that hold at least one token of the
+ *   selected chunks of this ctx (chunk j = tokens [j*c, min((j+1)*c, n)), Eq. 1 range):
+ *   read amplification RA = tokens of those blocks / tokens of the chunks (PAPER.md:209-221,
+ *   325-327; RA = 1 when block_tokens == c).
+ *   ids     device int32 [n_ids], ascending global chunk ids (n_ids may be 0)
+ *   blocks  device int32, capacity ceil(n / block_tokens): ascending block ids (written)
+ *   n_blocks device int32 [1]: number of blocks (written)
+ * ckv_load_chunks: plan (A4) and gather (A5) an explicit ascending list of local chunk ids of
+ *   `layer` into the HBM cache (demand load, no (I, F) update); the link bytes and
+ *   hits/misses accumulate into ckv_get_stats.  1 <= n_ids <= k.  Used to time whole-block
+ *   loads from a coarse store (a ctx with chunk_size = block size) on the same gather engine.
+ * Errors: CKV_EINVAL (null / range), CKV_ESTATE (layer not stored), CKV_ECUDA. */
+ckv_status ckv_block_cover(ckv_ctx* ctx, const int32_t* ids, int32_t n_ids, int32_t block_tokens,
+                           int32_t* blocks, int32_t* n_blocks, void* stream);
+ckv_status ckv_load_chunks(ckv_ctx* ctx, int32_t layer, const int32_t* ids, int32_t n_ids, void* stream);
+
 /* ---- test entry points (parity of integer work, no allocation) ----
  * ckv_test_topk: ids[k] (device int32, ascending) = top-k of A[m] (device float, A >= 0)
  *   with lower-index tie-break, by the same radix-select kernel the hot path uses.

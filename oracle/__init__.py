@@ -30,3 +30,4 @@ from .ckv_oracle import (  # noqa: F401
     coverage_ratio,
 )
 from .cache_model import CacheModel  # noqa: F401
+from .granularity import block_cover, read_amplification  # noqa: F401

@@ -65,6 +65,8 @@ SIGNATURES = {
     "ckv_reset_cache": (ctypes.c_int, [_P, _P]),
     "ckv_set_period": (ctypes.c_int, [_P, _I32, _I32]),
     "ckv_set_cache_policy": (ctypes.c_int, [_P, _I32, _P]),
+    "ckv_block_cover": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P, _P]),
+    "ckv_load_chunks": (ctypes.c_int, [_P, _I32, _P, _I32, _P]),
     "ckv_get_stats": (ctypes.c_int, [_P, ctypes.POINTER(ckv_stats)]),
     "ckv_reset_stats": (ctypes.c_int, [_P]),
     "ckv_num_chunks": (_I32, [_P]),
@@ -209,6 +211,20 @@ class Context:
         """Eviction score: "attn" (S = I*F, Eq. 2), "lfu" (S = F) or "lru"; empties the cache."""
         pol = self.CACHE_POLICIES[policy] if isinstance(policy, str) else int(policy)
         self._check(self.lib.ckv_set_cache_policy(self.h, pol, _stream(stream)), "ckv_set_cache_policy")
+
+    def block_cover(self, ids, block_tokens, stream=None):
+        """Ascending ids of the block_tokens-token blocks holding a token of the chunks `ids` (NEXT-4)."""
+        cap = -(-self.cfg.prefix_len // block_tokens)
+        blocks = torch.empty(max(cap, 1), dtype=torch.int32, device=ids.device)
+        nb = torch.zeros(1, dtype=torch.int32, device=ids.device)
+        self._check(self.lib.ckv_block_cover(self.h, _ptr(ids), ids.numel(), block_tokens, _ptr(blocks), _ptr(nb),
+                                             _stream(stream)), "ckv_block_cover")
+        return blocks, nb
+
+    def load_chunks(self, layer, ids, stream=None):
+        """Demand-load an explicit ascending list of chunk ids of `layer` into the HBM cache."""
+        self._check(self.lib.ckv_load_chunks(self.h, layer, _ptr(ids), ids.numel(), _stream(stream)),
+                    "ckv_load_chunks")
 
     def reset_cache(self, stream=None):
         self._check(self.lib.ckv_reset_cache(self.h, _stream(stream)), "ckv_reset_cache")

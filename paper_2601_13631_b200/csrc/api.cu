@@ -61,6 +61,7 @@ struct ckv_ctx {
   cudaEvent_t ev_ids = nullptr;
   std::vector<cudaEvent_t> ev_pplan, ev_pf;
   std::vector<int> pf_issued;
+  std::vector<int> pf_joined;  // epoch in which the main stream already waited for ev_pf[layer]
   std::vector<char> stored;
   int epoch = 0;
   int last_layer = -1;
@@ -248,14 +249,16 @@ ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int
 // A4 -> A5 -> A7 -> A8 -> A9 for the local selected ids.
 ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, const void* q,
                       const void* ks, const void* vs, int ns, int include_suffix, void* out, float* o_f32,
-                      float* lse_nat, cudaStream_t st) {
-  const bool pf = ctx->pf_issued[layer] == ctx->epoch;
+                      float* lse_nat, int32_t* ids_out, cudaStream_t st) {
+  // a prefetch of this layer that the stream already joined (before the score kernel) needs no
+  // further event waits: they would only cut the programmatic launch edges of plan and attention
+  const bool pf = ctx->pf_issued[layer] == ctx->epoch && ctx->pf_joined[layer] != ctx->epoch;
   if (pf) {
     CK(cudaStreamWaitEvent(st, ctx->ev_pplan[layer], 0));
     pdl_mark_event_wait(st);
   }
   PlanOut po{ctx->gl_main, ctx->nload_main, ctx->kept_slots, nullptr, ctx->counts + (size_t)(layer * 2) * 4,
-             ctx->stats, ctx->A, ctx->epoch_dev};
+             ctx->stats, ctx->A, ctx->epoch_dev, ids_out};
   PROF_BEGIN(3);
   LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 0, 0, ctx->epoch, ctx->rec_bytes, nullptr,
                        ctx->scratch_main, po, st));
@@ -456,8 +459,8 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   CKC(dalloc(&ctx->kept_slots, (size_t)ctx->k));
   CKC(dalloc(&ctx->ids_glob, (size_t)ctx->k));
   CKC(dalloc(&ctx->flag, (size_t)ctx->m));
-  CKC(dalloc(&ctx->scratch_main, (size_t)ctx->k + 2 * ctx->P));
-  CKC(dalloc(&ctx->scratch_side, (size_t)ctx->k + 2 * ctx->P));
+  CKC(dalloc(&ctx->scratch_main, (size_t)2 * ctx->k + 2 * ctx->P));
+  CKC(dalloc(&ctx->scratch_side, (size_t)2 * ctx->k + 2 * ctx->P));
   CKC(dalloc(&ctx->gl_main, (size_t)2 * ctx->k));
   CKC(dalloc(&ctx->gl_side, (size_t)2 * ctx->k));
   CKC(dalloc(&ctx->nload_main, 1));
@@ -481,6 +484,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
     CKC(cudaEventCreateWithFlags(&ctx->ev_pf[l], cudaEventDisableTiming));
   }
   ctx->pf_issued.assign(ctx->L, -1);
+  ctx->pf_joined.assign(ctx->L, -1);
   ctx->stored.assign(ctx->L, 0);
   ctx->score_kind = (ctx->dtype == CKV_BF16 && ctx->d == 128 && !(c.flags & CKV_FLAG_SIMT_SCORE)) ? 1 : 0;
   if (ctx->score_kind == 1) {
@@ -591,6 +595,7 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     if (side_sync && ctx->pf_issued[layer] == ctx->epoch) {
       CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
       pdl_mark_event_wait(st);
+      ctx->pf_joined[layer] = ctx->epoch;
     }
     int nsplit = 0;
     if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
@@ -612,9 +617,10 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
         pdl_mark_event_wait(st);
       }
   }
-  if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, st)) != CKV_OK)
+  // the demand planner also writes selected_ids (no separate copy node per layer)
+  if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, selected_ids, st)) !=
+      CKV_OK)
     return s;
-  CK(cudaMemcpyAsync(selected_ids, ids, sizeof(int32_t) * ctx->k, cudaMemcpyDeviceToDevice, st));
   if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;
 }
@@ -676,7 +682,7 @@ ckv_status ckv_shard_attend(ckv_ctx* ctx, int32_t layer, const uint64_t* cand_al
                        nids, st));
   if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st)) != CKV_OK) return s;
   if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, ctx->shard == ctx->W - 1, nullptr, o_part,
-                      lse_part, st)) != CKV_OK)
+                      lse_part, nullptr, st)) != CKV_OK)
     return s;
   CK(cudaMemcpyAsync(selected_ids, ctx->ids_glob, sizeof(int32_t) * ctx->k, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;
@@ -841,6 +847,33 @@ ckv_status ckv_test_cache_step(ckv_ctx* ctx, int32_t layer, const int32_t* ids, 
     CK(cudaStreamSynchronize(st));
     LK(launch_cache_update(cache_layer(ctx, layer), ids, ctx->n_ids_buf[0], A, ctx->epoch, st));
   }
+  return CKV_OK;
+}
+
+ckv_status ckv_block_cover(ckv_ctx* ctx, const int32_t* ids, int32_t n_ids, int32_t block_tokens, int32_t* blocks,
+                           int32_t* n_blocks, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!ids || !blocks || !n_blocks || n_ids < 0 || block_tokens < 1) return fail(ctx, CKV_EINVAL, "bad argument");
+  CK(cudaSetDevice(ctx->cfg.device));
+  LK(launch_block_cover(ids, n_ids, ctx->c, block_tokens, ctx->n, blocks, n_blocks,
+                        static_cast<cudaStream_t>(stream)));
+  return CKV_OK;
+}
+
+ckv_status ckv_load_chunks(ckv_ctx* ctx, int32_t layer, const int32_t* ids, int32_t n_ids, void* stream) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (layer < 0 || layer >= ctx->L || !ids || n_ids < 1 || n_ids > ctx->k) return fail(ctx, CKV_EINVAL, "bad argument");
+  if (!ctx->stored[layer]) return fail(ctx, CKV_ESTATE, "layer %d prefix not stored", layer);
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PlanOut po{ctx->gl_main, ctx->nload_main, nullptr, nullptr, ctx->counts + (size_t)(layer * 2) * 4, ctx->stats,
+             nullptr, nullptr};
+  LK(launch_cache_plan(cache_layer(ctx, layer), ids, nullptr, n_ids, 0, 0, ctx->epoch, ctx->rec_bytes, nullptr,
+                       ctx->scratch_main, po, st));
+  LK(launch_gather(ctx->gl_main, ctx->nload_main, host_layer_dev(ctx, layer), pool_layer(ctx, layer), ctx->rec_bytes,
+                   st));
   return CKV_OK;
 }
 

@@ -139,6 +139,8 @@ cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, 
 cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1,
                               int32_t* flag_scratch, int32_t* ids_glob, int32_t* ids_local,
                               int32_t* n_local, cudaStream_t st);
+cudaError_t launch_block_cover(const int32_t* ids, int n_ids, int u, int B, int64_t n, int32_t* blocks,
+                               int32_t* n_blocks, cudaStream_t st);
 // A4 / A5 / A9
 struct CacheLayer {
   int32_t* slot_of;   // [m_loc]
@@ -159,6 +161,7 @@ struct PlanOut {
   int64_t* stats;        // device counters or null
   const float* upd_A;    // if set (demand plans): fused A9 update I += A, F += 1 after planning
   const int32_t* epoch_dev;  // if set: request epoch read from device memory (graph-safe)
+  int32_t* ids_out = nullptr;  // if set: copy of the planned ids (the caller's selected_ids)
 };
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t* scratch64,

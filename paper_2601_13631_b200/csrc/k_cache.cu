@@ -41,38 +41,55 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
   int32_t* miss = scratch;            // [n_ids]
   int32_t* freel = scratch + n_ids;   // [P]
   int32_t* vict = freel + cl.P;       // [P]
+  int32_t* mpos = vict + cl.P;        // [n_ids]: position in ids of each miss
   if (threadIdx.x == 0) { s_hits = 0; s_spec_used = 0; }
   __syncthreads();
 
-  // 1. hit / miss, misses compacted in ascending chunk order
+  // 1. hit / miss, misses compacted in ascending chunk order.  Hits write their kept slot now;
+  //    a miss's position in ids is kept (mpos) so step 4 writes its slot without another lookup.
+  //    The A9 update is fused here: it touches only requested chunks, which
+  //    are never eviction candidates, so the victims are those of an update after planning.
   int n_miss = 0;
   for (int b = 0; b < n_ids; b += NT) {
     const int t = b + threadIdx.x;
     bool is_miss = false;
+    int j = -1;
     if (t < n_ids) {
-      const int s = cl.slot_of[ids[t]];
+      j = ids[t];
+      const int s = cl.slot_of[j];
       is_miss = s < 0;
       if (!is_miss) {
         atomicAdd(&s_hits, 1);
         if (!prefetch && cl.pf_epoch[s] == epoch) atomicAdd(&s_spec_used, 1);
       }
+      if (out.kept_slots) out.kept_slots[t] = s;  // misses: -1 until step 4 assigns a slot
+      if (out.ids_out) out.ids_out[t] = j;
+      if (out.upd_A) {
+        cl.I[j] += out.upd_A[j];
+        cl.F[j] += 1;
+        cl.T[j] = epoch;
+      }
     }
     int tot;
     const int pos = block_excl_scan<NT>(is_miss ? 1 : 0, tot, ss);
-    if (is_miss) miss[n_miss + pos] = ids[t];
+    if (is_miss) {
+      miss[n_miss + pos] = j;
+      mpos[n_miss + pos] = t;
+    }
     n_miss += tot;
   }
   if (prefetch) n_miss = min(n_miss, quota);
-  // 2. free slots, ascending
+  // 2. free slots, ascending (only needed when something is loaded)
   int n_free = 0;
-  for (int b = 0; b < cl.P; b += NT) {
-    const int s = b + threadIdx.x;
-    const bool f = s < cl.P && cl.owner[s] < 0;
-    int tot;
-    const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
-    if (f) freel[n_free + pos] = s;
-    n_free += tot;
-  }
+  if (n_miss > 0)
+    for (int b = 0; b < cl.P; b += NT) {
+      const int s = b + threadIdx.x;
+      const bool f = s < cl.P && cl.owner[s] < 0;
+      int tot;
+      const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+      if (f) freel[n_free + pos] = s;
+      n_free += tot;
+    }
   // 3. victims: the `need` lowest (S, j) evictable residents
   int need = n_miss - n_free;
   int n_vict = 0;
@@ -129,17 +146,8 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
     cl.pf_epoch[s] = prefetch ? epoch : -1;
     out.gather_list[2 * t] = j;
     out.gather_list[2 * t + 1] = s;
+    if (out.kept_slots) out.kept_slots[mpos[t]] = s;
   }
-  __syncthreads();
-  if (out.kept_slots)
-    for (int t = threadIdx.x; t < n_ids; t += NT) out.kept_slots[t] = cl.slot_of[ids[t]];
-  if (out.upd_A)  // A9: after the victims were chosen with the old S
-    for (int t = threadIdx.x; t < n_ids; t += NT) {
-      const int j = ids[t];
-      cl.I[j] += out.upd_A[j];
-      cl.F[j] += 1;
-      cl.T[j] = epoch;
-    }
   if (threadIdx.x == 0) {
     *out.n_load = n_miss;
     if (out.counts) {

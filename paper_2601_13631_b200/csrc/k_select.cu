@@ -13,10 +13,60 @@ namespace {
 
 constexpr int NT = 1024;
 
+// Keys in registers (KPT per thread, m <= NT * KPT): A_j is summed from the per-KV-head partials
+// once, and the eight radix passes and the compaction run without memory traffic.
+template <int KPT>
 __global__ void __launch_bounds__(NT) topk_scores_kernel(float* __restrict__ A, const float* __restrict__ Apart,
                                                          int nparts, int m, int k, int id_offset,
                                                          int32_t* __restrict__ ids, uint64_t* __restrict__ cand,
                                                          int n_cand_out, int32_t* __restrict__ n_out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ SelectSmem ss;
+  uint64_t key[KPT];
+#pragma unroll
+  for (int u = 0; u < KPT; ++u) {
+    const int j = threadIdx.x + NT * u;
+    key[u] = 0ull;
+    if (j < m) {
+      float a;
+      if (Apart) {  // A_j = sum over KV heads of the chunk-sum partials, fixed order
+        a = 0.f;
+        for (int h = 0; h < nparts; ++h) a += Apart[(size_t)h * m + j];
+        A[j] = a;
+      } else {
+        a = A[j];
+      }
+      key[u] = ((uint64_t)__float_as_uint(a) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j + id_offset));
+    }
+  }
+  const int kk = min(k, m);
+  const uint64_t T = block_kth_largest_regs<NT, KPT>(key, m, kk, ss);
+  // ascending compaction
+  int base = 0;
+#pragma unroll
+  for (int u = 0; u < KPT; ++u) {
+    if (NT * u >= m) break;
+    const int j = threadIdx.x + NT * u;
+    const bool f = (j < m) && key[u] >= T;
+    int tot;
+    const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+    if (f) {
+      if (ids) ids[base + pos] = j + id_offset;
+      if (cand) cand[base + pos] = key[u];
+    }
+    base += tot;
+  }
+  if (cand)
+    for (int t = kk + threadIdx.x; t < n_cand_out; t += NT) cand[t] = 0ull;
+  if (n_out && threadIdx.x == 0) *n_out = base;
+}
+
+// Large m (> NT * 8 chunks): keys re-read from A every pass.
+__global__ void __launch_bounds__(NT) topk_scores_big_kernel(float* __restrict__ A, const float* __restrict__ Apart,
+                                                             int nparts, int m, int k, int id_offset,
+                                                             int32_t* __restrict__ ids, uint64_t* __restrict__ cand,
+                                                             int n_cand_out, int32_t* __restrict__ n_out) {
   pdl_wait();
   pdl_trigger();
   __shared__ SelectSmem ss;
@@ -33,7 +83,6 @@ __global__ void __launch_bounds__(NT) topk_scores_kernel(float* __restrict__ A, 
   };
   const int kk = min(k, m);
   const uint64_t T = block_kth_largest<NT>(key, m, kk, ss);
-  // ascending compaction
   int base = 0;
   for (int j0 = 0; j0 < m; j0 += NT) {
     const int j = j0 + threadIdx.x;
@@ -86,11 +135,57 @@ __global__ void __launch_bounds__(NT) topk_merge_kernel(const uint64_t* __restri
   if (threadIdx.x == 0) *n_local = lbase;
 }
 
+// NEXT-4 granularity accounting: the ascending ids of the B-token
+// blocks of a coarse block store that hold at least one token of the selected u-token units
+// (ids ascending; unit j = tokens [j*u, min((j+1)*u, n))).  Because the ids ascend, the block
+// range of unit t only has to be clipped against the last block of unit t-1 to stay unique.
+__global__ void __launch_bounds__(NT) block_cover_kernel(const int32_t* __restrict__ ids, int n_ids, int u, int B,
+                                                         int64_t n, int32_t* __restrict__ blocks,
+                                                         int32_t* __restrict__ n_blocks) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ SelectSmem ss;
+  auto last_block = [&](int j) -> int64_t { return (min((int64_t)(j + 1) * u, n) - 1) / B; };
+  int base = 0;
+  for (int t0 = 0; t0 < n_ids; t0 += NT) {
+    const int t = t0 + threadIdx.x;
+    int64_t start = 0, nb = 0;
+    if (t < n_ids) {
+      const int j = ids[t];
+      start = (int64_t)j * u / B;
+      if (t > 0) start = max(start, last_block(ids[t - 1]) + 1);
+      nb = max((int64_t)0, last_block(j) - start + 1);
+    }
+    int tot;
+    const int pos = block_excl_scan<NT>((int)nb, tot, ss);
+    for (int i = 0; i < (int)nb; ++i) blocks[base + pos + i] = (int32_t)(start + i);
+    base += tot;
+  }
+  if (threadIdx.x == 0) *n_blocks = base;
+}
+
 }  // namespace
+
+cudaError_t launch_block_cover(const int32_t* ids, int n_ids, int u, int B, int64_t n, int32_t* blocks,
+                               int32_t* n_blocks, cudaStream_t st) {
+  if (cudaError_t e_ = launch_kernel(block_cover_kernel, 1, NT, 0, st, ids, n_ids, u, B, n, blocks, n_blocks)) return e_;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, int k, int id_offset, int32_t* ids,
                                uint64_t* cand_out, int n_cand_out, int32_t* n_out, cudaStream_t st) {
-  if (cudaError_t e_ = launch_kernel(topk_scores_kernel, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out)) return e_;
+  cudaError_t e_;
+  if (m <= NT)
+    e_ = launch_kernel(topk_scores_kernel<1>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+  else if (m <= 2 * NT)
+    e_ = launch_kernel(topk_scores_kernel<2>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+  else if (m <= 4 * NT)
+    e_ = launch_kernel(topk_scores_kernel<4>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+  else if (m <= 8 * NT)
+    e_ = launch_kernel(topk_scores_kernel<8>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+  else
+    e_ = launch_kernel(topk_scores_big_kernel, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+  if (e_) return e_;
   return cudaGetLastError();
 }
 

@@ -49,9 +49,20 @@ __device__ uint64_t block_kth_largest(KeyFn key, int n, int k, SelectSmem& ss) {
   for (int shift = 56; shift >= 0; shift -= 8) {
     for (int b = threadIdx.x; b < 256; b += NT) ss.hist[b] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += NT) {
-      const uint64_t kv = key(i);
-      if ((kv & mask) == prefix) atomicAdd(&ss.hist[(kv >> shift) & 255u], 1);
+    for (int i0 = 0; i0 < n; i0 += NT) {  // whole warps per iteration (warp-aggregated counts)
+      const int i = i0 + threadIdx.x;
+      uint64_t kv = 0;
+      bool in = false;
+      if (i < n) {
+        kv = key(i);
+        in = (kv & mask) == prefix;
+      }
+      const unsigned act = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const unsigned dig = (unsigned)(kv >> shift) & 255u;
+        const unsigned peers = __match_any_sync(act, dig);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&ss.hist[dig], __popc(peers));
+      }
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -93,6 +104,71 @@ __device__ uint64_t block_kth_largest(KeyFn key, int n, int k, SelectSmem& ss) {
     // every key of the chosen bin is selected: keys >= prefix (low digits 0) are exactly k
     if (done) break;
   }
+  return prefix;
+}
+
+// Same select over keys held in registers: thread t owns keys i = t + NT*u (u < KPT), valid iff
+// i < n.  No memory traffic per pass (the hot-path top-k over m <= NT*KPT chunk scores).
+template <int NT, int KPT>
+__device__ uint64_t block_kth_largest_regs(const uint64_t (&keys)[KPT], int n, int k, SelectSmem& ss) {
+  uint64_t prefix = 0, mask = 0;
+  int krem = k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int b = threadIdx.x; b < 256; b += NT) ss.hist[b] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+      const int i = threadIdx.x + NT * u;
+      const bool in = i < n && (keys[u] & mask) == prefix;
+      // warp-aggregated: early passes put most keys in a few bins (same float exponent)
+      const unsigned act = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const unsigned dig = (unsigned)(keys[u] >> shift) & 255u;
+        const unsigned peers = __match_any_sync(act, dig);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&ss.hist[dig], __popc(peers));
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int cnt[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        cnt[j] = ss.hist[255 - 8 * lane - j];
+        tot += cnt[j];
+      }
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int excl = incl - tot;
+      const unsigned bal = __ballot_sync(0xffffffffu, excl < krem && incl >= krem);
+      if (lane == __ffs(bal) - 1) {
+        int cum = excl;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (cum + cnt[j] >= krem) {
+            ss.state[0] = 255 - 8 * lane - j;
+            ss.state[1] = krem - cum;
+            ss.state[2] = (cnt[j] == krem - cum);
+            break;
+          }
+          cum += cnt[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (uint64_t)ss.state[0] << shift;
+    mask |= (uint64_t)255u << shift;
+    krem = ss.state[1];
+    const bool done = ss.state[2] != 0;
+    if (done) break;
+    // the next pass's histogram clear is ordered after every thread read state (the clear
+    // touches hist only, and state is rewritten only after the next pass's second barrier)
+  }
+  __syncthreads();
   return prefix;
 }
 

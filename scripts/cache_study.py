@@ -6,7 +6,8 @@ Workload: the C3 shape (Qwen2.5-7B, 28 layers, 32K prefix, c = 16, n_s = 128, bf
 distinct requests (each its own topic mixture, synth.make_request) drawn 48 times with Zipf(1)
 popularity (seed 42); the first 16 draws warm the cache ("warm up one full pass"),
 the other 32 are measured.  Budgets 10% and 25% (the ablation's ratio); per-layer
-HBM cache of P = 2.5 k slots (prefetch quota k included when prefetch is on).  Per variant:
+HBM cache of P = 1.25k, 1.5k, 2k, 3k slots (the prefetch quota, min(k, P - k), is part of P when
+prefetch is on, so both variants have the same HBM).  Per variant:
 hit rate, host-link MB per layer (critical-path delta and speculative), and the median eager
 us/layer over the measured requests (CUDA events on the launching stream).
 
@@ -51,12 +52,11 @@ def main():
     results = []
     for bp in [int(b) for b in args.budgets.split(",")]:
         k = ckv_budget_chunks(base.prefix_len, base.chunk_size, bp)
-        P = k * 5 // 2
         ids = [torch.empty(k, dtype=torch.int32, device=dev) for _ in range(L)]
-        for prefetch in (True, False):
+        for P, prefetch in [(P, pf) for P in (k * 5 // 4, k * 3 // 2, 2 * k, 3 * k) for pf in (True, False)]:
+            quota = min(k, P - k) if prefetch else 0
             ctx = Context(L, base.num_q_heads, base.num_kv_heads, base.head_dim, base.chunk_size, base.prefix_len,
-                          base.suffix_len, dtype="bf16", budget_bp=bp, prefetch_chunks=k if prefetch else 0,
-                          cache_slots=P)
+                          base.suffix_len, dtype="bf16", budget_bp=bp, prefetch_chunks=quota, cache_slots=P)
             for l in range(L):
                 ctx.store_prefix(l, *prefix[l])
             for policy in ("attn", "lfu", "lru"):
@@ -77,7 +77,7 @@ def main():
                 st = ctx.get_stats()
                 nl = max(st["total_layers"], 1)
                 sel = st["total_hits"] + st["total_misses"]
-                row = {"budget_bp": bp, "k": k, "slots_per_layer": P, "prefetch": prefetch, "policy": policy,
+                row = {"budget_bp": bp, "k": k, "slots_per_layer": P, "prefetch_quota": quota, "policy": policy,
                        "hit_rate": st["total_hits"] / max(sel, 1),
                        "delta_MB_per_layer": st["total_link_bytes_delta"] / nl / 1e6,
                        "spec_MB_per_layer": st["total_link_bytes_spec"] / nl / 1e6,

@@ -334,3 +334,37 @@ def test_delta_law_and_whole_chunk_transfers():
     assert st["total_link_bytes_spec"] == st["total_spec_loads"] * rec
     assert st["total_hits"] + st["total_misses"] == 3 * cfg.num_layers * k
     assert st["total_layers"] == 3 * cfg.num_layers
+
+
+# ---------------------------------------------------------------- granularity (NEXT-4)
+@pytest.mark.parametrize("c,B,n", [(1, 64, 5000), (16, 64, 5000), (16, 16, 4999), (16, 24, 4999), (64, 16, 5000),
+                                   (4, 6, 777)])
+def test_block_cover_matches_oracle(c, B, n):
+    m = -(-n // c)
+    ctx = Context(1, 2, 1, 64, c, n, 4, dtype="fp32", budget_chunks=m, cache_slots=m)
+    g = np.random.default_rng(c * 1000 + B)
+    for trial in range(8):
+        cnt = [0, 1, m][trial] if trial < 3 else int(g.integers(1, m + 1))
+        ids = np.sort(g.choice(m, cnt, replace=False)).astype(np.int32)
+        blocks, nb = ctx.block_cover(torch.from_numpy(ids).cuda(), B)
+        nb = int(nb.item())
+        assert blocks[:nb].cpu().tolist() == O.block_cover(ids, c, B, n)
+    ctx.close()
+
+
+def test_load_chunks_counts_whole_records():
+    n, c = 4096, 64
+    m = n // c
+    ctx = Context(1, 2, 2, 64, c, n, 4, dtype="fp32", budget_chunks=m, cache_slots=m)
+    kp = torch.randn(n, 2, 64, device="cuda")
+    ctx.store_prefix(0, kp, kp)
+    ids = torch.tensor([0, 3, 7, 8, 40, 63], dtype=torch.int32, device="cuda")
+    ctx.reset_stats()
+    ctx.load_chunks(0, ids)
+    st = ctx.get_stats()
+    rec = 2 * 2 * c * 64 * 4
+    assert st["total_misses"] == 6 and st["total_hits"] == 0 and st["total_link_bytes_delta"] == 6 * rec
+    ctx.load_chunks(0, ids)  # now resident
+    st = ctx.get_stats()
+    assert st["total_hits"] == 6 and st["total_misses"] == 6
+    ctx.close()

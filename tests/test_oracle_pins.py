@@ -367,3 +367,44 @@ def test_period_reuses_first_layer_ids():
     Qs, Ks, Vs, Kp, Vp = lay[2]
     toks = O.kept_token_index(first[0], 96, 8)
     np.testing.assert_allclose(per[2]["out"], O.attention(Qs, Ks, Vs, Kp, Vp, toks, 2)[0], atol=1e-14)
+
+
+# ------------------------------------------------------------ granularity / RA (NEXT-4)
+def _paper_ra_cases():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "paper_read_amplification.json")) as f:
+        return json.load(f)["cases"]
+
+
+@pytest.mark.parametrize("case", _paper_ra_cases(), ids=lambda c: c["cite"][:18])
+def test_read_amplification_paper_values(case):
+    """The RA values PAPER.md prints (52, 4, 1), on token placements that match the text."""
+    B, need, nblk = case["block_tokens"], case["needed_tokens"], case["blocks"]
+    u = case.get("unit_tokens", 1)
+    n = 64 * 64
+    # `need` tokens spread over `nblk` distinct blocks (one per block, the rest in block 0)
+    units = need // u
+    ids = sorted({(b * B) // u for b in range(nblk)} | set(range(1, units - nblk + 1)) if nblk > 1
+                 else range(units))
+    assert len(ids) == units
+    read, needed, ra = O.read_amplification(ids, u, B, n)
+    assert (read, needed) == (case["tokens_read"], need)
+    assert int(ra) == case["ra_floor"]
+    assert len(O.block_cover(ids, u, B, n)) == nblk
+
+
+def test_block_cover_laws():
+    g = np.random.default_rng(11)
+    for u, B, n in [(1, 64, 1000), (16, 64, 1000), (16, 16, 1000), (16, 24, 999), (64, 16, 1000), (4, 6, 77)]:
+        m = -(-n // u)
+        for _ in range(20):
+            ids = np.sort(g.choice(m, g.integers(1, m + 1), replace=False))
+            cov = O.block_cover(ids, u, B, n)
+            read, needed, ra = O.read_amplification(ids, u, B, n)
+            assert ra >= 1.0 - 1e-15 and read <= n
+            if u == B:  # alignment law: the selection unit is the storage unit -> RA = 1 (PAPER.md:326-327)
+                assert cov == ids.tolist() and read == needed
+            if B % u == 0:  # every unit sits inside one block
+                assert cov == sorted({int(j) * u // B for j in ids})
+        assert O.block_cover(range(m), u, B, n) == list(range(-(-n // B)))  # everything -> every block
