@@ -226,7 +226,7 @@ int64_t ckv_kernel_launches(const ckv_ctx* ctx);
  *   selected chunks of this ctx (chunk j = tokens [j*c, min((j+1)*c, n)), Eq. 1 range):
  *   read amplification RA = tokens of those blocks / tokens of the chunks (PAPER.md:209-221,
  *   325-327; RA = 1 when block_tokens == c).
- *   ids     device int32 [n_ids], ascending global chunk ids (n_ids may be 0)
+ *   ids     device int32 [n_ids], ascending global chunk ids (n_ids may be 0; ids may then be NULL)
  *   blocks  device int32, capacity ceil(n / block_tokens): ascending block ids (written)
  *   n_blocks device int32 [1]: number of blocks (written)
  * ckv_load_chunks: plan (A4) and gather (A5) an explicit ascending list of local chunk ids of

@@ -257,16 +257,20 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
     CK(cudaStreamWaitEvent(st, ctx->ev_pplan[layer], 0));
     pdl_mark_event_wait(st);
   }
+  // tcgen05 path: the compaction kernel loads the misses itself (A5 fused, no gather launch)
+  const bool fused_gather = ctx->dtype == CKV_BF16 && ctx->attn_kind == 1;
   PlanOut po{ctx->gl_main, ctx->nload_main, ctx->kept_slots, nullptr, ctx->counts + (size_t)(layer * 2) * 4,
-             ctx->stats, ctx->A, ctx->epoch_dev, ids_out};
+             ctx->stats, ctx->A, ctx->epoch_dev, ids_out, fused_gather ? 1 : 0};
   PROF_BEGIN(3);
   LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 0, 0, ctx->epoch, ctx->rec_bytes, nullptr,
                        ctx->scratch_main, po, st));
   PROF_END(3);
-  PROF_BEGIN(4);
-  LK(launch_gather(ctx->gl_main, ctx->nload_main, host_layer_dev(ctx, layer), pool_layer(ctx, layer), ctx->rec_bytes,
-                   st));
-  PROF_END(4);
+  if (!fused_gather) {
+    PROF_BEGIN(4);
+    LK(launch_gather(ctx->gl_main, ctx->nload_main, host_layer_dev(ctx, layer), pool_layer(ctx, layer),
+                     ctx->rec_bytes, st));
+    PROF_END(4);
+  }
   if (pf) {
     CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
     pdl_mark_event_wait(st);
@@ -289,7 +293,8 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
       e = launch_attn_tc(g, static_cast<const __nv_bfloat16*>(q), static_cast<const __nv_bfloat16*>(ks),
                          static_cast<const __nv_bfloat16*>(vs),
                          reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->kept_slots, ids,
-                         n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->dense_kv, st);
+                         n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->dense_kv,
+                         host_layer_dev(ctx, layer), st);
       if (e == cudaSuccess) ctx->launches += 1;  // + the dense K/V compaction kernel
     }
     if (e == cudaErrorNotSupported) {
@@ -854,7 +859,8 @@ ckv_status ckv_block_cover(ckv_ctx* ctx, const int32_t* ids, int32_t n_ids, int3
                            int32_t* n_blocks, void* stream) {
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
-  if (!ids || !blocks || !n_blocks || n_ids < 0 || block_tokens < 1) return fail(ctx, CKV_EINVAL, "bad argument");
+  if ((!ids && n_ids > 0) || !blocks || !n_blocks || n_ids < 0 || block_tokens < 1)
+    return fail(ctx, CKV_EINVAL, "bad argument");
   CK(cudaSetDevice(ctx->cfg.device));
   LK(launch_block_cover(ids, n_ids, ctx->c, block_tokens, ctx->n, blocks, n_blocks,
                         static_cast<cudaStream_t>(stream)));

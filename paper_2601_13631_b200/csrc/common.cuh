@@ -162,6 +162,8 @@ struct PlanOut {
   const float* upd_A;    // if set (demand plans): fused A9 update I += A, F += 1 after planning
   const int32_t* epoch_dev;  // if set: request epoch read from device memory (graph-safe)
   int32_t* ids_out = nullptr;  // if set: copy of the planned ids (the caller's selected_ids)
+  int mark_miss = 0;  // kept_slots of a miss = -(slot + 2): the consumer (compact_kv) loads it from the
+                      // host store itself and fills the slot (no separate gather launch)
 };
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t* scratch64,
@@ -193,7 +195,8 @@ size_t attn_tc_dense_bytes(const LayerGeom& g, int k_cap, int max_ns);
 cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* k_suf,
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
                            const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
-                           int nsplit, float* o_part, float* lse_part, void* dense_ws, cudaStream_t st);
+                           int nsplit, float* o_part, float* lse_part, void* dense_ws, const char* host_layer,
+                           cudaStream_t st);
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit,
                                 T* out, float* o_f32, float* lse_nat, cudaStream_t st);

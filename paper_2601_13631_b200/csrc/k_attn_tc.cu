@@ -95,7 +95,12 @@ __device__ __forceinline__ bool tile_present(const AttnParams& p, const Tiles& t
 // prefix (kvh, kept chunk i, part = K h0 | K h1 | V h0 | V h1): c rows of 128 B copied as is
 // (record rows are swizzled by (row & 7) and c % 8 == 0, so they land swizzled);
 // suffix (kvh, key t, K|V): one 256 B row of k_suf / v_suf, 16-byte units swizzled on the way.
-__global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, const char* __restrict__ pool,
+// A kept chunk the planner marked as a miss (slot encoded as -(s + 2)) is read from the mapped
+// host store instead (A5 fused: whole records) and also written to its cache
+// slot s, so the layer has no separate gather launch on its critical path.
+__global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __restrict__ pool,
+                                                         const char* __restrict__ host_layer,
+                                                         const int32_t* __restrict__ kept_ids,
                                                          int64_t rec_bytes, const int32_t* __restrict__ kept_slots,
                                                          const int32_t* __restrict__ n_kept_dev, int k_cap,
                                                          const __nv_bfloat16* __restrict__ k_suf,
@@ -115,12 +120,32 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, const char
       const int64_t ci = w >> 2;
       const int kvh = (int)(ci / k_cap), i = (int)(ci % k_cap);
       if (i >= n_kept) continue;
-      const uint4* src = reinterpret_cast<const uint4*>(pool + (int64_t)kept_slots[i] * rec_bytes +
-                                                        (int64_t)kvh * 4 * piece + part * piece);
+      const int slot = kept_slots[i];
+      if (slot == -1) continue;  // not loaded (planner capacity failure, reported in the stats)
+      const int64_t off = (int64_t)kvh * 4 * piece + part * piece;
       const int key = i * g.c;
       uint4* dst = reinterpret_cast<uint4*>(dense + ((int64_t)kvh * T_cap + key / BN) * kKVBytes +
                                             part * kPartBytes + (key % BN) * 128);
-      for (int u = lane; u < (int)(piece / 16); u += 32) dst[u] = src[u];
+      if (slot >= 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(pool + (int64_t)slot * rec_bytes + off);
+        for (int u = lane; u < (int)(piece / 16); u += 32) dst[u] = src[u];
+      } else {
+        const uint4* src = reinterpret_cast<const uint4*>(host_layer + (int64_t)kept_ids[i] * rec_bytes + off);
+        uint4* cdst = reinterpret_cast<uint4*>(pool + (int64_t)(-slot - 2) * rec_bytes + off);
+        const int nu = (int)(piece / 16);
+        for (int u0 = 0; u0 < nu; u0 += 32 * 8) {  // 8 host loads in flight per lane
+          uint4 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (u0 + lane + 32 * q < nu) v[q] = __ldg(src + u0 + lane + 32 * q);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (u0 + lane + 32 * q < nu) {
+              dst[u0 + lane + 32 * q] = v[q];
+              cdst[u0 + lane + 32 * q] = v[q];
+            }
+        }
+      }
     } else {
       const int64_t si = w - n_pre;
       const int kv = (int)(si & 1);
@@ -477,7 +502,8 @@ size_t attn_tc_dense_bytes(const LayerGeom& g, int k_cap, int max_ns) {
 cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* k_suf,
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
                            const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
-                           int nsplit, float* o_part, float* lse_part, void* dense_ws, cudaStream_t st) {
+                           int nsplit, float* o_part, float* lse_part, void* dense_ws, const char* host_layer,
+                           cudaStream_t st) {
   if (!attn_tc_supported(g) || !dense_ws) return cudaErrorNotSupported;
   AttnParams p;
   p.g = g;
@@ -498,7 +524,9 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   const int64_t rec_bytes = (int64_t)2 * g.Hkv * g.c * D * 2;
   const int64_t n_warps = (int64_t)g.Hkv * k_cap * 4 + (include_suffix ? (int64_t)g.Hkv * g.ns * 2 : 0);
   const int cblocks = (int)std::min<int64_t>((n_warps + 7) / 8, 8 * sm_count());
-  if (cudaError_t e_ = launch_kernel(compact_kv_kernel, cblocks, 256, 0, st, g, reinterpret_cast<const char*>(pool_layer), rec_bytes, kept_slots,
+  if (cudaError_t e_ = launch_kernel(compact_kv_kernel, cblocks, 256, 0, st, g,
+                                     reinterpret_cast<char*>(const_cast<__nv_bfloat16*>(pool_layer)), host_layer,
+                                     kept_ids, rec_bytes, kept_slots,
                                              n_kept_dev, k_cap, k_suf, v_suf, include_suffix, p.NTp_cap, p.T_cap,
                                              static_cast<char*>(dense_ws))) return e_;
   cudaError_t e = cudaGetLastError();

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
     cl.pf_epoch[s] = prefetch ? epoch : -1;
     out.gather_list[2 * t] = j;
     out.gather_list[2 * t + 1] = s;
-    if (out.kept_slots) out.kept_slots[mpos[t]] = s;
+    if (out.kept_slots) out.kept_slots[mpos[t]] = out.mark_miss ? -(s + 2) : s;
   }
   if (threadIdx.x == 0) {
     *out.n_load = n_miss;

@@ -81,7 +81,7 @@ def main():
         ctx.close()
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out, "w") as f:
-        json.dump({"workload": "c3_7b layer 0, 10% budget, requests 0..%d" % (args.requests - 1), "rows": rows},
+        json.dump({"workload": f"c3_7b layer 0, 10% budget, requests 0..{args.requests - 1}", "rows": rows},
                   f, indent=1)
 
 
