@@ -54,6 +54,7 @@ struct ckv_ctx {
   float *o_part = nullptr, *lse_part = nullptr;
   int64_t* stats = nullptr;  // [16]
   int32_t* epoch_dev = nullptr;  // request counter on the device (graph-safe)
+  int32_t* ticket = nullptr;     // grid ticket of the fused select kernel
   void* tmap_cache = nullptr;
   void* dense_kv = nullptr;  // tcgen05 attention: dense K/V tiles of the current layer
 
@@ -246,10 +247,18 @@ ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int
   return CKV_OK;
 }
 
+// tcgen05 path: the compaction kernel loads the misses itself (A5 fused, no gather launch)
+bool gather_fused(const ckv_ctx* ctx) { return ctx->dtype == CKV_BF16 && ctx->attn_kind == 1; }
+
+PlanOut demand_plan_out(ckv_ctx* ctx, int layer, int32_t* ids_out) {
+  return PlanOut{ctx->gl_main, ctx->nload_main, ctx->kept_slots, nullptr, ctx->counts + (size_t)(layer * 2) * 4,
+                 ctx->stats, ctx->A, ctx->epoch_dev, ids_out, gather_fused(ctx) ? 1 : 0};
+}
+
 // A4 -> A5 -> A7 -> A8 -> A9 for the local selected ids.
 ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, const void* q,
                       const void* ks, const void* vs, int ns, int include_suffix, void* out, float* o_f32,
-                      float* lse_nat, int32_t* ids_out, cudaStream_t st) {
+                      float* lse_nat, int32_t* ids_out, bool planned, cudaStream_t st) {
   // a prefetch of this layer that the stream already joined (before the score kernel) needs no
   // further event waits: they would only cut the programmatic launch edges of plan and attention
   const bool pf = ctx->pf_issued[layer] == ctx->epoch && ctx->pf_joined[layer] != ctx->epoch;
@@ -257,14 +266,13 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
     CK(cudaStreamWaitEvent(st, ctx->ev_pplan[layer], 0));
     pdl_mark_event_wait(st);
   }
-  // tcgen05 path: the compaction kernel loads the misses itself (A5 fused, no gather launch)
-  const bool fused_gather = ctx->dtype == CKV_BF16 && ctx->attn_kind == 1;
-  PlanOut po{ctx->gl_main, ctx->nload_main, ctx->kept_slots, nullptr, ctx->counts + (size_t)(layer * 2) * 4,
-             ctx->stats, ctx->A, ctx->epoch_dev, ids_out, fused_gather ? 1 : 0};
-  PROF_BEGIN(3);
-  LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 0, 0, ctx->epoch, ctx->rec_bytes, nullptr,
-                       ctx->scratch_main, po, st));
-  PROF_END(3);
+  const bool fused_gather = gather_fused(ctx);
+  if (!planned) {
+    PROF_BEGIN(3);
+    LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 0, 0, ctx->epoch, ctx->rec_bytes, nullptr,
+                         ctx->scratch_main, demand_plan_out(ctx, layer, ids_out), st));
+    PROF_END(3);
+  }
   if (!fused_gather) {
     PROF_BEGIN(4);
     LK(launch_gather(ctx->gl_main, ctx->nload_main, host_layer_dev(ctx, layer), pool_layer(ctx, layer),
@@ -331,7 +339,7 @@ void free_all(ckv_ctx* ctx) {
                       ctx->lampart, ctx->Lam2, ctx->A, ctx->Apart, ctx->ids_buf[0], ctx->ids_buf[1], ctx->n_ids_buf[0],
                       ctx->n_ids_buf[1], ctx->kept_slots, ctx->ids_glob, ctx->flag, ctx->scratch_main,
                       ctx->scratch_side, ctx->gl_main, ctx->gl_side, ctx->nload_main, ctx->nload_side, ctx->counts,
-                      ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache, ctx->dense_kv, ctx->epoch_dev};
+                      ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache, ctx->dense_kv, ctx->epoch_dev, ctx->ticket};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (ctx->host_store) cudaFreeHost(ctx->host_store);
@@ -476,6 +484,8 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   CKC(dalloc(&ctx->lse_part, (size_t)ctx->nsplit_attn_max * ctx->Hkv * R_max));
   CKC(dalloc(&ctx->stats, 16));
   CKC(dalloc(&ctx->epoch_dev, 1));
+  CKC(dalloc(&ctx->ticket, 1));
+  CKC(cudaMemset(ctx->ticket, 0, sizeof(int32_t)));
   CKC(cudaMemset(ctx->epoch_dev, 0, sizeof(int32_t)));
   CKC(cudaMemset(ctx->stats, 0, sizeof(int64_t) * 16));
   int lo = 0, hi = 0;
@@ -592,6 +602,7 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
   const int pend = (pid + 1) * p < ctx->L ? (pid + 1) * p : ctx->L;  // end of this period
   int32_t* ids = ctx->ids_buf[pid & 1];  // double-buffered by period: side-stream plans may still read it
   int32_t* nids = ctx->n_ids_buf[pid & 1];
+  bool planned = false;  // the demand plan of this layer ran inside the fused select kernel
   if (first) {  // identification: A1 -> A2 -> A3
     // The persistent score kernel needs every SM: side-stream prefetch work for this layer must
     // not still be resident when it starts (one late CTA delays the whole statically partitioned
@@ -605,12 +616,22 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     int nsplit = 0;
     if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
     LayerGeom g = geom(ctx, n_suffix);
-    PROF_BEGIN(2);
-    LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
-    PROF_END(2);
-    PROF_BEGIN(6);
-    LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, ids, nullptr, 0, nids, st));
-    PROF_END(6);
+    if (chunk_sum_select_supported(g)) {
+      // A2 chunk sums + A3 top-k (+ A4 plan + A9 when this layer's prefetch is joined) in one launch
+      planned = ctx->pf_issued[layer] != ctx->epoch || ctx->pf_joined[layer] == ctx->epoch;
+      SelectPlanArgs a{ctx->A, ctx->k, ids, nids, ctx->ticket, planned ? 1 : 0, cache_layer(ctx, layer), ctx->epoch,
+                       ctx->rec_bytes, ctx->scratch_main, demand_plan_out(ctx, layer, selected_ids)};
+      PROF_BEGIN(2);
+      LK(launch_chunk_sum_select(g, ctx->lam2, ctx->Lam2, ctx->Apart, a, st));
+      PROF_END(2);
+    } else {
+      PROF_BEGIN(2);
+      LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
+      PROF_END(2);
+      PROF_BEGIN(6);
+      LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, ids, nullptr, 0, nids, st));
+      PROF_END(6);
+    }
     // intra-period loads (exact ids) for the period's other layers, then the speculative load of
     // the next period's first layer (A6), all on the side stream in layer order
     for (int lp = layer + 1; lp <= pend && lp < ctx->L; ++lp)
@@ -623,8 +644,8 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
       }
   }
   // the demand planner also writes selected_ids (no separate copy node per layer)
-  if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, selected_ids, st)) !=
-      CKV_OK)
+  if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, selected_ids,
+                      planned, st)) != CKV_OK)
     return s;
   if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;
@@ -687,7 +708,7 @@ ckv_status ckv_shard_attend(ckv_ctx* ctx, int32_t layer, const uint64_t* cand_al
                        nids, st));
   if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st)) != CKV_OK) return s;
   if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, ctx->shard == ctx->W - 1, nullptr, o_part,
-                      lse_part, nullptr, st)) != CKV_OK)
+                      lse_part, nullptr, false, st)) != CKV_OK)
     return s;
   CK(cudaMemcpyAsync(selected_ids, ctx->ids_glob, sizeof(int32_t) * ctx->k, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;

@@ -165,6 +165,23 @@ struct PlanOut {
   int mark_miss = 0;  // kept_slots of a miss = -(slot + 2): the consumer (compact_kv) loads it from the
                       // host store itself and fills the slot (no separate gather launch)
 };
+// A2 chunk sums -> A3 top-k -> A4 plan in one launch (k_reduce.cu)
+struct SelectPlanArgs {
+  float* A;           // [m_loc] out: A_j
+  int k;              // budget chunks
+  int32_t* ids;       // [k] out: selected ids, ascending
+  int32_t* n_ids;     // [1] out
+  int32_t* ticket;    // [1] zero-initialised grid ticket (reset by the last CTA)
+  int plan;           // also run the demand plan of this layer
+  CacheLayer cl;
+  int epoch;
+  int64_t rec_bytes;
+  int32_t* scratch;
+  PlanOut out;
+};
+bool chunk_sum_select_supported(const LayerGeom& g);
+cudaError_t launch_chunk_sum_select(const LayerGeom& g, const float* lam2, const float* Lam2, float* Apart,
+                                    const SelectPlanArgs& a, cudaStream_t st);
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t* scratch64,
                               int32_t* scratch32, PlanOut out, cudaStream_t st);

@@ -13,8 +13,6 @@ namespace {
 
 constexpr int NT = 1024;
 
-// Keys in registers (KPT per thread, m <= NT * KPT): A_j is summed from the per-KV-head partials
-// once, and the eight radix passes and the compaction run without memory traffic.
 template <int KPT>
 __global__ void __launch_bounds__(NT) topk_scores_kernel(float* __restrict__ A, const float* __restrict__ Apart,
                                                          int nparts, int m, int k, int id_offset,
@@ -23,43 +21,7 @@ __global__ void __launch_bounds__(NT) topk_scores_kernel(float* __restrict__ A, 
   pdl_wait();
   pdl_trigger();
   __shared__ SelectSmem ss;
-  uint64_t key[KPT];
-#pragma unroll
-  for (int u = 0; u < KPT; ++u) {
-    const int j = threadIdx.x + NT * u;
-    key[u] = 0ull;
-    if (j < m) {
-      float a;
-      if (Apart) {  // A_j = sum over KV heads of the chunk-sum partials, fixed order
-        a = 0.f;
-        for (int h = 0; h < nparts; ++h) a += Apart[(size_t)h * m + j];
-        A[j] = a;
-      } else {
-        a = A[j];
-      }
-      key[u] = ((uint64_t)__float_as_uint(a) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j + id_offset));
-    }
-  }
-  const int kk = min(k, m);
-  const uint64_t T = block_kth_largest_regs<NT, KPT>(key, m, kk, ss);
-  // ascending compaction
-  int base = 0;
-#pragma unroll
-  for (int u = 0; u < KPT; ++u) {
-    if (NT * u >= m) break;
-    const int j = threadIdx.x + NT * u;
-    const bool f = (j < m) && key[u] >= T;
-    int tot;
-    const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
-    if (f) {
-      if (ids) ids[base + pos] = j + id_offset;
-      if (cand) cand[base + pos] = key[u];
-    }
-    base += tot;
-  }
-  if (cand)
-    for (int t = kk + threadIdx.x; t < n_cand_out; t += NT) cand[t] = 0ull;
-  if (n_out && threadIdx.x == 0) *n_out = base;
+  topk_body<NT, KPT>(A, Apart, nparts, m, k, id_offset, ids, cand, n_cand_out, n_out, ss);
 }
 
 // Large m (> NT * 8 chunks): keys re-read from A every pass.

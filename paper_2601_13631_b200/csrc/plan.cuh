@@ -1,0 +1,175 @@
+// A4 cache plan (+ fused A9) as a device function of one CTA, shared by the standalone planner
+// kernel (k_cache.cu) and the fused chunk-sum -> top-k -> plan kernel (k_reduce.cu).
+//
+// HBM chunk cache (§4.4, 424-455): per (layer, chunk) the cumulative importance
+// I_j and access count F_j live in a table that survives eviction; the
+// cache score is S_j = I_j * F_j (Eq. 2).  Selected chunks are checked
+// against the cache before loading; misses take free slots first, then the
+// slots of the lowest-(S, j) residents that are neither requested nor pinned by an
+// in-flight prefetch ("Both heaps will evict low-scored ContiguousChunks").
+#pragma once
+#include "common.cuh"
+#include "select.cuh"
+
+namespace ckv {
+
+__device__ __forceinline__ bool bsearch_ids(const int32_t* ids, int n, int j) {
+  int lo = 0, hi = n - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int v = ids[mid];
+    if (v == j) return true;
+    if (v < j) lo = mid + 1; else hi = mid - 1;
+  }
+  return false;
+}
+
+struct PlanSmem {
+  SelectSmem ss;
+  int hits, spec_used;
+};
+
+// The A4 planner (+ fused A9) run by one CTA of NT threads (every thread must call it).
+template <int NT>
+__device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict__ ids, int n_ids, int prefetch,
+                                int quota, int epoch, int64_t rec_bytes, int32_t* __restrict__ scratch,
+                                const PlanOut& out, PlanSmem& ps) {
+  SelectSmem& ss = ps.ss;
+  int& s_hits = ps.hits;
+  int& s_spec_used = ps.spec_used;
+  if (out.epoch_dev) epoch = *out.epoch_dev;
+  int32_t* miss = scratch;            // [n_ids]
+  int32_t* freel = scratch + n_ids;   // [P]
+  int32_t* vict = freel + cl.P;       // [P]
+  int32_t* mpos = vict + cl.P;        // [n_ids]: position in ids of each miss
+  if (threadIdx.x == 0) { s_hits = 0; s_spec_used = 0; }
+  __syncthreads();
+
+  // 1. hit / miss, misses compacted in ascending chunk order.  Hits write their kept slot now;
+  //    a miss's position in ids is kept (mpos) so step 4 writes its slot without another lookup.
+  //    The A9 update is fused here: it touches only requested chunks, which
+  //    are never eviction candidates, so the victims are those of an update after planning.
+  int n_miss = 0;
+  for (int b = 0; b < n_ids; b += NT) {
+    const int t = b + threadIdx.x;
+    bool is_miss = false;
+    int j = -1;
+    if (t < n_ids) {
+      j = ids[t];
+      const int s = cl.slot_of[j];
+      is_miss = s < 0;
+      if (!is_miss) {
+        atomicAdd(&s_hits, 1);
+        if (!prefetch && cl.pf_epoch[s] == epoch) atomicAdd(&s_spec_used, 1);
+      }
+      if (out.kept_slots) out.kept_slots[t] = s;  // misses: -1 until step 4 assigns a slot
+      if (out.ids_out) out.ids_out[t] = j;
+      if (out.upd_A) {
+        cl.I[j] += out.upd_A[j];
+        cl.F[j] += 1;
+        cl.T[j] = epoch;
+      }
+    }
+    int tot;
+    const int pos = block_excl_scan<NT>(is_miss ? 1 : 0, tot, ss);
+    if (is_miss) {
+      miss[n_miss + pos] = j;
+      mpos[n_miss + pos] = t;
+    }
+    n_miss += tot;
+  }
+  if (prefetch) n_miss = min(n_miss, quota);
+  // 2. free slots, ascending (only needed when something is loaded)
+  int n_free = 0;
+  if (n_miss > 0)
+    for (int b = 0; b < cl.P; b += NT) {
+      const int s = b + threadIdx.x;
+      const bool f = s < cl.P && cl.owner[s] < 0;
+      int tot;
+      const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+      if (f) freel[n_free + pos] = s;
+      n_free += tot;
+    }
+  // 3. victims: the `need` lowest (S, j) evictable residents
+  int need = n_miss - n_free;
+  int n_vict = 0;
+  if (need > 0) {
+    auto key = [&](int s) -> uint64_t {
+      const int j = cl.owner[s];
+      if (j < 0) return 0ull;
+      if (bsearch_ids(ids, n_ids, j)) return 0ull;
+      if (!prefetch && cl.pf_epoch[s] == epoch) return 0ull;
+      // Eq. 2 by default; the ablation policies of PAPER.md:610-613
+      const float S = cl.policy == 0 ? cl.I[j] * (float)cl.F[j] : cl.policy == 1 ? (float)cl.F[j] : (float)cl.T[j];
+      return ~(((uint64_t)__float_as_uint(S) << 32) | (uint64_t)(uint32_t)j);
+    };
+    // capacity guard (cannot trigger when P >= k + quota; kept as a loud failure, not a crash)
+    int n_evictable = 0;
+    for (int b = 0; b < cl.P; b += NT) {
+      const int s = b + threadIdx.x;
+      int tot;
+      block_excl_scan<NT>((s < cl.P && key(s) != 0ull) ? 1 : 0, tot, ss);
+      n_evictable += tot;
+    }
+    if (need > n_evictable) {
+      if (threadIdx.x == 0 && out.stats) out.stats[15] = 1;
+      need = n_evictable;
+      n_miss = n_free + need;
+    }
+    const uint64_t T = need > 0 ? block_kth_largest<NT>(key, cl.P, need, ss) : ~0ull;
+    for (int b = 0; b < cl.P; b += NT) {
+      const int s = b + threadIdx.x;
+      uint64_t kv = 0ull;
+      if (s < cl.P) kv = key(s);
+      const bool f = kv != 0ull && kv >= T;
+      int tot;
+      const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+      if (f) vict[n_vict + pos] = s;
+      n_vict += tot;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n_vict; t += NT) {
+      const int s = vict[t];
+      const int j = cl.owner[s];
+      if (out.victims) out.victims[t] = j;
+      cl.slot_of[j] = -1;
+      cl.owner[s] = -1;
+    }
+  }
+  __syncthreads();
+  // 4. assign slots to misses: free slots, then victim slots (both ascending)
+  for (int t = threadIdx.x; t < n_miss; t += NT) {
+    const int s = (t < n_free) ? freel[t] : vict[t - n_free];
+    const int j = miss[t];
+    cl.slot_of[j] = s;
+    cl.owner[s] = j;
+    cl.pf_epoch[s] = prefetch ? epoch : -1;
+    out.gather_list[2 * t] = j;
+    out.gather_list[2 * t + 1] = s;
+    if (out.kept_slots) out.kept_slots[mpos[t]] = out.mark_miss ? -(s + 2) : s;
+  }
+  if (threadIdx.x == 0) {
+    *out.n_load = n_miss;
+    if (out.counts) {
+      out.counts[0] = s_hits;
+      out.counts[1] = n_miss;
+      out.counts[2] = n_vict;
+      out.counts[3] = s_spec_used;
+    }
+    if (out.stats) {
+      unsigned long long* st = reinterpret_cast<unsigned long long*>(out.stats);
+      if (prefetch) {
+        atomicAdd(st + 2, (unsigned long long)n_miss);
+        atomicAdd(st + 5, (unsigned long long)((int64_t)n_miss * rec_bytes));
+      } else {
+        atomicAdd(st + 0, (unsigned long long)s_hits);
+        atomicAdd(st + 1, (unsigned long long)n_miss);
+        atomicAdd(st + 3, (unsigned long long)s_spec_used);
+        atomicAdd(st + 4, (unsigned long long)((int64_t)n_miss * rec_bytes));
+        atomicAdd(st + 6, 1ull);
+      }
+    }
+  }
+}
+
+}  // namespace ckv

@@ -172,4 +172,50 @@ __device__ uint64_t block_kth_largest_regs(const uint64_t (&keys)[KPT], int n, i
   return prefix;
 }
 
+// Keys in registers (KPT per thread, m <= NT * KPT): A_j is summed from the per-KV-head partials
+// once, and the eight radix passes and the compaction run without memory traffic.
+// Apart is read with ld.global.cg: in the fused kernel other CTAs of the same grid wrote it.
+template <int NT, int KPT>
+__device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart, int nparts, int m, int k,
+                          int id_offset, int32_t* __restrict__ ids, uint64_t* __restrict__ cand, int n_cand_out,
+                          int32_t* __restrict__ n_out, SelectSmem& ss) {
+  uint64_t key[KPT];
+#pragma unroll
+  for (int u = 0; u < KPT; ++u) {
+    const int j = threadIdx.x + NT * u;
+    key[u] = 0ull;
+    if (j < m) {
+      float a;
+      if (Apart) {  // A_j = sum over KV heads of the chunk-sum partials, fixed order
+        a = 0.f;
+        for (int h = 0; h < nparts; ++h) a += __ldcg(Apart + (size_t)h * m + j);
+        A[j] = a;
+      } else {
+        a = A[j];
+      }
+      key[u] = ((uint64_t)__float_as_uint(a) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j + id_offset));
+    }
+  }
+  const int kk = min(k, m);
+  const uint64_t T = block_kth_largest_regs<NT, KPT>(key, m, kk, ss);
+  // ascending compaction
+  int base = 0;
+#pragma unroll
+  for (int u = 0; u < KPT; ++u) {
+    if (NT * u >= m) break;
+    const int j = threadIdx.x + NT * u;
+    const bool f = (j < m) && key[u] >= T;
+    int tot;
+    const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+    if (f) {
+      if (ids) ids[base + pos] = j + id_offset;
+      if (cand) cand[base + pos] = key[u];
+    }
+    base += tot;
+  }
+  if (cand)
+    for (int t = kk + threadIdx.x; t < n_cand_out; t += NT) cand[t] = 0ull;
+  if (n_out && threadIdx.x == 0) *n_out = base;
+}
+
 }  // namespace ckv
