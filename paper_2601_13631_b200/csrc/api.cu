@@ -616,7 +616,10 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     int nsplit = 0;
     if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
     LayerGeom g = geom(ctx, n_suffix);
-    if (chunk_sum_select_supported(g)) {
+    // measured on B200 (C3, graph replay): 96.3 us/layer fused vs 92.2 separate (the separate kernels'
+    // launches overlap through PDL; the fused tail runs the same single-CTA work) -> opt-in only
+    static const bool fuse_select = getenv("CKV_FUSED_SELECT") && getenv("CKV_FUSED_SELECT")[0] == '1';
+    if (fuse_select && chunk_sum_select_supported(g)) {
       // A2 chunk sums + A3 top-k (+ A4 plan + A9 when this layer's prefetch is joined) in one launch
       planned = ctx->pf_issued[layer] != ctx->epoch || ctx->pf_joined[layer] == ctx->epoch;
       SelectPlanArgs a{ctx->A, ctx->k, ids, nids, ctx->ticket, planned ? 1 : 0, cache_layer(ctx, layer), ctx->epoch,
