@@ -215,7 +215,40 @@ __global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_par
   for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
   const int64_t obase = ((int64_t)r * g.Hq + h) * g.d;
   const float inv = den > 0.f ? 1.f / den : 0.f;
-  if ((g.d & 127) == 0) {
+  if ((g.d & 127) == 0 && nsplit <= 8) {
+    // all split loads issued before the weighted sum (independent 16-byte loads in flight)
+    for (int x = lane * 4; x < g.d; x += 128) {
+      float4 v[8];
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp)
+        if (sp < nsplit) v[sp] = __ldcg(reinterpret_cast<const float4*>(o_part + (sp * nrow + row) * g.d + x));
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp) {
+        if (sp >= nsplit) break;
+        const float w = __shfl_sync(0xffffffffu, w0, sp);
+        if (w == 0.f) continue;  // empty split (its partial is not written)
+        acc.x += w * v[sp].x;
+        acc.y += w * v[sp].y;
+        acc.z += w * v[sp].z;
+        acc.w += w * v[sp].w;
+      }
+      const float o4[4] = {acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv};
+      if (out) {
+        if constexpr (sizeof(T) == 2) {
+          __nv_bfloat162 b0 = __floats2bfloat162_rn(o4[0], o4[1]), b1 = __floats2bfloat162_rn(o4[2], o4[3]);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&b0);
+          u.y = *reinterpret_cast<uint32_t*>(&b1);
+          *reinterpret_cast<uint2*>(out + obase + x) = u;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) out[obase + x + i] = from_f<T>(o4[i]);
+        }
+      }
+      if (o_f32) *reinterpret_cast<float4*>(o_f32 + obase + x) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+    }
+  } else if ((g.d & 127) == 0) {
     for (int x = lane * 4; x < g.d; x += 128) {
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int sp = 0; sp < nsplit; ++sp) {

@@ -128,7 +128,16 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __re
                                             part * kPartBytes + (key % BN) * 128);
       if (slot >= 0) {
         const uint4* src = reinterpret_cast<const uint4*>(pool + (int64_t)slot * rec_bytes + off);
-        for (int u = lane; u < (int)(piece / 16); u += 32) dst[u] = src[u];
+        const int nu = (int)(piece / 16);
+        for (int u0 = 0; u0 < nu; u0 += 32 * 4) {  // 4 independent 16-byte loads in flight per lane
+          uint4 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (u0 + lane + 32 * q < nu) v[q] = __ldcg(src + u0 + lane + 32 * q);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (u0 + lane + 32 * q < nu) dst[u0 + lane + 32 * q] = v[q];
+        }
       } else {
         const uint4* src = reinterpret_cast<const uint4*>(host_layer + (int64_t)kept_ids[i] * rec_bytes + off);
         uint4* cdst = reinterpret_cast<uint4*>(pool + (int64_t)(-slot - 2) * rec_bytes + off);
