@@ -182,7 +182,7 @@ def run_ckv(args, rank, world):
     ctx = ckv.Context(cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.chunk_size,
                       cfg.prefix_len, cfg.suffix_len, dtype=cfg.dtype, budget_bp=cfg.budget_bp,
                       prefetch_chunks=quota, cache_slots=cache_slots, device=local_rank, shard_index=rank,
-                      num_shards=world)
+                      num_shards=world, flags=ckv.CKV_FLAG_CYCLIC_SHARDS if args.cyclic else 0)
     dt = ctx.torch_dtype
     for l in range(cfg.num_layers):
         kp, vp = make_prefix(cfg, l)
@@ -386,7 +386,7 @@ def run_ckv(args, rank, world):
         "config": {"workload": CFG_NAME, "layers": L, "prefix_len": cfg.prefix_len, "chunk": cfg.chunk_size,
                    "suffix": cfg.suffix_len, "heads": f"{cfg.num_q_heads}/{cfg.num_kv_heads}",
                    "head_dim": cfg.head_dim, "budget_chunks": k, "prefetch_quota": quota,
-                   "requests": N_REQUESTS, "cache_slots_per_layer": cache_slots, "parallelism": f"prefix-shard{world}" if world > 1 else "single",
+                   "requests": N_REQUESTS, "cache_slots_per_layer": cache_slots, "parallelism": (f"prefix-shard{world}" + ("-cyclic" if args.cyclic else "")) if world > 1 else "single",
                    "l2": "inputs larger than L2 (0.94 GB of probe keys streamed per step)",
                    "bytes_per_layer": bpl},
         "roofline": {"kernel": "score_partial (A1)", "bound": "tensor", "achieved": achieved, "peak": peak,
@@ -432,6 +432,8 @@ def main():
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
+    ap.add_argument("--cyclic", action="store_true", help="N > 1: cyclic chunk sharding (j mod N) instead of "
+                    "contiguous ranges (balanced kept chunks, SURVEY §8(f) NEXT-3)")
     ap.add_argument("--quick", action="store_true", help="tuning: print only the warm graph-step time")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--local-gpu", type=int, default=None, help="pin every rank to this GPU (functional runs)")

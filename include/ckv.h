@@ -66,6 +66,8 @@ typedef enum { CKV_NORM_PREFIX = 0, CKV_NORM_FULLROW = 1 } ckv_norm;
 /* cfg.flags */
 #define CKV_FLAG_SIMT_SCORE 0x1u  /* force the SIMT (FFMA) scoring kernel in bf16 mode */
 #define CKV_FLAG_SIMT_ATTN 0x2u   /* force the SIMT attention kernel in bf16 mode */
+#define CKV_FLAG_CYCLIC_SHARDS 0x4u /* num_shards > 1: shard g owns chunks j with j mod W == g (balanced
+                                       sharding) instead of a contiguous range */
 
 typedef struct {
   int32_t num_layers;      /* L >= 1 */
@@ -84,7 +86,8 @@ typedef struct {
   int32_t prefetch_chunks; /* speculative next-layer prefetch quota per layer (chunks); 0 = off */
   int32_t device;          /* CUDA device ordinal */
   int32_t shard_index;     /* position shard owned by this ctx; 0 for one GPU */
-  int32_t num_shards;      /* W >= 1; shard g owns chunks [g*ceil(m/W), min((g+1)*ceil(m/W), m)) */
+  int32_t num_shards;      /* W >= 1; shard g owns chunks [g*ceil(m/W), min((g+1)*ceil(m/W), m)), or
+                              j mod W == g with CKV_FLAG_CYCLIC_SHARDS */
   uint32_t flags;          /* CKV_FLAG_* */
   int32_t period;          /* p >= 1 (0 => 1): layers [P p, (P+1) p) reuse the chunk ids identified at
                               layer P p (Def. 3); the other layers skip A1-A3 and

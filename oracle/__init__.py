@@ -27,6 +27,7 @@ from .ckv_oracle import (  # noqa: F401
     reprefill_layer,
     reprefill_periods,
     sharded_reprefill_layer,
+    shard_chunks,
     coverage_ratio,
 )
 from .cache_model import CacheModel  # noqa: F401

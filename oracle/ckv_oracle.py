@@ -232,10 +232,19 @@ def reprefill_layer(Qs, Ks, Vs, Kp, Vp, c: int, k: int, G: int, norm: int = NORM
             "gap": score_gap(A, k)}
 
 
+def shard_chunks(W: int, g: int, m: int, cyclic: bool = False) -> list[int]:
+    """Chunk ids owned by shard g of W: contiguous [g*ceil(m/W), min((g+1)*ceil(m/W), m)),
+    or cyclic {j : j mod W == g} (the balanced alternative of SURVEY §8(f) NEXT-3), ascending."""
+    if cyclic:
+        return list(range(g, m, W))
+    per = -(-m // W)
+    return list(range(min(g * per, m), min((g + 1) * per, m)))
+
+
 def sharded_reprefill_layer(W: int, Qs, Ks, Vs, Kp, Vp, c: int, k: int, G: int,
-                            norm: int = NORM_PREFIX):
+                            norm: int = NORM_PREFIX, cyclic: bool = False):
     """Position-sharded form of reprefill_layer, written out step by step:
-    shard g owns chunks [g*ceil(m/W), min((g+1)*ceil(m/W), m)).
+    shard g owns the chunks shard_chunks(W, g, m, cyclic) and scores the tokens of those chunks.
       1. shard-local Lambda_g = LSE over the shard's keys; 2. global Lambda = LSE_g Lambda_g
       (+ the causal-suffix term on rank W-1 in FULLROW mode);
       3. shard A_j with the global Lambda; 4. local top-min(k, m_g) candidates -> merged top-k;
@@ -243,16 +252,14 @@ def sharded_reprefill_layer(W: int, Qs, Ks, Vs, Kp, Vp, c: int, k: int, G: int,
     Qs_, Kp_ = _f64(Qs), _f64(Kp)
     n = Kp_.shape[0]
     m = chunk_count(n, c)
-    per = -(-m // W)
-    shards = [(g * per, min((g + 1) * per, m)) for g in range(W)]
+    shards = [shard_chunks(W, g, m, cyclic) for g in range(W)]
     ns, hq, _ = Qs_.shape
     lam_g = []
-    for (j0, j1) in shards:
-        if j1 <= j0:
+    for own in shards:
+        if not own:
             lam_g.append(np.full((hq, ns), -np.inf))
             continue
-        t0, t1 = j0 * c, min(j1 * c, n)
-        lam_g.append(row_lse(Qs_, Kp_[t0:t1], G))
+        lam_g.append(row_lse(Qs_, Kp_[kept_token_index(own, n, c)], G))
     lam = lam_g[0]
     for g in range(1, W):
         lam = np.logaddexp(lam, lam_g[g])
@@ -262,21 +269,25 @@ def sharded_reprefill_layer(W: int, Qs, Ks, Vs, Kp, Vp, c: int, k: int, G: int,
         lam = np.logaddexp(lam, suf.reshape(hq, ns))
     cands = []
     A_full = np.zeros(m)
-    for (j0, j1) in shards:
-        if j1 <= j0:
+    for own in shards:
+        if not own:
             continue
-        t0, t1 = j0 * c, min(j1 * c, n)
-        a_g, _ = token_scores(Qs_, Kp_[t0:t1], G, lam=lam)
-        A_g = chunk_scores(a_g, c)
-        A_full[j0:j1] = A_g
-        loc = select_topk(A_g, min(k, j1 - j0))
-        cands += [(A_g[j], j0 + int(j)) for j in loc]
+        # the shard's chunk scores: Eq. 1 over each owned chunk's own tokens
+        a_g, _ = token_scores(Qs_, Kp_[kept_token_index(own, n, c)], G, lam=lam)
+        A_g, pos = np.zeros(len(own)), 0
+        for t, j in enumerate(own):
+            lo, hi = chunk_range(j, n, c)
+            A_g[t] = a_g[pos:pos + hi - lo].sum()
+            pos += hi - lo
+        A_full[own] = A_g
+        loc = select_topk(A_g, min(k, len(own)))
+        cands += [(A_g[t], own[int(t)]) for t in loc]
     top = sorted(cands, key=lambda t: (-t[0], t[1]))[:k]
     sel = np.array(sorted(j for _, j in top), dtype=np.int64)
     parts = []
-    for g, (j0, j1) in enumerate(shards):
-        own = [j for j in sel if j0 <= j < j1]
-        parts.append(attention(Qs, Ks, Vs, Kp, Vp, kept_token_index(own, n, c), G,
+    for g, own in enumerate(shards):
+        mine = [j for j in sel if j in set(own)]
+        parts.append(attention(Qs, Ks, Vs, Kp, Vp, kept_token_index(mine, n, c), G,
                                include_suffix=(g == W - 1)))
     O, lse = lse_merge(parts)
     return {"ids": sel, "out": O, "lse": lse, "A": A_full, "Lambda": lam}

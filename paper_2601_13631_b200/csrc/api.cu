@@ -28,6 +28,7 @@ struct ckv_ctx {
   int64_t n = 0;
   int m = 0;
   int W = 1, shard = 0, j0 = 0, j1 = 0, m_loc = 0;
+  int cyc_W = 0;  // > 0: cyclic shards (CKV_FLAG_CYCLIC_SHARDS), local chunk t = global t*W + shard
   int64_t t0 = 0;
   int n_loc = 0, n_pad = 0;
   int k = 0, P = 0, quota = 0, max_ns = 0, period = 1, subperiod = 1;
@@ -262,11 +263,13 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
   // a prefetch of this layer that the stream already joined (before the score kernel) needs no
   // further event waits: they would only cut the programmatic launch edges of plan and attention
   const bool pf = ctx->pf_issued[layer] == ctx->epoch && ctx->pf_joined[layer] != ctx->epoch;
+  const bool fused_gather = gather_fused(ctx);
+  // one join per layer: on the fused path the compaction right after the plan needs the prefetched
+  // data anyway, so wait for the whole side-stream load (one cut programmatic edge, not two)
   if (pf) {
-    CK(cudaStreamWaitEvent(st, ctx->ev_pplan[layer], 0));
+    CK(cudaStreamWaitEvent(st, fused_gather ? ctx->ev_pf[layer] : ctx->ev_pplan[layer], 0));
     pdl_mark_event_wait(st);
   }
-  const bool fused_gather = gather_fused(ctx);
   if (!planned) {
     PROF_BEGIN(3);
     LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 0, 0, ctx->epoch, ctx->rec_bytes, nullptr,
@@ -279,7 +282,7 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
                      ctx->rec_bytes, st));
     PROF_END(4);
   }
-  if (pf) {
+  if (pf && !fused_gather) {
     CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
     pdl_mark_event_wait(st);
   }
@@ -398,13 +401,28 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   ctx->m = (int)((c.prefix_len + c.chunk_size - 1) / c.chunk_size);
   ctx->W = c.num_shards;
   ctx->shard = c.shard_index;
-  const int per = (ctx->m + ctx->W - 1) / ctx->W;
-  ctx->j0 = ctx->shard * per < ctx->m ? ctx->shard * per : ctx->m;
-  ctx->j1 = (ctx->shard + 1) * per < ctx->m ? (ctx->shard + 1) * per : ctx->m;
-  ctx->m_loc = ctx->j1 - ctx->j0;
-  ctx->t0 = (int64_t)ctx->j0 * ctx->c;
-  int64_t t1 = (int64_t)ctx->j1 * ctx->c < ctx->n ? (int64_t)ctx->j1 * ctx->c : ctx->n;
-  ctx->n_loc = (int)(t1 - ctx->t0);
+  if ((c.flags & CKV_FLAG_CYCLIC_SHARDS) && ctx->W > 1) {
+    // shard g owns chunks j = t*W + g (SURVEY §8(f) NEXT-3 balanced sharding), packed chunk by chunk;
+    // only the global last chunk can be partial and it is the shard's last local chunk
+    ctx->cyc_W = ctx->W;
+    ctx->m_loc = ctx->shard < ctx->m ? (ctx->m - ctx->shard + ctx->W - 1) / ctx->W : 0;
+    ctx->j0 = ctx->shard;  // the residue (topk_merge ownership test)
+    ctx->j1 = ctx->m;
+    ctx->t0 = 0;
+    if (ctx->m_loc > 0) {
+      const int64_t jl = (int64_t)(ctx->m_loc - 1) * ctx->W + ctx->shard;
+      const int64_t last_len = ((jl + 1) * ctx->c < ctx->n ? (jl + 1) * ctx->c : ctx->n) - jl * ctx->c;
+      ctx->n_loc = (int)((int64_t)(ctx->m_loc - 1) * ctx->c + last_len);
+    }
+  } else {
+    const int per = (ctx->m + ctx->W - 1) / ctx->W;
+    ctx->j0 = ctx->shard * per < ctx->m ? ctx->shard * per : ctx->m;
+    ctx->j1 = (ctx->shard + 1) * per < ctx->m ? (ctx->shard + 1) * per : ctx->m;
+    ctx->m_loc = ctx->j1 - ctx->j0;
+    ctx->t0 = (int64_t)ctx->j0 * ctx->c;
+    int64_t t1 = (int64_t)ctx->j1 * ctx->c < ctx->n ? (int64_t)ctx->j1 * ctx->c : ctx->n;
+    ctx->n_loc = (int)(t1 - ctx->t0);
+  }
   ctx->n_pad = ((ctx->n_loc + 255) / 256 + 1) * 256;
   if (ctx->m_loc < 1) return bad("shard owns no chunk (num_shards > m)");
   ctx->k = c.budget_chunks > 0 ? c.budget_chunks : ckv_budget_chunks(c.prefix_len, c.chunk_size, c.budget_bp);
@@ -555,16 +573,18 @@ ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const vo
   CK(cudaMalloc(&staging, stage_bytes));
   void* probe_l = const_cast<void*>(probe_layer(ctx, layer));
   if (ctx->dtype == CKV_FP32) {
-    LK(launch_pack_probe<float>(static_cast<const float*>(kd), ctx->t0, ctx->n_loc, ctx->n_pad, ctx->Hkv, ctx->d,
-                                static_cast<float*>(probe_l), st));
-    LK(launch_pack_records<float>(static_cast<const float*>(kd), static_cast<const float*>(vd), ctx->t0, ctx->n_loc,
-                                  ctx->m_loc, ctx->c, ctx->Hkv, ctx->d, ctx->rec_swz, static_cast<float*>(staging), st));
+    LK(launch_pack_probe<float>(static_cast<const float*>(kd), ctx->t0, ctx->cyc_W, ctx->shard, ctx->c, ctx->n_loc,
+                                ctx->n_pad, ctx->Hkv, ctx->d, static_cast<float*>(probe_l), st));
+    LK(launch_pack_records<float>(static_cast<const float*>(kd), static_cast<const float*>(vd), ctx->t0, ctx->cyc_W,
+                                  ctx->shard, ctx->n_loc, ctx->m_loc, ctx->c, ctx->Hkv, ctx->d, ctx->rec_swz,
+                                  static_cast<float*>(staging), st));
   } else {
-    LK(launch_pack_probe<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(kd), ctx->t0, ctx->n_loc, ctx->n_pad,
-                                        ctx->Hkv, ctx->d, static_cast<__nv_bfloat16*>(probe_l), st));
+    LK(launch_pack_probe<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(kd), ctx->t0, ctx->cyc_W, ctx->shard,
+                                        ctx->c, ctx->n_loc, ctx->n_pad, ctx->Hkv, ctx->d,
+                                        static_cast<__nv_bfloat16*>(probe_l), st));
     LK(launch_pack_records<__nv_bfloat16>(static_cast<const __nv_bfloat16*>(kd), static_cast<const __nv_bfloat16*>(vd),
-                                          ctx->t0, ctx->n_loc, ctx->m_loc, ctx->c, ctx->Hkv, ctx->d, ctx->rec_swz,
-                                          static_cast<__nv_bfloat16*>(staging), st));
+                                          ctx->t0, ctx->cyc_W, ctx->shard, ctx->n_loc, ctx->m_loc, ctx->c, ctx->Hkv,
+                                          ctx->d, ctx->rec_swz, static_cast<__nv_bfloat16*>(staging), st));
   }
   CK(cudaMemcpyAsync(ctx->host_store + (size_t)layer * stage_bytes, staging, stage_bytes, cudaMemcpyDeviceToHost, st));
   CacheLayer cl = cache_layer(ctx, layer);
@@ -632,7 +652,7 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
       LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
       PROF_END(2);
       PROF_BEGIN(6);
-      LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, ids, nullptr, 0, nids, st));
+      LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, nullptr, 0, nids, st));
       PROF_END(6);
     }
     // intra-period loads (exact ids) for the period's other layers, then the speculative load of
@@ -689,7 +709,8 @@ ckv_status ckv_shard_select(ckv_ctx* ctx, int32_t layer, const void* q, const vo
                                      static_cast<const __nv_bfloat16*>(k_suf), ctx->fullrow, lam_all, ctx->W,
                                      ctx->Lam2, nullptr, st));
   LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
-  LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, ctx->j0, nullptr, cand, ctx->k, nullptr, st));
+  LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, ctx->j0, ctx->cyc_W > 0 ? ctx->cyc_W : 1,
+                        nullptr, cand, ctx->k, nullptr, st));
   if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;
 }
@@ -707,7 +728,7 @@ ckv_status ckv_shard_attend(ckv_ctx* ctx, int32_t layer, const uint64_t* cand_al
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int32_t* ids = ctx->ids_buf[layer & 1];
   int32_t* nids = ctx->n_ids_buf[layer & 1];
-  LK(launch_topk_merge(cand_all, ctx->W * ctx->k, ctx->k, ctx->m, ctx->j0, ctx->j1, ctx->flag, ctx->ids_glob, ids,
+  LK(launch_topk_merge(cand_all, ctx->W * ctx->k, ctx->k, ctx->m, ctx->j0, ctx->j1, ctx->cyc_W, ctx->flag, ctx->ids_glob, ids,
                        nids, st));
   if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st)) != CKV_OK) return s;
   if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, ctx->shard == ctx->W - 1, nullptr, o_part,
@@ -855,7 +876,7 @@ ckv_status ckv_test_topk(ckv_ctx* ctx, const float* A, int32_t m, int32_t k, int
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
   if (!A || !ids || m < 1 || k < 1 || k > m) return fail(ctx, CKV_EINVAL, "bad argument");
-  LK(launch_topk_scores(const_cast<float*>(A), nullptr, 0, m, k, 0, ids, nullptr, 0, nullptr,
+  LK(launch_topk_scores(const_cast<float*>(A), nullptr, 0, m, k, 0, 1, ids, nullptr, 0, nullptr,
                         static_cast<cudaStream_t>(stream)));
   return CKV_OK;
 }

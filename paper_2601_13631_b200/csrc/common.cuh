@@ -134,13 +134,18 @@ cudaError_t launch_chunk_sum(const LayerGeom& g, const float* lam2, const float*
                              cudaStream_t st);  // Apart [Hkv][m_loc]
 // A3
 // A [m] is written first as sum_h Apart[h][j] when Apart != nullptr (else A is the input)
-cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, int k, int id_offset, int32_t* ids,
+cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, int k, int id_offset, int id_mul, int32_t* ids,
                                uint64_t* cand_out, int n_cand_out, int32_t* n_out, cudaStream_t st);
-cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1,
+cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1, int cyc_W,
                               int32_t* flag_scratch, int32_t* ids_glob, int32_t* ids_local,
                               int32_t* n_local, cudaStream_t st);
 cudaError_t launch_block_cover(const int32_t* ids, int n_ids, int u, int B, int64_t n, int32_t* blocks,
                                int32_t* n_blocks, cudaStream_t st);
+// Global prefix token of local token i: contiguous shards t0 + i; cyclic shards (cyc_W > 0) own
+// chunks j = t*cyc_W + cyc_g, packed chunk by chunk.
+__device__ __forceinline__ int64_t shard_token(int64_t i, int64_t t0, int cyc_W, int cyc_g, int c) {
+  return cyc_W > 0 ? ((i / c) * cyc_W + cyc_g) * c + i % c : t0 + i;
+}
 // A4 / A5 / A9
 struct CacheLayer {
   int32_t* slot_of;   // [m_loc]
@@ -192,10 +197,10 @@ cudaError_t launch_cache_update(const CacheLayer& cl, const int32_t* ids, const 
                                 const float* A, int tick, cudaStream_t st);
 // store
 template <typename T>
-cudaError_t launch_pack_probe(const T* k, int64_t t0, int n_loc, int n_pad, int Hkv, int d, T* probe_layer,
+cudaError_t launch_pack_probe(const T* k, int64_t t0, int cyc_W, int cyc_g, int c, int n_loc, int n_pad, int Hkv, int d, T* probe_layer,
                               cudaStream_t st);
 template <typename T>
-cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int n_loc, int m_loc, int c, int Hkv,
+cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int cyc_W, int cyc_g, int n_loc, int m_loc, int c, int Hkv,
                                 int d, int swz, T* staging, cudaStream_t st);
 // A7 / A8
 template <typename T>

@@ -82,8 +82,8 @@ __global__ void cache_update_kernel(CacheLayer cl, const int32_t* __restrict__ i
 }
 
 template <typename T>
-__global__ void pack_probe_kernel(const T* __restrict__ k, int64_t t0, int n_loc, int n_pad, int Hkv, int d,
-                                  T* __restrict__ probe) {
+__global__ void pack_probe_kernel(const T* __restrict__ k, int64_t t0, int cyc_W, int cyc_g, int c, int n_loc,
+                                  int n_pad, int Hkv, int d, T* __restrict__ probe) {
   pdl_wait();
   pdl_trigger();
   // probe[kvh][i][x] = k[t0 + i][kvh][x]
@@ -92,12 +92,13 @@ __global__ void pack_probe_kernel(const T* __restrict__ k, int64_t t0, int n_loc
     const int x = (int)(e % d);
     const int64_t r = e / d;
     const int i = (int)(r % n_loc), kvh = (int)(r / n_loc);
-    probe[((int64_t)kvh * n_pad + i) * d + x] = k[((t0 + i) * Hkv + kvh) * d + x];
+    probe[((int64_t)kvh * n_pad + i) * d + x] = k[(shard_token(i, t0, cyc_W, cyc_g, c) * Hkv + kvh) * d + x];
   }
 }
 
 template <typename T>
-__global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t t0, int n_loc,
+__global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict__ v, int64_t t0, int cyc_W,
+                                    int cyc_g, int n_loc,
                                     int m_loc, int c, int Hkv, int d, int swz, T* __restrict__ rec) {
   pdl_wait();
   pdl_trigger();
@@ -113,7 +114,7 @@ __global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict
     const int kv = (int)(r / Hkv);
     const int64_t i = (int64_t)j * c + p;
     T val = from_f<T>(0.f);
-    if (i < n_loc) val = (kv == 0 ? k : v)[((t0 + i) * Hkv + kvh) * d + x];
+    if (i < n_loc) val = (kv == 0 ? k : v)[(shard_token(i, t0, cyc_W, cyc_g, c) * Hkv + kvh) * d + x];
     rec[(int64_t)j * per + rec_elem(swz, kv, kvh, p, x, Hkv, c, d)] = val;
   }
 }
@@ -150,23 +151,26 @@ cudaError_t launch_cache_update(const CacheLayer& cl, const int32_t* ids, const 
 }
 
 template <typename T>
-cudaError_t launch_pack_probe(const T* k, int64_t t0, int n_loc, int n_pad, int Hkv, int d, T* probe_layer,
-                              cudaStream_t st) {
-  if (cudaError_t e_ = launch_kernel(pack_probe_kernel<T>, 1184, 256, 0, st, k, t0, n_loc, n_pad, Hkv, d, probe_layer)) return e_;
+cudaError_t launch_pack_probe(const T* k, int64_t t0, int cyc_W, int cyc_g, int c, int n_loc, int n_pad, int Hkv, int d,
+                              T* probe_layer, cudaStream_t st) {
+  if (cudaError_t e_ = launch_kernel(pack_probe_kernel<T>, 1184, 256, 0, st, k, t0, cyc_W, cyc_g, c, n_loc, n_pad, Hkv, d,
+                                     probe_layer)) return e_;
   return cudaGetLastError();
 }
 template <typename T>
-cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int n_loc, int m_loc, int c, int Hkv, int d,
-                                int swz, T* staging, cudaStream_t st) {
-  if (cudaError_t e_ = launch_kernel(pack_records_kernel<T>, 1184, 256, 0, st, k, v, t0, n_loc, m_loc, c, Hkv, d, swz, staging)) return e_;
+cudaError_t launch_pack_records(const T* k, const T* v, int64_t t0, int cyc_W, int cyc_g, int n_loc, int m_loc, int c,
+                                int Hkv, int d, int swz, T* staging, cudaStream_t st) {
+  if (cudaError_t e_ = launch_kernel(pack_records_kernel<T>, 1184, 256, 0, st, k, v, t0, cyc_W, cyc_g, n_loc, m_loc, c, Hkv,
+                                     d, swz, staging)) return e_;
   return cudaGetLastError();
 }
-template cudaError_t launch_pack_probe<float>(const float*, int64_t, int, int, int, int, float*, cudaStream_t);
-template cudaError_t launch_pack_probe<__nv_bfloat16>(const __nv_bfloat16*, int64_t, int, int, int, int,
+template cudaError_t launch_pack_probe<float>(const float*, int64_t, int, int, int, int, int, int, int, float*,
+                                              cudaStream_t);
+template cudaError_t launch_pack_probe<__nv_bfloat16>(const __nv_bfloat16*, int64_t, int, int, int, int, int, int, int,
                                                       __nv_bfloat16*, cudaStream_t);
-template cudaError_t launch_pack_records<float>(const float*, const float*, int64_t, int, int, int, int, int, int,
-                                                float*, cudaStream_t);
-template cudaError_t launch_pack_records<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, int64_t, int,
-                                                        int, int, int, int, int, __nv_bfloat16*, cudaStream_t);
+template cudaError_t launch_pack_records<float>(const float*, const float*, int64_t, int, int, int, int, int, int, int,
+                                                int, float*, cudaStream_t);
+template cudaError_t launch_pack_records<__nv_bfloat16>(const __nv_bfloat16*, const __nv_bfloat16*, int64_t, int, int,
+                                                        int, int, int, int, int, int, __nv_bfloat16*, cudaStream_t);
 
 }  // namespace ckv

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(1024) chunk_sum_select_kernel(LayerGeom g, con
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  topk_body<1024, KPT>(a.A, Apart, g.Hkv, g.m_loc, a.k, 0, a.ids, nullptr, 0, a.n_ids, ps.ss);
+  topk_body<1024, KPT>(a.A, Apart, g.Hkv, g.m_loc, a.k, 0, 1, a.ids, nullptr, 0, a.n_ids, ps.ss);
   __syncthreads();
   if (threadIdx.x == 0) *a.ticket = 0;  // ready for the next launch (stream-ordered)
   if (a.plan)

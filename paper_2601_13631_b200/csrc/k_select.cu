@@ -15,18 +15,18 @@ constexpr int NT = 1024;
 
 template <int KPT>
 __global__ void __launch_bounds__(NT) topk_scores_kernel(float* __restrict__ A, const float* __restrict__ Apart,
-                                                         int nparts, int m, int k, int id_offset,
+                                                         int nparts, int m, int k, int id_offset, int id_mul,
                                                          int32_t* __restrict__ ids, uint64_t* __restrict__ cand,
                                                          int n_cand_out, int32_t* __restrict__ n_out) {
   pdl_wait();
   pdl_trigger();
   __shared__ SelectSmem ss;
-  topk_body<NT, KPT>(A, Apart, nparts, m, k, id_offset, ids, cand, n_cand_out, n_out, ss);
+  topk_body<NT, KPT>(A, Apart, nparts, m, k, id_offset, id_mul, ids, cand, n_cand_out, n_out, ss);
 }
 
 // Large m (> NT * 8 chunks): keys re-read from A every pass.
 __global__ void __launch_bounds__(NT) topk_scores_big_kernel(float* __restrict__ A, const float* __restrict__ Apart,
-                                                             int nparts, int m, int k, int id_offset,
+                                                             int nparts, int m, int k, int id_offset, int id_mul,
                                                              int32_t* __restrict__ ids, uint64_t* __restrict__ cand,
                                                              int n_cand_out, int32_t* __restrict__ n_out) {
   pdl_wait();
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(NT) topk_scores_big_kernel(float* __restrict__
     __syncthreads();
   }
   auto key = [&](int j) -> uint64_t {
-    return ((uint64_t)__float_as_uint(A[j]) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j + id_offset));
+    return ((uint64_t)__float_as_uint(A[j]) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j * id_mul + id_offset));
   };
   const int kk = min(k, m);
   const uint64_t T = block_kth_largest<NT>(key, m, kk, ss);
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(NT) topk_scores_big_kernel(float* __restrict__
     int tot;
     const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
     if (f) {
-      if (ids) ids[base + pos] = j + id_offset;
+      if (ids) ids[base + pos] = j * id_mul + id_offset;
       if (cand) cand[base + pos] = key(j);
     }
     base += tot;
@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(NT) topk_scores_big_kernel(float* __restrict__
 // Global top-k over the gathered candidates of all shards; ids_glob ascending (identical
 // on every rank), ids_local = the selected ids this shard owns, as local chunk indices.
 __global__ void __launch_bounds__(NT) topk_merge_kernel(const uint64_t* __restrict__ cand_all, int n_cand, int k,
-                                                        int m_glob, int j0, int j1, int32_t* __restrict__ flag,
+                                                        int m_glob, int j0, int j1, int cyc_W,
+                                                        int32_t* __restrict__ flag,
                                                         int32_t* __restrict__ ids_glob, int32_t* __restrict__ ids_local,
                                                         int32_t* __restrict__ n_local) {
   pdl_wait();
@@ -88,10 +89,11 @@ __global__ void __launch_bounds__(NT) topk_merge_kernel(const uint64_t* __restri
     const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
     if (f) ids_glob[base + pos] = j;
     base += tot;
-    const bool fl = f && j >= j0 && j < j1;
+    // owned by this shard: [j0, j1) (contiguous) or j % cyc_W == j0 (cyclic; local id j / cyc_W)
+    const bool fl = f && (cyc_W > 0 ? (j % cyc_W) == j0 : (j >= j0 && j < j1));
     int ltot;
     const int lpos = block_excl_scan<NT>(fl ? 1 : 0, ltot, ss);
-    if (fl) ids_local[lbase + lpos] = j - j0;
+    if (fl) ids_local[lbase + lpos] = cyc_W > 0 ? j / cyc_W : j - j0;
     lbase += ltot;
   }
   if (threadIdx.x == 0) *n_local = lbase;
@@ -134,27 +136,27 @@ cudaError_t launch_block_cover(const int32_t* ids, int n_ids, int u, int B, int6
   return cudaGetLastError();
 }
 
-cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, int k, int id_offset, int32_t* ids,
+cudaError_t launch_topk_scores(float* A, const float* Apart, int nparts, int m, int k, int id_offset, int id_mul, int32_t* ids,
                                uint64_t* cand_out, int n_cand_out, int32_t* n_out, cudaStream_t st) {
   cudaError_t e_;
   if (m <= NT)
-    e_ = launch_kernel(topk_scores_kernel<1>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+    e_ = launch_kernel(topk_scores_kernel<1>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, id_mul, ids, cand_out, n_cand_out, n_out);
   else if (m <= 2 * NT)
-    e_ = launch_kernel(topk_scores_kernel<2>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+    e_ = launch_kernel(topk_scores_kernel<2>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, id_mul, ids, cand_out, n_cand_out, n_out);
   else if (m <= 4 * NT)
-    e_ = launch_kernel(topk_scores_kernel<4>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+    e_ = launch_kernel(topk_scores_kernel<4>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, id_mul, ids, cand_out, n_cand_out, n_out);
   else if (m <= 8 * NT)
-    e_ = launch_kernel(topk_scores_kernel<8>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+    e_ = launch_kernel(topk_scores_kernel<8>, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, id_mul, ids, cand_out, n_cand_out, n_out);
   else
-    e_ = launch_kernel(topk_scores_big_kernel, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, ids, cand_out, n_cand_out, n_out);
+    e_ = launch_kernel(topk_scores_big_kernel, 1, NT, 0, st, A, Apart, nparts, m, k, id_offset, id_mul, ids, cand_out, n_cand_out, n_out);
   if (e_) return e_;
   return cudaGetLastError();
 }
 
-cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1,
+cudaError_t launch_topk_merge(const uint64_t* cand_all, int n_cand, int k, int m_glob, int j0, int j1, int cyc_W,
                               int32_t* flag_scratch, int32_t* ids_glob, int32_t* ids_local, int32_t* n_local,
                               cudaStream_t st) {
-  if (cudaError_t e_ = launch_kernel(topk_merge_kernel, 1, NT, 0, st, cand_all, n_cand, k, m_glob, j0, j1, flag_scratch, ids_glob, ids_local,
+  if (cudaError_t e_ = launch_kernel(topk_merge_kernel, 1, NT, 0, st, cand_all, n_cand, k, m_glob, j0, j1, cyc_W, flag_scratch, ids_glob, ids_local,
                                       n_local)) return e_;
   return cudaGetLastError();
 }

@@ -177,7 +177,7 @@ __device__ uint64_t block_kth_largest_regs(const uint64_t (&keys)[KPT], int n, i
 // Apart is read with ld.global.cg: in the fused kernel other CTAs of the same grid wrote it.
 template <int NT, int KPT>
 __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart, int nparts, int m, int k,
-                          int id_offset, int32_t* __restrict__ ids, uint64_t* __restrict__ cand, int n_cand_out,
+                          int id_offset, int id_mul, int32_t* __restrict__ ids, uint64_t* __restrict__ cand, int n_cand_out,
                           int32_t* __restrict__ n_out, SelectSmem& ss) {
   uint64_t key[KPT];
 #pragma unroll
@@ -193,7 +193,7 @@ __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart
       } else {
         a = A[j];
       }
-      key[u] = ((uint64_t)__float_as_uint(a) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j + id_offset));
+      key[u] = ((uint64_t)__float_as_uint(a) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j * id_mul + id_offset));
     }
   }
   const int kk = min(k, m);
@@ -208,7 +208,7 @@ __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart
     int tot;
     const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
     if (f) {
-      if (ids) ids[base + pos] = j + id_offset;
+      if (ids) ids[base + pos] = j * id_mul + id_offset;
       if (cand) cand[base + pos] = key[u];
     }
     base += tot;

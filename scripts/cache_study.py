@@ -33,8 +33,14 @@ def main():
     ap.add_argument("--draws", type=int, default=48)
     ap.add_argument("--requests", type=int, default=16)
     ap.add_argument("--budgets", default="1000,2500")
+    ap.add_argument("--config", default="c3_7b", help="synth config (c5_32b: the shared-prefix C5 shape)")
+    ap.add_argument("--layers", type=int, default=0, help="run only the first L layers (per-layer cache "
+                    "partitions make layers independent; 0 = all)")
+    ap.add_argument("--slots", default="1.25,1.5,2,3", help="HBM slots per layer as multiples of k")
     args = ap.parse_args()
-    base = CONFIGS["c3_7b"]
+    base = CONFIGS[args.config]
+    if args.layers:
+        base = base.replace(num_layers=args.layers)
     L, dev = base.num_layers, torch.device("cuda", 0)
     prefix = []
     for l in range(L):
@@ -53,7 +59,8 @@ def main():
     for bp in [int(b) for b in args.budgets.split(",")]:
         k = ckv_budget_chunks(base.prefix_len, base.chunk_size, bp)
         ids = [torch.empty(k, dtype=torch.int32, device=dev) for _ in range(L)]
-        for P, prefetch in [(P, pf) for P in (k * 5 // 4, k * 3 // 2, 2 * k, 3 * k) for pf in (True, False)]:
+        mults = [float(x) for x in args.slots.split(",")]
+        for P, prefetch in [(int(k * f), pf) for f in mults for pf in (True, False)]:
             quota = min(k, P - k) if prefetch else 0
             ctx = Context(L, base.num_q_heads, base.num_kv_heads, base.head_dim, base.chunk_size, base.prefix_len,
                           base.suffix_len, dtype="bf16", budget_bp=bp, prefetch_chunks=quota, cache_slots=P)
@@ -88,8 +95,8 @@ def main():
             ctx.close()
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out, "w") as f:
-        json.dump({"workload": "c3_7b shape, R=%d requests, %d Zipf(1) draws (first %d warm-up), seed 42"
-                   % (R, args.draws, warm), "draws": draws, "rows": results}, f, indent=1)
+        json.dump({"workload": f"{args.config} shape ({L} layers), R={R} requests, {args.draws} Zipf(1) draws "
+                               f"(first {warm} warm-up), seed 42", "draws": draws, "rows": results}, f, indent=1)
 
 
 if __name__ == "__main__":

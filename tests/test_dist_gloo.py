@@ -23,18 +23,17 @@ from paper_2601_13631_b200.sharded import ShardedReprefill
 class OracleShard:
     """CPU stand-in for one libckv shard context (test infrastructure)."""
 
-    def __init__(self, Kp, Vp, c, k, G, shard, W):
+    def __init__(self, Kp, Vp, c, k, G, shard, W, cyclic=False):
         self.Kp, self.Vp, self.c, self.k, self.G, self.W = Kp, Vp, c, k, G, W
         n = Kp.shape[0]
         self.m = O.chunk_count(n, c)
-        per = -(-self.m // W)
-        self.j0, self.j1 = min(shard * per, self.m), min((shard + 1) * per, self.m)
-        self.t0, self.t1 = self.j0 * c, min(self.j1 * c, n)
+        self.own = O.shard_chunks(W, shard, self.m, cyclic)       # owned global chunk ids, ascending
+        self.tok = O.kept_token_index(self.own, n, c)              # their prefix tokens
         self.shard = shard
 
     def shard_score(self, layer, q, k_suf, lam_local):
         qs = q.double().numpy()
-        lam = O.row_lse(qs, self.Kp[self.t0:self.t1], self.G)            # [Hq, ns] natural log
+        lam = O.row_lse(qs, self.Kp[self.tok], self.G)                  # [Hq, ns] natural log
         lam_local.copy_(torch.from_numpy(lam.reshape(-1) / np.log(2.0)))  # base 2, index h*ns + r
 
     def shard_select(self, layer, q, k_suf, lam_all, cand):
@@ -43,10 +42,13 @@ class OracleShard:
         lam2 = lam_all.double().numpy().reshape(self.W, hq * ns)
         mx = lam2.max(0)
         glob = (mx + np.log2(np.exp2(lam2 - mx).sum(0))) * np.log(2.0)
-        a, _ = O.token_scores(qs, self.Kp[self.t0:self.t1], self.G, lam=glob.reshape(hq, ns))
-        A = O.chunk_scores(a, self.c).astype(np.float32)
-        loc = O.select_topk(A.astype(np.float64), min(self.k, self.j1 - self.j0))
-        keys = [(int(np.float32(A[j]).view(np.uint32)) << 32) | (0xFFFFFFFF - (self.j0 + int(j))) for j in loc]
+        a, _ = O.token_scores(qs, self.Kp[self.tok], self.G, lam=glob.reshape(hq, ns))
+        # Eq. 1 per owned chunk (each owned chunk's tokens are consecutive in self.tok)
+        lens = [O.chunk_range(j, self.Kp.shape[0], self.c)[1] - O.chunk_range(j, self.Kp.shape[0], self.c)[0]
+                for j in self.own]
+        A = np.add.reduceat(a, np.cumsum([0] + lens[:-1])).astype(np.float32)
+        loc = O.select_topk(A.astype(np.float64), min(self.k, len(self.own)))
+        keys = [(int(np.float32(A[j]).view(np.uint32)) << 32) | (0xFFFFFFFF - self.own[int(j)]) for j in loc]
         keys += [0] * (self.k - len(keys))
         cand.copy_(torch.tensor(np.array(keys, dtype=np.uint64).view(np.int64)))
 
@@ -54,7 +56,7 @@ class OracleShard:
         keys = cand_all.numpy().view(np.uint64)
         top = sorted((int(x) for x in keys if x != 0), reverse=True)[: self.k]
         sel = sorted(0xFFFFFFFF - (x & 0xFFFFFFFF) for x in top)
-        own = [j for j in sel if self.j0 <= j < self.j1]
+        own = [j for j in sel if j in set(self.own)]
         O_, lse = O.attention(q.double().numpy(), k_suf.double().numpy(), v_suf.double().numpy(), self.Kp, self.Vp,
                               O.kept_token_index(own, self.Kp.shape[0], self.c), self.G,
                               include_suffix=self.shard == self.W - 1)
@@ -82,14 +84,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, W, port, ret):
+def _worker(rank, W, port, ret, cyclic):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=W)
     g = np.random.default_rng(0)
     n, c, ns, hq, hkv, d, k = 203, 8, 5, 4, 2, 16, 6
     Qs, Ks, Vs = g.standard_normal((ns, hq, d)) * 2, g.standard_normal((ns, hkv, d)), g.standard_normal((ns, hkv, d))
     Kp, Vp = g.standard_normal((n, hkv, d)), g.standard_normal((n, hkv, d))
-    shard = OracleShard(Kp, Vp, c, k, hq // hkv, rank, W)
+    shard = OracleShard(Kp, Vp, c, k, hq // hkv, rank, W, cyclic)
     runner = ShardedReprefill(shard)
     q, ks, vs = (torch.from_numpy(x).float() for x in (Qs, Ks, Vs))
     # float32 buffers in the runner; the stand-in computes in fp64 from them
@@ -100,12 +102,12 @@ def _worker(rank, W, port, ret):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("W", [2])
-def test_sharded_protocol_gloo(W):
+@pytest.mark.parametrize("W,cyclic", [(2, False), (2, True)])
+def test_sharded_protocol_gloo(W, cyclic):
     port = _free_port()
     mgr = mp.Manager()
     ret = mgr.dict()
-    mp.spawn(_worker, args=(W, port, ret), nprocs=W, join=True)
+    mp.spawn(_worker, args=(W, port, ret, cyclic), nprocs=W, join=True)
     for r in range(W):
         got, want, err = ret[r]
         assert got == want

@@ -8,7 +8,7 @@ import pytest
 import torch
 
 import oracle as O
-from paper_2601_13631_b200 import CKV_FLAG_SIMT_SCORE, CkvError, Context
+from paper_2601_13631_b200 import CKV_FLAG_CYCLIC_SHARDS, CKV_FLAG_SIMT_SCORE, CkvError, Context
 from synth import CONFIGS, ShapeConfig, make_prefix, make_request
 from tests.gpu_util import check_layer, make_ctx, run_layers, to_dev
 
@@ -267,11 +267,13 @@ def test_cache_plan_matches_model(policy):
 
 
 # ---------------------------------------------------------------- sharded (logical, 1 GPU)
-@pytest.mark.parametrize("W", [2, 3, 4])
-def test_sharded_logical_on_one_gpu(W):
-    cfg = ShapeConfig("sh", 2, 8, 2, 128, 4000, 16, 10, 1000, "bf16")
+@pytest.mark.parametrize("W,cyclic,n", [(2, False, 4000), (3, False, 4000), (4, False, 4000), (2, True, 4000),
+                                         (3, True, 4000), (3, True, 3990)])
+def test_sharded_logical_on_one_gpu(W, cyclic, n):
+    cfg = ShapeConfig("sh", 2, 8, 2, 128, n, 16, 10, 1000, "bf16")
     k = _k(cfg)
-    ctxs = [make_ctx(cfg, shard=g, W=W, prefetch=k // 2)[0] for g in range(W)]
+    flags = CKV_FLAG_CYCLIC_SHARDS if cyclic else 0
+    ctxs = [make_ctx(cfg, shard=g, W=W, prefetch=k // 2, flags=flags)[0] for g in range(W)]
     for l in range(cfg.num_layers):
         kp, vp = make_prefix(cfg, l)
         qs, ks, vs = make_request(cfg, l, 0)

@@ -233,15 +233,26 @@ def test_split_merge_identity():
 
 @pytest.mark.parametrize("W", [2, 3, 4, 8])
 @pytest.mark.parametrize("norm", [O.NORM_PREFIX, O.NORM_FULLROW])
-def test_sharding_identity(W, norm):
+@pytest.mark.parametrize("cyclic", [False, True])
+def test_sharding_identity(W, norm, cyclic):
     Qs, Ks, Vs, Kp, Vp = rand_case(13, n=200, c=8, ns=4, hq=4, hkv=2, d=8, scale=2.5)
     k = 6
     ref = O.reprefill_layer(Qs, Ks, Vs, Kp, Vp, c=8, k=k, G=2, norm=norm)
-    sh = O.sharded_reprefill_layer(W, Qs, Ks, Vs, Kp, Vp, c=8, k=k, G=2, norm=norm)
+    sh = O.sharded_reprefill_layer(W, Qs, Ks, Vs, Kp, Vp, c=8, k=k, G=2, norm=norm, cyclic=cyclic)
     assert sh["ids"].tolist() == ref["ids"].tolist()
     np.testing.assert_allclose(sh["A"], ref["A"], rtol=1e-11)
     np.testing.assert_allclose(sh["Lambda"], ref["Lambda"], rtol=1e-13)
     np.testing.assert_allclose(sh["out"], ref["out"], atol=1e-12)
+
+
+def test_shard_chunks_partition():
+    for m in (1, 7, 64, 101):
+        for W in (1, 2, 3, 8):
+            for cyc in (False, True):
+                parts = [O.shard_chunks(W, g, m, cyc) for g in range(W)]
+                assert sorted(j for p in parts for j in p) == list(range(m))  # a partition of the chunks
+                assert all(p == sorted(p) for p in parts)
+            assert O.shard_chunks(W, 1 % W, m, True) == [j for j in range(m) if j % W == 1 % W]
 
 
 # ------------------------------------------------------------ brute force
