@@ -111,6 +111,16 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def mufu_roofline(cfg, world, score_avg_ms, clocks):
+    """A1's binding roofline: exp2 throughput (algorithmic exps = Hq * n_s * n per layer)."""
+    exps = cfg.num_q_heads * cfg.suffix_len * (cfg.prefix_len / world)
+    mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    peak = 16 * 148 * mhz * 1e6 / 1e12  # Tex2/s: MUFU ex2 16/clk/SM (B300_MICROARCH, measured scripts/mufu_bench.cu)
+    achieved = exps / (score_avg_ms * 1e-3) / 1e12
+    return {"bound": "alu", "unit": "Tex2/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+            "algorithmic": f"{exps:.4g} exp2 per launch", "sm_mhz": mhz}
+
+
 # ------------------------------------------------------------------ reference arm (the oracle)
 def cpu_cores():
     try:
@@ -394,7 +404,10 @@ def run_ckv(args, rank, world):
                      "peak_source": f"{peak_src} bf16_tflops_sustained", "score_kernel_kind":
                          ["simt", "tcgen05"][ctx.score_kernel_kind], "avg_launch_ms": score_avg,
                      "hbm_achieved_gbs": (cfg.prefix_len / world) * cfg.num_kv_heads * cfg.head_dim * 2
-                     / (score_avg * 1e-3) / 1e9},
+                     / (score_avg * 1e-3) / 1e9,
+                     # the roofline that binds A1 first: one exp2 per logit on the MUFU pipe,
+                     # 16 ex2/clk/SM x 148 SMs at the SM clock sampled during the timed region
+                     "binding": mufu_roofline(cfg, world, score_avg, clk.summary())},
         "stage_ms_per_step": step_stage_ms, "profiled_ms_per_step": ms_prof / args.steps,
         "cache": {"hit_rate": stats["total_hits"] / max(stats["total_hits"] + stats["total_misses"], 1),
                   "misses_per_layer": stats["total_misses"] / n_lay,
