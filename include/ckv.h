@@ -68,6 +68,9 @@ typedef enum { CKV_NORM_PREFIX = 0, CKV_NORM_FULLROW = 1 } ckv_norm;
 #define CKV_FLAG_SIMT_ATTN 0x2u   /* force the SIMT attention kernel in bf16 mode */
 #define CKV_FLAG_CYCLIC_SHARDS 0x4u /* num_shards > 1: shard g owns chunks j with j mod W == g (balanced
                                        sharding) instead of a contiguous range */
+#define CKV_FLAG_GLOBAL_HEAP 0x8u   /* one HBM chunk cache of L * cache_slots slots shared by every layer
+                                       ("a single global GPU heap"): victims are the lowest
+                                       (S, layer, chunk) residents of any layer; default: per-layer pools */
 
 typedef struct {
   int32_t num_layers;      /* L >= 1 */
@@ -82,7 +85,7 @@ typedef struct {
   int32_t budget_bp;       /* budget ratio in basis points 1..10000 (used iff budget_chunks == 0) */
   int32_t score_norm;      /* ckv_norm */
   int32_t cache_slots;     /* HBM chunk-cache slots per layer (P); 0 => 2k + prefetch_chunks;
-                              must be >= k + prefetch_chunks */
+                              must be >= k + prefetch_chunks (global heap: the pool holds L * P) */
   int32_t prefetch_chunks; /* speculative next-layer prefetch quota per layer (chunks); 0 = off */
   int32_t device;          /* CUDA device ordinal */
   int32_t shard_index;     /* position shard owned by this ctx; 0 for one GPU */
@@ -248,7 +251,8 @@ ckv_status ckv_load_chunks(ckv_ctx* ctx, int32_t layer, const int32_t* ids, int3
  *   ascending ids[k] (device int32); prefetch != 0 plans a speculative load (quota
  *   cfg.prefetch_chunks) instead of a demand load; when A (device float [m_local])
  *   is non-NULL the A9 update I += A, F += 1 follows.  loads (device int32
- *   [2*k]: chunk, slot pairs in ascending chunk order) and counts (device int32 [4]:
+ *   [2*k]: chunk, slot pairs in ascending chunk order), victims (device int32 [k]: evicted
+ *   entries as table indices layer * m_local + chunk) and counts (device int32 [4]:
  *   hits, loads, victims, 0) are written; no data is copied. */
 ckv_status ckv_test_topk(ckv_ctx* ctx, const float* A, int32_t m, int32_t k, int32_t* ids,
                          void* stream);

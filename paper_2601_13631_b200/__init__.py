@@ -7,6 +7,7 @@ build (build.py) and the multi-GPU orchestration over torch.distributed
 """
 from .ckv import (  # noqa: F401
     CKV_FLAG_CYCLIC_SHARDS,
+    CKV_FLAG_GLOBAL_HEAP,
     CKV_FLAG_SIMT_ATTN,
     CKV_FLAG_SIMT_SCORE,
     CKV_NORM_FULLROW,

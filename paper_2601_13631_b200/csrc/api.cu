@@ -44,6 +44,7 @@ struct ckv_ctx {
   char* pool = nullptr;
   int32_t *slot_of = nullptr, *owner = nullptr, *pf_epoch = nullptr, *F = nullptr, *T = nullptr;
   int cache_policy = 0;  // ckv_cache_policy
+  bool global_heap = false;  // CKV_FLAG_GLOBAL_HEAP: one pool of L * P slots shared by all layers
   float* I = nullptr;
   float *lam2 = nullptr, *lampart = nullptr, *Lam2 = nullptr, *A = nullptr, *Apart = nullptr;
   int32_t* ids_buf[2] = {nullptr, nullptr};
@@ -168,13 +169,19 @@ int attn_nsplit(const ckv_ctx* ctx, int ns, int n_kept_cap) {
 CacheLayer cache_layer(const ckv_ctx* ctx, int layer) {
   CacheLayer cl;
   cl.slot_of = ctx->slot_of + (size_t)layer * ctx->m_loc;
-  cl.owner = ctx->owner + (size_t)layer * ctx->P;
-  cl.pf_epoch = ctx->pf_epoch + (size_t)layer * ctx->P;
+  const size_t pool_off = ctx->global_heap ? 0 : (size_t)layer * ctx->P;
+  cl.owner = ctx->owner + pool_off;
+  cl.pf_epoch = ctx->pf_epoch + pool_off;
+  cl.slot_of0 = ctx->slot_of;
+  cl.I0 = ctx->I;
+  cl.F0 = ctx->F;
+  cl.T0 = ctx->T;
+  cl.lbase = layer * ctx->m_loc;
   cl.I = ctx->I + (size_t)layer * ctx->m_loc;
   cl.F = ctx->F + (size_t)layer * ctx->m_loc;
   cl.T = ctx->T + (size_t)layer * ctx->m_loc;
   cl.m_loc = ctx->m_loc;
-  cl.P = ctx->P;
+  cl.P = ctx->global_heap ? ctx->L * ctx->P : ctx->P;
   cl.policy = ctx->cache_policy;
   return cl;
 }
@@ -182,7 +189,10 @@ CacheLayer cache_layer(const ckv_ctx* ctx, int layer) {
 const char* host_layer_dev(const ckv_ctx* ctx, int layer) {
   return ctx->host_store_dev + (size_t)layer * ctx->m_loc * ctx->rec_bytes;
 }
-char* pool_layer(const ckv_ctx* ctx, int layer) { return ctx->pool + (size_t)layer * ctx->P * ctx->rec_bytes; }
+// slot s of `layer` (per-layer pools) or of the shared pool (global heap: slots are pool-wide)
+char* pool_layer(const ckv_ctx* ctx, int layer) {
+  return ctx->global_heap ? ctx->pool : ctx->pool + (size_t)layer * ctx->P * ctx->rec_bytes;
+}
 const void* probe_layer(const ckv_ctx* ctx, int layer) {
   return static_cast<const char*>(ctx->probe) + (size_t)layer * ctx->Hkv * ctx->n_pad * ctx->d * ctx->esz;
 }
@@ -430,6 +440,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   ctx->quota = c.prefetch_chunks < 0 ? 0 : (c.prefetch_chunks > ctx->k ? ctx->k : c.prefetch_chunks);
   ctx->P = c.cache_slots > 0 ? c.cache_slots : 2 * ctx->k + ctx->quota;
   if (ctx->P < ctx->k + ctx->quota) return bad("cache_slots < k + prefetch_chunks");
+  ctx->global_heap = (c.flags & CKV_FLAG_GLOBAL_HEAP) != 0;
   ctx->max_ns = c.max_suffix_len;
   ctx->period = c.period > 0 ? c.period : 1;
   ctx->subperiod = c.subperiod > 0 ? c.subperiod : 1;
@@ -490,8 +501,9 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   CKC(dalloc(&ctx->kept_slots, (size_t)ctx->k));
   CKC(dalloc(&ctx->ids_glob, (size_t)ctx->k));
   CKC(dalloc(&ctx->flag, (size_t)ctx->m));
-  CKC(dalloc(&ctx->scratch_main, (size_t)2 * ctx->k + 2 * ctx->P));
-  CKC(dalloc(&ctx->scratch_side, (size_t)2 * ctx->k + 2 * ctx->P));
+  const size_t pool_slots = ctx->global_heap ? (size_t)ctx->L * ctx->P : (size_t)ctx->P;
+  CKC(dalloc(&ctx->scratch_main, (size_t)2 * ctx->k + 2 * pool_slots));
+  CKC(dalloc(&ctx->scratch_side, (size_t)2 * ctx->k + 2 * pool_slots));
   CKC(dalloc(&ctx->gl_main, (size_t)2 * ctx->k));
   CKC(dalloc(&ctx->gl_side, (size_t)2 * ctx->k));
   CKC(dalloc(&ctx->nload_main, 1));
@@ -588,9 +600,15 @@ ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const vo
   }
   CK(cudaMemcpyAsync(ctx->host_store + (size_t)layer * stage_bytes, staging, stage_bytes, cudaMemcpyDeviceToHost, st));
   CacheLayer cl = cache_layer(ctx, layer);
-  CK(cudaMemsetAsync(cl.slot_of, 0xFF, sizeof(int32_t) * ctx->m_loc, st));
-  CK(cudaMemsetAsync(cl.owner, 0xFF, sizeof(int32_t) * ctx->P, st));
-  CK(cudaMemsetAsync(cl.pf_epoch, 0xFF, sizeof(int32_t) * ctx->P, st));
+  if (ctx->global_heap) {  // the shared pool may hold any layer's chunks: empty all of it
+    CK(cudaMemsetAsync(ctx->slot_of, 0xFF, sizeof(int32_t) * ctx->L * ctx->m_loc, st));
+    CK(cudaMemsetAsync(ctx->owner, 0xFF, sizeof(int32_t) * ctx->L * ctx->P, st));
+    CK(cudaMemsetAsync(ctx->pf_epoch, 0xFF, sizeof(int32_t) * ctx->L * ctx->P, st));
+  } else {
+    CK(cudaMemsetAsync(cl.slot_of, 0xFF, sizeof(int32_t) * ctx->m_loc, st));
+    CK(cudaMemsetAsync(cl.owner, 0xFF, sizeof(int32_t) * ctx->P, st));
+    CK(cudaMemsetAsync(cl.pf_epoch, 0xFF, sizeof(int32_t) * ctx->P, st));
+  }
   CK(cudaMemsetAsync(cl.I, 0, sizeof(float) * ctx->m_loc, st));
   CK(cudaMemsetAsync(cl.F, 0, sizeof(int32_t) * ctx->m_loc, st));
   CK(cudaMemsetAsync(cl.T, 0, sizeof(int32_t) * ctx->m_loc, st));

@@ -147,13 +147,21 @@ __device__ __forceinline__ int64_t shard_token(int64_t i, int64_t t0, int cyc_W,
   return cyc_W > 0 ? ((i / c) * cyc_W + cyc_g) * c + i % c : t0 + i;
 }
 // A4 / A5 / A9
+// Owners are encoded as table indices e = layer * m_loc + j into the [L][m_loc] tables, so victims
+// of any layer resolve with the *0 base pointers (the global heap of CKV_FLAG_GLOBAL_HEAP, where
+// one pool of L * P slots serves every layer; per-layer pools see only their own layer's e).
 struct CacheLayer {
-  int32_t* slot_of;   // [m_loc]
-  int32_t* owner;     // [P]
+  int32_t* slot_of;   // [m_loc] this layer's view
+  int32_t* owner;     // [P] (the whole pool in global-heap mode)
   int32_t* pf_epoch;  // [P]
   float* I;           // [m_loc]
   int32_t* F;         // [m_loc]
   int32_t* T;         // [m_loc] request tick of the last selection (LRU policy)
+  int32_t* slot_of0;  // [L * m_loc] layer-0 bases of the tables
+  float* I0;
+  int32_t* F0;
+  int32_t* T0;
+  int lbase;          // layer * m_loc
   int m_loc, P;
   int policy;         // ckv_cache_policy: eviction score S (0: I*F, 1: F, 2: last-use tick)
 };

@@ -24,6 +24,8 @@ __device__ __forceinline__ bool bsearch_ids(const int32_t* ids, int n, int j) {
   return false;
 }
 
+constexpr int kPlanKPT = 4;  // victim keys per thread held in registers (P <= 4 * NT)
+
 struct PlanSmem {
   SelectSmem ss;
   int hits, spec_used;
@@ -95,44 +97,75 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
   int n_vict = 0;
   if (need > 0) {
     auto key = [&](int s) -> uint64_t {
-      const int j = cl.owner[s];
-      if (j < 0) return 0ull;
-      if (bsearch_ids(ids, n_ids, j)) return 0ull;
+      const int e = cl.owner[s];  // table index layer * m_loc + j
+      if (e < 0) return 0ull;
+      const int jl = e - cl.lbase;
+      if (jl >= 0 && jl < cl.m_loc && bsearch_ids(ids, n_ids, jl)) return 0ull;  // requested by this plan
       if (!prefetch && cl.pf_epoch[s] == epoch) return 0ull;
-      // Eq. 2 by default; the ablation policies of PAPER.md:610-613
-      const float S = cl.policy == 0 ? cl.I[j] * (float)cl.F[j] : cl.policy == 1 ? (float)cl.F[j] : (float)cl.T[j];
-      return ~(((uint64_t)__float_as_uint(S) << 32) | (uint64_t)(uint32_t)j);
+      // Eq. 2 by default; the ablation policies of PAPER.md:610-613.  Ties by
+      // (S, layer, j) = (S, e)
+      const float S = cl.policy == 0 ? cl.I0[e] * (float)cl.F0[e] : cl.policy == 1 ? (float)cl.F0[e] : (float)cl.T0[e];
+      return ~(((uint64_t)__float_as_uint(S) << 32) | (uint64_t)(uint32_t)e);
     };
-    // capacity guard (cannot trigger when P >= k + quota; kept as a loud failure, not a crash)
-    int n_evictable = 0;
-    for (int b = 0; b < cl.P; b += NT) {
-      const int s = b + threadIdx.x;
-      int tot;
-      block_excl_scan<NT>((s < cl.P && key(s) != 0ull) ? 1 : 0, tot, ss);
-      n_evictable += tot;
-    }
-    if (need > n_evictable) {
-      if (threadIdx.x == 0 && out.stats) out.stats[15] = 1;
-      need = n_evictable;
-      n_miss = n_free + need;
-    }
-    const uint64_t T = need > 0 ? block_kth_largest<NT>(key, cl.P, need, ss) : ~0ull;
-    for (int b = 0; b < cl.P; b += NT) {
-      const int s = b + threadIdx.x;
-      uint64_t kv = 0ull;
-      if (s < cl.P) kv = key(s);
-      const bool f = kv != 0ull && kv >= T;
-      int tot;
-      const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
-      if (f) vict[n_vict + pos] = s;
-      n_vict += tot;
+    if (cl.P <= NT * kPlanKPT) {
+      // keys evaluated once into registers (slot s = threadIdx.x + NT*u): the radix passes then
+      // cost no memory traffic (integer LFU / LRU scores tie a lot and run all 8 passes)
+      uint64_t kr[kPlanKPT];
+      int ev = 0;
+#pragma unroll
+      for (int u = 0; u < kPlanKPT; ++u) {
+        const int s = threadIdx.x + NT * u;
+        kr[u] = s < cl.P ? key(s) : 0ull;
+        ev += kr[u] != 0ull;
+      }
+      int n_evictable;
+      block_excl_scan<NT>(ev, n_evictable, ss);
+      if (need > n_evictable) {  // capacity guard (cannot trigger when P >= k + quota): loud, not a crash
+        if (threadIdx.x == 0 && out.stats) out.stats[15] = 1;
+        need = n_evictable;
+        n_miss = n_free + need;
+      }
+      const uint64_t T = need > 0 ? block_kth_largest_regs<NT, kPlanKPT>(kr, cl.P, need, ss) : ~0ull;
+#pragma unroll
+      for (int u = 0; u < kPlanKPT; ++u) {
+        if (NT * u >= cl.P) break;
+        const bool f = kr[u] != 0ull && kr[u] >= T;
+        int tot;
+        const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+        if (f) vict[n_vict + pos] = threadIdx.x + NT * u;
+        n_vict += tot;
+      }
+    } else {
+      int n_evictable = 0;
+      for (int b = 0; b < cl.P; b += NT) {
+        const int s = b + threadIdx.x;
+        int tot;
+        block_excl_scan<NT>((s < cl.P && key(s) != 0ull) ? 1 : 0, tot, ss);
+        n_evictable += tot;
+      }
+      if (need > n_evictable) {
+        if (threadIdx.x == 0 && out.stats) out.stats[15] = 1;
+        need = n_evictable;
+        n_miss = n_free + need;
+      }
+      const uint64_t T = need > 0 ? block_kth_largest<NT>(key, cl.P, need, ss) : ~0ull;
+      for (int b = 0; b < cl.P; b += NT) {
+        const int s = b + threadIdx.x;
+        uint64_t kv = 0ull;
+        if (s < cl.P) kv = key(s);
+        const bool f = kv != 0ull && kv >= T;
+        int tot;
+        const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+        if (f) vict[n_vict + pos] = s;
+        n_vict += tot;
+      }
     }
     __syncthreads();
     for (int t = threadIdx.x; t < n_vict; t += NT) {
       const int s = vict[t];
-      const int j = cl.owner[s];
-      if (out.victims) out.victims[t] = j;
-      cl.slot_of[j] = -1;
+      const int e = cl.owner[s];
+      if (out.victims) out.victims[t] = e;
+      cl.slot_of0[e] = -1;
       cl.owner[s] = -1;
     }
   }
@@ -142,7 +175,7 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
     const int s = (t < n_free) ? freel[t] : vict[t - n_free];
     const int j = miss[t];
     cl.slot_of[j] = s;
-    cl.owner[s] = j;
+    cl.owner[s] = cl.lbase + j;
     cl.pf_epoch[s] = prefetch ? epoch : -1;
     out.gather_list[2 * t] = j;
     out.gather_list[2 * t + 1] = s;

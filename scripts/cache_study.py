@@ -23,7 +23,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from paper_2601_13631_b200 import Context, ckv_budget_chunks  # noqa: E402
+from paper_2601_13631_b200 import CKV_FLAG_GLOBAL_HEAP, Context, ckv_budget_chunks  # noqa: E402
 from synth import CONFIGS, make_prefix, make_request  # noqa: E402
 
 
@@ -37,6 +37,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="run only the first L layers (per-layer cache "
                     "partitions make layers independent; 0 = all)")
     ap.add_argument("--slots", default="1.25,1.5,2,3", help="HBM slots per layer as multiples of k")
+    ap.add_argument("--heaps", default="layer", help="comma list of 'layer' (per-layer pools) and 'global' "
+                    "(one pool of L x slots shared by every layer, PAPER.md:447)")
     args = ap.parse_args()
     base = CONFIGS[args.config]
     if args.layers:
@@ -60,10 +62,12 @@ def main():
         k = ckv_budget_chunks(base.prefix_len, base.chunk_size, bp)
         ids = [torch.empty(k, dtype=torch.int32, device=dev) for _ in range(L)]
         mults = [float(x) for x in args.slots.split(",")]
-        for P, prefetch in [(int(k * f), pf) for f in mults for pf in (True, False)]:
+        for heap, P, prefetch in [(h, int(k * f), pf) for h in args.heaps.split(",") for f in mults
+                                  for pf in (True, False)]:
             quota = min(k, P - k) if prefetch else 0
             ctx = Context(L, base.num_q_heads, base.num_kv_heads, base.head_dim, base.chunk_size, base.prefix_len,
-                          base.suffix_len, dtype="bf16", budget_bp=bp, prefetch_chunks=quota, cache_slots=P)
+                          base.suffix_len, dtype="bf16", budget_bp=bp, prefetch_chunks=quota, cache_slots=P,
+                          flags=CKV_FLAG_GLOBAL_HEAP if heap == "global" else 0)
             for l in range(L):
                 ctx.store_prefix(l, *prefix[l])
             for policy in ("attn", "lfu", "lru"):
@@ -84,7 +88,7 @@ def main():
                 st = ctx.get_stats()
                 nl = max(st["total_layers"], 1)
                 sel = st["total_hits"] + st["total_misses"]
-                row = {"budget_bp": bp, "k": k, "slots_per_layer": P, "prefetch_quota": quota, "policy": policy,
+                row = {"budget_bp": bp, "k": k, "heap": heap, "slots_per_layer": P, "prefetch_quota": quota, "policy": policy,
                        "hit_rate": st["total_hits"] / max(sel, 1),
                        "delta_MB_per_layer": st["total_link_bytes_delta"] / nl / 1e6,
                        "spec_MB_per_layer": st["total_link_bytes_spec"] / nl / 1e6,

@@ -8,7 +8,7 @@ import pytest
 import torch
 
 import oracle as O
-from paper_2601_13631_b200 import CKV_FLAG_CYCLIC_SHARDS, CKV_FLAG_SIMT_SCORE, CkvError, Context
+from paper_2601_13631_b200 import CKV_FLAG_CYCLIC_SHARDS, CKV_FLAG_GLOBAL_HEAP, CKV_FLAG_SIMT_SCORE, CkvError, Context
 from synth import CONFIGS, ShapeConfig, make_prefix, make_request
 from tests.gpu_util import check_layer, make_ctx, run_layers, to_dev
 
@@ -93,6 +93,20 @@ def test_c2_shape_layers_prefetch_and_cache_invariance():
     for a, b, c in zip(res, res2, res3):
         assert np.array_equal(a["ids"], b["ids"]) and np.array_equal(a["ids"], c["ids"])
         assert np.array_equal(a["out"], b["out"]) and np.array_equal(a["out"], c["out"])
+
+
+def test_global_heap_layers_match_oracle():
+    """Global heap with a pool too small for every layer's selection: chunks of other layers are
+    evicted and reloaded (through the fused compaction gather); results stay the oracle's."""
+    cfg = C2_SMALL
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg, prefetch=k // 2, cache_slots=k + k // 2, flags=CKV_FLAG_GLOBAL_HEAP)
+    for req in range(2):
+        res = run_layers(ctx, cfg, prefix, range(cfg.num_layers), request=req)
+        _check_all(ctx, cfg, prefix, res, k)
+    st = ctx.get_stats()
+    assert st["total_misses"] > 0
+    ctx.close()
 
 
 def test_c3_full_size_two_layers():
@@ -264,6 +278,32 @@ def test_cache_plan_matches_model(policy):
         assert sorted(loads[:, 0].tolist()) == sorted(j for j, _ in loads_m)
         assert sorted(victims.cpu().numpy()[: counts[2]].tolist()) == sorted(vict_m)
         assert len(set(loads[:, 1].tolist())) == len(loads) and loads[:, 1].max(initial=0) < P
+
+
+@pytest.mark.parametrize("policy", ["attn", "lfu"])
+def test_global_heap_plan_matches_model(policy):
+    """CKV_FLAG_GLOBAL_HEAP: one pool of L*P slots; victims of any layer."""
+    L, m, P, k = 3, 48, 6, 6
+    ctx = Context(L, 1, 1, 64, 1, m, 1, dtype="fp32", budget_chunks=k, cache_slots=P, flags=CKV_FLAG_GLOBAL_HEAP)
+    for l in range(L):
+        ctx.store_prefix(l, torch.zeros(m, 1, 64, device="cuda"), torch.zeros(m, 1, 64, device="cuda"))
+    ctx.set_cache_policy(policy)
+    model = O.CacheModel(L, m, P, policy=policy, global_heap=True)
+    g = np.random.default_rng(5)
+    for step in range(60):
+        l = int(g.integers(0, L))
+        A = g.integers(0, 30, m).astype(np.float32)
+        ids = np.sort(g.choice(m // 2 if step % 3 else m, k, replace=False)).astype(np.int32)
+        hits_m, loads_m, vict_m = model.plan(l, ids)
+        model.update(l, ids, A.astype(np.float64), tick=step + 1)
+        loads, victims, counts = ctx.test_cache_step(l, torch.from_numpy(ids).cuda(), A=torch.from_numpy(A).cuda())
+        counts = counts.cpu().numpy()
+        loads = loads.cpu().numpy()[: 2 * counts[1]].reshape(-1, 2)
+        assert counts[0] == len(hits_m) and counts[1] == len(loads_m) and counts[2] == len(vict_m)
+        assert sorted(loads[:, 0].tolist()) == sorted(j for j, _ in loads_m)
+        assert sorted(victims.cpu().numpy()[: counts[2]].tolist()) == sorted(vl * m + vj for vl, vj in vict_m)
+        assert len(set(loads[:, 1].tolist())) == len(loads) and loads[:, 1].max(initial=0) < L * P
+    ctx.close()
 
 
 # ---------------------------------------------------------------- sharded (logical, 1 GPU)

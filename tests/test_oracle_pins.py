@@ -296,7 +296,7 @@ def test_cache_heap_law_persistence_and_delta():
     for req in range(30):
         A = g.integers(1, 10, m).astype(float)
         ids = O.select_topk(A + g.random(m) * 0, k) if req % 3 else g.choice(m, k, replace=False)
-        resident_before = {int(j) for j in cm.owner[0] if j >= 0}
+        resident_before = {j for e in cm.owner[0] if e is not None for _, j in [e]}
         S_before = cm.score(0).copy()
         hits, loads, victims = cm.plan(0, ids)
         # delta law: loads are exactly the requested ids not resident
@@ -309,7 +309,7 @@ def test_cache_heap_law_persistence_and_delta():
         if victims:
             assert max(vs) <= min(S_before[j] for j in evictable - set(victims)) if evictable - set(victims) else True
         # capacity
-        assert (cm.owner[0] >= 0).sum() <= P
+        assert sum(e is not None for e in cm.owner[0]) <= P
         for j in victims:  # persistence: (I, F) survive eviction
             seen_I[j] = (cm.I[0, j], cm.F[0, j])
         cm.update(0, ids, A)
@@ -332,6 +332,23 @@ def test_cache_policy_worked_example(policy, victim):
         cm.update(0, ids, A, tick=tick)
     hits, loads, victims = cm.plan(0, [3])
     assert hits == [] and victims == [victim] and loads == [(3, victim)]  # slot s holds chunk s
+
+
+def test_cache_global_heap_worked_example():
+    """Global heap: one pool of L*P slots; the victim is the lowest (S, layer, chunk)
+    resident of ANY layer.  L = 2, P = 1 per layer (pool of 2), Eq. 2 scores:
+      layer 0 selects {0} with A = 5 -> S(0,0) = 5;  layer 1 selects {0} with A = 1 -> S(1,0) = 1;
+      layer 0 then selects {1}: the pool is full; the per-layer model would evict (0,0) (its only
+      resident) but the global heap evicts (1,0), the lowest S in the pool, and keeps (0,0)."""
+    cm = O.CacheModel(2, 4, 1, global_heap=True)
+    cm.plan(0, [0]); cm.update(0, [0], np.array([5.0, 0, 0, 0]), tick=1)
+    cm.plan(1, [0]); cm.update(1, [0], np.array([1.0, 0, 0, 0]), tick=1)
+    hits, loads, victims = cm.plan(0, [1])
+    assert victims == [(1, 0)] and cm.slot_of[0, 0] >= 0 and cm.slot_of[1, 0] == -1
+    part = O.CacheModel(2, 4, 1)
+    part.plan(0, [0]); part.update(0, [0], np.array([5.0, 0, 0, 0]), tick=1)
+    part.plan(1, [0]); part.update(1, [0], np.array([1.0, 0, 0, 0]), tick=1)
+    assert part.plan(0, [1])[2] == [0]
 
 
 # ------------------------------------------------------------ synthetic inputs
