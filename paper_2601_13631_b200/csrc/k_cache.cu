@@ -24,8 +24,11 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
   pdl_wait();
   pdl_trigger();
   __shared__ PlanSmem ps;
+  extern __shared__ uint64_t plan_skeys[];
   const int n_ids = n_ids_dev ? *n_ids_dev : n_ids_host;
-  cache_plan_body<NT>(cl, ids, n_ids, prefetch, quota, epoch, rec_bytes, scratch, out, ps);
+  const bool smem_keys = cl.P > NT * kPlanKPT && cl.P <= kPlanSmemKeysMax;
+  cache_plan_body<NT>(cl, ids, n_ids, prefetch, quota, epoch, rec_bytes, scratch, out, ps,
+                      smem_keys ? plan_skeys : nullptr);
 }
 
 // Whole-record copy host store -> HBM slot: work items are 4 KiB segments of records so a
@@ -133,8 +136,19 @@ cudaError_t launch_epoch_inc(int32_t* epoch_dev, cudaStream_t st) {
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t*,
                               int32_t* scratch32, PlanOut out, cudaStream_t st) {
-  if (cudaError_t e_ = launch_kernel(cache_plan_kernel, 1, NT, 0, st, cl, ids, n_ids_dev, n_ids_host, prefetch, quota, epoch, rec_bytes, scratch32,
-                                      out)) return e_;
+  size_t smem = 0;
+  if (cl.P > NT * kPlanKPT && cl.P <= kPlanSmemKeysMax) {
+    static bool attr = false;
+    if (!attr) {
+      if (cudaError_t e = cudaFuncSetAttribute(cache_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(kPlanSmemKeysMax * sizeof(uint64_t))))
+        return e;
+      attr = true;
+    }
+    smem = (size_t)cl.P * sizeof(uint64_t);
+  }
+  if (cudaError_t e_ = launch_kernel(cache_plan_kernel, 1, NT, smem, st, cl, ids, n_ids_dev, n_ids_host, prefetch, quota,
+                                     epoch, rec_bytes, scratch32, out)) return e_;
   return cudaGetLastError();
 }
 

@@ -25,17 +25,19 @@ __device__ __forceinline__ bool bsearch_ids(const int32_t* ids, int n, int j) {
 }
 
 constexpr int kPlanKPT = 4;  // victim keys per thread held in registers (P <= 4 * NT)
+constexpr int kPlanSmemKeysMax = 24 * 1024;  // larger pools: keys in dynamic shared memory (192 KB)
 
 struct PlanSmem {
   SelectSmem ss;
   int hits, spec_used;
+  uint32_t req_bits[kPlanSmemKeysMax / 32];  // slots holding a requested chunk (pools <= kPlanSmemKeysMax)
 };
 
 // The A4 planner (+ fused A9) run by one CTA of NT threads (every thread must call it).
 template <int NT>
 __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict__ ids, int n_ids, int prefetch,
                                 int quota, int epoch, int64_t rec_bytes, int32_t* __restrict__ scratch,
-                                const PlanOut& out, PlanSmem& ps) {
+                                const PlanOut& out, PlanSmem& ps, uint64_t* skeys = nullptr) {
   SelectSmem& ss = ps.ss;
   int& s_hits = ps.hits;
   int& s_spec_used = ps.spec_used;
@@ -45,6 +47,9 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
   int32_t* vict = freel + cl.P;       // [P]
   int32_t* mpos = vict + cl.P;        // [n_ids]: position in ids of each miss
   if (threadIdx.x == 0) { s_hits = 0; s_spec_used = 0; }
+  const bool use_bits = cl.P <= kPlanSmemKeysMax;
+  if (use_bits)
+    for (int w = threadIdx.x; w < (cl.P + 31) / 32; w += NT) ps.req_bits[w] = 0u;
   __syncthreads();
 
   // 1. hit / miss, misses compacted in ascending chunk order.  Hits write their kept slot now;
@@ -62,6 +67,7 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
       is_miss = s < 0;
       if (!is_miss) {
         atomicAdd(&s_hits, 1);
+        if (use_bits) atomicOr(&ps.req_bits[s >> 5], 1u << (s & 31));
         if (!prefetch && cl.pf_epoch[s] == epoch) atomicAdd(&s_spec_used, 1);
       }
       if (out.kept_slots) out.kept_slots[t] = s;  // misses: -1 until step 4 assigns a slot
@@ -99,8 +105,12 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
     auto key = [&](int s) -> uint64_t {
       const int e = cl.owner[s];  // table index layer * m_loc + j
       if (e < 0) return 0ull;
-      const int jl = e - cl.lbase;
-      if (jl >= 0 && jl < cl.m_loc && bsearch_ids(ids, n_ids, jl)) return 0ull;  // requested by this plan
+      if (use_bits) {  // requested by this plan = the slot of a hit (marked in step 1)
+        if (ps.req_bits[s >> 5] & (1u << (s & 31))) return 0ull;
+      } else {
+        const int jl = e - cl.lbase;
+        if (jl >= 0 && jl < cl.m_loc && bsearch_ids(ids, n_ids, jl)) return 0ull;
+      }
       if (!prefetch && cl.pf_epoch[s] == epoch) return 0ull;
       // Eq. 2 by default; the ablation policies of PAPER.md:610-613.  Ties by
       // (S, layer, j) = (S, e)
@@ -133,6 +143,32 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
         int tot;
         const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
         if (f) vict[n_vict + pos] = threadIdx.x + NT * u;
+        n_vict += tot;
+      }
+    } else if (skeys) {
+      // large pools (global heap): keys evaluated once into shared memory, passes read them there
+      int ev = 0;
+      for (int s = threadIdx.x; s < cl.P; s += NT) {
+        const uint64_t kv = key(s);
+        skeys[s] = kv;
+        ev += kv != 0ull;
+      }
+      int n_evictable;
+      block_excl_scan<NT>(ev, n_evictable, ss);  // its barriers also publish skeys
+      if (need > n_evictable) {
+        if (threadIdx.x == 0 && out.stats) out.stats[15] = 1;
+        need = n_evictable;
+        n_miss = n_free + need;
+      }
+      auto skey = [&](int s) -> uint64_t { return skeys[s]; };
+      const uint64_t T = need > 0 ? block_kth_largest<NT>(skey, cl.P, need, ss) : ~0ull;
+      for (int b = 0; b < cl.P; b += NT) {
+        const int s = b + threadIdx.x;
+        const uint64_t kv = s < cl.P ? skeys[s] : 0ull;
+        const bool f = kv != 0ull && kv >= T;
+        int tot;
+        const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
+        if (f) vict[n_vict + pos] = s;
         n_vict += tot;
       }
     } else {
