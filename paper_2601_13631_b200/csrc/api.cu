@@ -670,7 +670,23 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
       LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
       PROF_END(2);
       PROF_BEGIN(6);
-      LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, nullptr, 0, nids, st));
+      // A3 + A4 in one CTA when this layer's prefetch is already joined (or none was issued)
+      // measured on B200 (C3, graph replay): 90.5 us/layer fused vs 89.0 separate -> opt-in only
+      static const bool topk_plan = getenv("CKV_TOPK_PLAN") && getenv("CKV_TOPK_PLAN")[0] == '1';
+      cudaError_t e = cudaErrorNotSupported;
+      if (topk_plan && (ctx->pf_issued[layer] != ctx->epoch || ctx->pf_joined[layer] == ctx->epoch)) {
+        SelectPlanArgs a{ctx->A, ctx->k, ids, nids, nullptr, 1, cache_layer(ctx, layer), ctx->epoch,
+                         ctx->rec_bytes, ctx->scratch_main, demand_plan_out(ctx, layer, selected_ids)};
+        e = launch_topk_plan(ctx->Apart, ctx->Hkv, ctx->m_loc, a, st);
+        if (e == cudaSuccess) {
+          planned = true;
+          ++ctx->launches;
+        }
+      }
+      if (e == cudaErrorNotSupported)
+        LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, nullptr, 0, nids, st));
+      else
+        CK(e);
       PROF_END(6);
     }
     // intra-period loads (exact ids) for the period's other layers, then the speculative load of

@@ -193,6 +193,9 @@ struct SelectPlanArgs {
   PlanOut out;
 };
 bool chunk_sum_select_supported(const LayerGeom& g);
+// A3 top-k + A4 demand plan in one single-CTA launch (k_cache.cu); cudaErrorNotSupported if m or the
+// pool is too large (nothing launched)
+cudaError_t launch_topk_plan(const float* Apart, int nparts, int m, const SelectPlanArgs& a, cudaStream_t st);
 cudaError_t launch_chunk_sum_select(const LayerGeom& g, const float* lam2, const float* Lam2, float* Apart,
                                     const SelectPlanArgs& a, cudaStream_t st);
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,

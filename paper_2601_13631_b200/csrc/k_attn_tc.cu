@@ -174,10 +174,11 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __re
 // O += P V for the tile that was scored one step earlier (MMA thread): P (A) from the tile's
 // S buffer in TMEM, V (B) the MN-major [half][128 keys][64] block of the stage.
 __device__ __forceinline__ void issue_pv(uint32_t tmem, uint8_t* kvbuf0, uint64_t* p_full, uint64_t* pv_done,
-                                         uint64_t* o_empty, uint64_t* kv_empty, uint32_t idesc_o, int jj, int stage,
-                                         int sbuf, int nkeys, int icount, int& pcount) {
+                                         uint64_t* o_empty, uint64_t* v_full, uint64_t* kv_empty, uint32_t idesc_o,
+                                         int jj, int stage, int vphase, int sbuf, int nkeys, int icount, int& pcount) {
   ptx::mbar_wait(p_full, pcount & 1);
   if (jj == 0) ptx::mbar_wait(o_empty, (icount & 1) ^ 1);
+  ptx::mbar_wait(&v_full[stage], vphase);
   ptx::tc_fence_after();
   const uint32_t va0 = ptx::smem_u32(kvbuf0 + stage * kKVBytes + 2 * kPartBytes);
   const int ksteps = (nkeys + 15) / 16;  // key steps past the tile's valid keys are skipped
@@ -196,9 +197,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
   __shared__ float red_m[2][NWQ * 128];  // [tile parity][warp of a quadrant][128 rows]
   __shared__ float red_l[NWQ * 128];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kKVBytes);
-  uint64_t* kv_full = bars + 0;             // [kStages]
-  uint64_t* kv_empty = bars + kStages;      // [kStages]
-  uint64_t* s_full = bars + 2 * kStages;    // [2]
+  // K and V halves of a stage have their own barriers: K(t) is released as soon as S(t) is
+  // computed, so the K of later tiles streams in while the softmax and PV of earlier tiles run
+  uint64_t* k_full = bars + 0;              // [kStages]
+  uint64_t* kv_empty = bars + kStages;      // [kStages] V half released (after PV)
+  uint64_t* v_full = bars + 2 * kStages;    // [kStages]
+  uint64_t* k_empty = bars + 3 * kStages;   // [kStages] K half released (after S)
+  uint64_t* s_full = bars + 4 * kStages;    // [2]
   uint64_t* p_full = s_full + 2;
   uint64_t* pv_done = p_full + 1;
   uint64_t* o_full = pv_done + 1;
@@ -212,8 +217,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
-      ptx::mbar_init(&kv_full[i], 1);
+      ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&kv_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) ptx::mbar_init(&s_full[i], 1);
     ptx::mbar_init(p_full, kSoftWarps);
@@ -244,10 +251,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         for (int t = tl.t0; t < tl.t1; ++t) {
           if (!tile_present(p, tl, t)) continue;
           const int st = kvcount % kStages;
-          ptx::mbar_wait(&kv_empty[st], ((kvcount / kStages) & 1) ^ 1);
-          ptx::mbar_expect_tx(&kv_full[st], kKVBytes);
-          ptx::bulk_g2s(kvbuf0 + st * kKVBytes, p.dense + ((int64_t)kvh * p.T_cap + t) * kKVBytes, kKVBytes,
-                        &kv_full[st]);
+          const uint32_t par = ((kvcount / kStages) & 1) ^ 1;
+          const char* src = p.dense + ((int64_t)kvh * p.T_cap + t) * kKVBytes;
+          ptx::mbar_wait(&k_empty[st], par);
+          ptx::mbar_expect_tx(&k_full[st], kKVBytes / 2);
+          ptx::bulk_g2s(kvbuf0 + st * kKVBytes, src, kKVBytes / 2, &k_full[st]);
+          ptx::mbar_wait(&kv_empty[st], par);
+          ptx::mbar_expect_tx(&v_full[st], kKVBytes / 2);
+          ptx::bulk_g2s(kvbuf0 + st * kKVBytes + kKVBytes / 2, src + kKVBytes / 2, kKVBytes / 2, &v_full[st]);
           ++kvcount;
         }
       }
@@ -269,11 +280,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
         const Tiles tl = item_tiles(p, sp, n_kept);
         ptx::mbar_wait(q_full, icount & 1);
         trace_ev(p, 1, icount);
-        int j = 0, prev_stage = 0, prev_sb = 0, prev_keys = 0;
+        int j = 0, prev_stage = 0, prev_sb = 0, prev_keys = 0, prev_vph = 0;
         for (int t = tl.t0; t < tl.t1; ++t) {
           if (!tile_present(p, tl, t)) continue;
           const int st = kvcount % kStages;
-          ptx::mbar_wait(&kv_full[st], (kvcount / kStages) & 1);
+          ptx::mbar_wait(&k_full[st], (kvcount / kStages) & 1);
           trace_ev(p, 2, kvcount);
           ptx::tc_fence_after();
           const int sb = scount & 1;
@@ -283,10 +294,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
             ptx::mma_bf16_ts(tmem + sb * BN, tmem + kColQ + k * 8,
                              ptx::umma_desc_sw128(ka + (k >> 2) * kPartBytes + (k & 3) * 32), idesc_s, k > 0 ? 1u : 0u);
           ptx::mma_commit(&s_full[sb]);
+          ptx::mma_commit(&k_empty[st]);
           ++scount;
           if (j > 0)
-            issue_pv(tmem, kvbuf0, p_full, pv_done, o_empty, kv_empty, idesc_o, j - 1, prev_stage, prev_sb, prev_keys,
-                     icount, pcount);
+            issue_pv(tmem, kvbuf0, p_full, pv_done, o_empty, v_full, kv_empty, idesc_o, j - 1, prev_stage, prev_vph,
+                     prev_sb, prev_keys, icount, pcount);
+          prev_vph = (kvcount / kStages) & 1;
           prev_stage = st;
           prev_sb = sb;
           prev_keys = (t < p.NTp_cap) ? min(BN, n_valid_prefix - t * BN) : min(BN, p.g.ns - (t - p.NTp_cap) * BN);
@@ -294,8 +307,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           ++j;
         }
         if (j > 0)
-          issue_pv(tmem, kvbuf0, p_full, pv_done, o_empty, kv_empty, idesc_o, j - 1, prev_stage, prev_sb, prev_keys,
-                   icount, pcount);
+          issue_pv(tmem, kvbuf0, p_full, pv_done, o_empty, v_full, kv_empty, idesc_o, j - 1, prev_stage, prev_vph,
+                   prev_sb, prev_keys, icount, pcount);
         ptx::mma_commit(o_full);
       }
     }
