@@ -10,6 +10,8 @@
 // Every transfer moves one whole chunk record (unit of storage = unit of transfer =
 // unit of eviction), so read amplification is 1.
 #include "common.cuh"
+#include <cstdlib>
+
 #include "plan.cuh"
 
 namespace ckv {
@@ -184,7 +186,13 @@ cudaError_t launch_topk_plan(const float* Apart, int nparts, int m, const Select
 
 cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
                           char* pool_layer, int64_t rec_bytes, cudaStream_t st) {
-  if (cudaError_t e_ = launch_kernel(gather_kernel, GATHER_BLOCKS, GATHER_THREADS, 0, st, gather_list, n_load, host_layer_dev, pool_layer, rec_bytes)) return e_;
+  static int blocks = 0;
+  if (!blocks) {  // tuning knob (CKV_GATHER_BLOCKS), default GATHER_BLOCKS
+    const char* e = getenv("CKV_GATHER_BLOCKS");
+    blocks = (e && atoi(e) > 0) ? atoi(e) : GATHER_BLOCKS;
+  }
+  if (cudaError_t e_ = launch_kernel(gather_kernel, blocks, GATHER_THREADS, 0, st, gather_list, n_load, host_layer_dev,
+                                     pool_layer, rec_bytes)) return e_;
   return cudaGetLastError();
 }
 
