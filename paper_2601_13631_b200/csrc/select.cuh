@@ -8,6 +8,8 @@ struct SelectSmem {
   int hist[256];
   int warp_tot[32];
   int state[3];
+  alignas(16) int hist3[3][256];  // rotating histograms of the one-barrier-per-pass select
+  int wc[8][32];      // per-(key slot, warp) flag counts of the one-barrier compaction
 };
 
 // Exclusive prefix sum of v over the block (threadIdx order); *tot = block total.
@@ -174,6 +176,108 @@ __device__ uint64_t block_kth_largest_regs(const uint64_t (&keys)[KPT], int n, i
 
 // Keys in registers (KPT per thread, m <= NT * KPT): A_j is summed from the per-KV-head partials
 // once, and the eight radix passes and the compaction run without memory traffic.
+
+// One barrier per radix pass (keys in registers, NT == 1024): three rotating histograms (the one
+// for pass p+1 is cleared during pass p; it was last read in pass p-2, which every warp finished
+// before barrier p-1), and EVERY warp scans the 256 bins itself after the pass's barrier, so the
+// threshold digit needs no broadcast barrier.  Returns the k-th largest key.
+template <int NT, int KPT>
+__device__ uint64_t block_kth_largest_regs1(const uint64_t (&keys)[KPT], int n, int k, SelectSmem& ss) {
+  static_assert(NT == 1024, "one warp per lane of the per-warp scans");
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 256) ss.hist3[0][threadIdx.x] = 0;
+  __syncthreads();
+  uint64_t prefix = 0, mask = 0;
+  int krem = k;
+  for (int p = 0, shift = 56; shift >= 0; ++p, shift -= 8) {
+    int* h = ss.hist3[p % 3];
+    if (threadIdx.x < 256) ss.hist3[(p + 1) % 3][threadIdx.x] = 0;
+#pragma unroll
+    for (int u = 0; u < KPT; ++u) {
+      const int i = threadIdx.x + NT * u;
+      const bool in = i < n && (keys[u] & mask) == prefix;
+      const unsigned act = __ballot_sync(0xffffffffu, in);
+      if (in) {
+        const unsigned dig = (unsigned)(keys[u] >> shift) & 255u;
+        const unsigned peers = __match_any_sync(act, dig);
+        if (lane == __ffs(peers) - 1) atomicAdd(&h[dig], __popc(peers));
+      }
+    }
+    __syncthreads();
+    // lane l owns bins [248 - 8l, 256 - 8l), read as two 16-byte vectors (no bank conflicts),
+    // cnt[j] = bin 255 - 8l - j (descending)
+    const int4 lo = *reinterpret_cast<const int4*>(h + 248 - 8 * lane);
+    const int4 hi = *reinterpret_cast<const int4*>(h + 252 - 8 * lane);
+    const int cnt[8] = {hi.w, hi.z, hi.y, hi.x, lo.w, lo.z, lo.y, lo.x};
+    const int tot = (cnt[0] + cnt[1] + cnt[2] + cnt[3]) + (cnt[4] + cnt[5] + cnt[6] + cnt[7]);
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int excl = incl - tot;
+    const unsigned bal = __ballot_sync(0xffffffffu, excl < krem && incl >= krem);
+    const int src = __ffs(bal) - 1;
+    int sel = 0, knew = 0, done = 0;
+    if (lane == src) {
+      int cum = excl;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (cum + cnt[j] >= krem) {
+          sel = 255 - 8 * lane - j;
+          knew = krem - cum;
+          done = cnt[j] == krem - cum;
+          break;
+        }
+        cum += cnt[j];
+      }
+    }
+    sel = __shfl_sync(0xffffffffu, sel, src);
+    knew = __shfl_sync(0xffffffffu, knew, src);
+    done = __shfl_sync(0xffffffffu, done, src);
+    prefix |= (uint64_t)sel << shift;
+    mask |= (uint64_t)255u << shift;
+    krem = knew;
+    if (done) break;  // uniform across the block: every warp computed the same histogram scan
+  }
+  return prefix;
+}
+
+// Ascending compaction of the keys >= T held in registers (slot u of thread t = index t + NT*u)
+// with one barrier: warp ballots give in-warp positions, per-(slot, warp) counts go to shared
+// memory, and every warp derives its block offsets from them.  Returns the number written.
+template <int NT, int KPT, typename Emit>
+__device__ int block_compact_regs1(const uint64_t (&keys)[KPT], int n, uint64_t T, SelectSmem& ss, Emit emit) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bool f[KPT];
+  int pos[KPT];
+#pragma unroll
+  for (int u = 0; u < KPT; ++u) {
+    f[u] = (threadIdx.x + NT * u < n) && keys[u] >= T;
+    const unsigned b = __ballot_sync(0xffffffffu, f[u]);
+    pos[u] = __popc(b & ((1u << lane) - 1u));
+    if (lane == 0) ss.wc[u][wid] = __popc(b);
+  }
+  __syncthreads();
+  int base = 0;
+#pragma unroll
+  for (int u = 0; u < KPT; ++u) {
+    const int v = ss.wc[u][lane];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int woff = __shfl_sync(0xffffffffu, incl - v, wid);
+    const int tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (f[u]) emit(base + woff + pos[u], threadIdx.x + NT * u, keys[u]);
+    base += tot;
+  }
+  return base;
+}
+
 // Apart is read with ld.global.cg: in the fused kernel other CTAs of the same grid wrote it.
 template <int NT, int KPT>
 __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart, int nparts, int m, int k,
@@ -197,22 +301,12 @@ __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart
     }
   }
   const int kk = min(k, m);
-  const uint64_t T = block_kth_largest_regs<NT, KPT>(key, m, kk, ss);
+  const uint64_t T = block_kth_largest_regs1<NT, KPT>(key, m, kk, ss);
   // ascending compaction
-  int base = 0;
-#pragma unroll
-  for (int u = 0; u < KPT; ++u) {
-    if (NT * u >= m) break;
-    const int j = threadIdx.x + NT * u;
-    const bool f = (j < m) && key[u] >= T;
-    int tot;
-    const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
-    if (f) {
-      if (ids) ids[base + pos] = j * id_mul + id_offset;
-      if (cand) cand[base + pos] = key[u];
-    }
-    base += tot;
-  }
+  const int base = block_compact_regs1<NT, KPT>(key, m, T, ss, [&](int pos, int j, uint64_t kv) {
+    if (ids) ids[pos] = j * id_mul + id_offset;
+    if (cand) cand[pos] = kv;
+  });
   if (cand)
     for (int t = kk + threadIdx.x; t < n_cand_out; t += NT) cand[t] = 0ull;
   if (n_out && threadIdx.x == 0) *n_out = base;
