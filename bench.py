@@ -355,6 +355,29 @@ def run_ckv(args, rank, world):
     cold_stats = ctx.get_stats()
     cold_layers = max(cold_stats["total_layers"], 1)
 
+    # HBM probe: the same prefix with an 8-token suffix (56 GQA rows per KV head:
+    # 0.22 exp and 56 flop per key byte, below both ridges), where A1 streams the probe keys at
+    # the HBM roofline; the score stage (library events) includes the small Q pack at n_s = 8
+    hbm_probe = None
+    if world == 1:
+        ns8 = 8
+        per8 = [[t[:ns8].contiguous() for t in reqs[0][l]] for l in range(L)]
+        for l in range(L):  # warm
+            ctx.reprefill_layer(l, *per8[l])
+        torch.cuda.synchronize()
+        ctx.profile(True)
+        for _ in range(3):
+            for l in range(L):
+                ctx.reprefill_layer(l, *per8[l])
+        pr8 = ctx.profile_read()
+        ctx.profile(False)
+        t8 = pr8["score"][0] / max(pr8["score"][1], 1)  # ms per launch
+        kbytes = (cfg.prefix_len / world) * cfg.num_kv_heads * cfg.head_dim * 2
+        hbm_peak = load_peaks()[0].get("hbm_gbs", 6650.0)
+        hbm_probe = {"config": f"{CFG_NAME} prefix, n_s = {ns8}", "score_us_per_launch": t8 * 1e3,
+                     "probe_key_bytes": kbytes, "achieved_gbs": kbytes / (t8 * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+                     "frac": kbytes / (t8 * 1e-3) / 1e9 / hbm_peak}
+
     # the paper's own configuration: Periods of p = 8 layers, subperiod sp = 4:
     # chunk ids are identified on 1 layer in 8, the Period's other layers are prefetched
     period_line = None
@@ -456,7 +479,10 @@ def run_ckv(args, rank, world):
                        / cold_layers,
                        "link_gbs": (cold_stats["total_link_bytes_delta"] + cold_stats["total_link_bytes_spec"])
                        / (sum(cold_ms) * 1e-3) / 1e9,
-                       "link_peak_gbs": link_peak, "link_peak_how": "pinned H2D cudaMemcpy 256 MiB, best of 5"},
+                       "link_peak_gbs": link_peak, "link_peak_how": "pinned H2D cudaMemcpy 256 MiB, best of 5",
+                       # exposed gather = t_layer(cold, prefetch on) - t_layer(all-hit)
+                       "exposed_gather_us_per_layer": sum(cold_ms) / len(cold_ms) * 1e3 / L - ms_step * 1e3 / L},
+        "hbm_probe": hbm_probe,
         "e2e": {"value": bpl * L / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
                 "pipelined": "per-layer H2D / D2H streams overlapping the compute", "cuda_graph": bool(e2e_graphs),
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

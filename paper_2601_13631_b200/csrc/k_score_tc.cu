@@ -267,6 +267,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ab = acount & 1;
       ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
       ptx::tc_fence_after();
+      if (mt * BM + quad * 32 >= p.g.R) {  // warp-uniform: this lane quadrant is all padding rows
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
+        ++acount;
+        continue;
+      }
       const int rho = mt * BM + row_in_tile;
       const bool row_ok = rho < p.g.R;
       // both 32-key groups are read from TMEM, then the accumulator is released at once
