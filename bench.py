@@ -374,7 +374,8 @@ def run_ckv(args, rank, world):
         t8 = pr8["score"][0] / max(pr8["score"][1], 1)  # ms per launch
         kbytes = (cfg.prefix_len / world) * cfg.num_kv_heads * cfg.head_dim * 2
         hbm_peak = load_peaks()[0].get("hbm_gbs", 6650.0)
-        hbm_probe = {"config": f"{CFG_NAME} prefix, n_s = {ns8}", "score_us_per_launch": t8 * 1e3,
+        hbm_probe = {"config": f"{CFG_NAME} prefix, n_s = {ns8}", "timing": "library events, eager (incl. the Q pack)",
+                     "score_us_per_launch": t8 * 1e3,
                      "probe_key_bytes": kbytes, "achieved_gbs": kbytes / (t8 * 1e-3) / 1e9, "peak_gbs": hbm_peak,
                      "frac": kbytes / (t8 * 1e-3) / 1e9 / hbm_peak}
 
