@@ -355,6 +355,38 @@ def run_ckv(args, rank, world):
     cold_stats = ctx.get_stats()
     cold_layers = max(cold_stats["total_layers"], 1)
 
+    # V-only store variant (CKV_FLAG_V_ONLY_STORE): the kept chunks' K comes from
+    # the HBM probe array, so every miss moves half the bytes; same cold-cache protocol
+    cold_v = None
+    if world == 1:
+        vctx = ckv.Context(cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.chunk_size,
+                           cfg.prefix_len, cfg.suffix_len, dtype=cfg.dtype, budget_bp=cfg.budget_bp,
+                           prefetch_chunks=quota, cache_slots=cache_slots, device=local_rank,
+                           flags=ckv.CKV_FLAG_V_ONLY_STORE)
+        for l in range(L):
+            kp, vp = make_prefix(cfg, l)
+            vctx.store_prefix(l, torch.from_numpy(kp).to(dev, dt), torch.from_numpy(vp).to(dev, dt))
+
+        def vstep(i):
+            for l in range(L):
+                vctx.reprefill_layer(l, *reqs[i % N_REQUESTS][l], out=outs[l], ids=ids[l])
+        for i in range(3):
+            vstep(i)
+        vms = []
+        vctx.reset_stats()
+        for i in range(min(args.steps, 5)):
+            vctx.reset_cache()
+            torch.cuda.synchronize()
+            vms.append(timed(vstep, 1))
+        vst = vctx.get_stats()
+        vlink = vst["total_link_bytes_delta"] + vst["total_link_bytes_spec"]
+        cold_v = {"us_per_layer": sum(vms) / len(vms) * 1e3 / L, "eager": True,
+                  "link_bytes_per_layer": vlink / max(vst["total_layers"], 1),
+                  "link_gbs": vlink / (sum(vms) * 1e-3) / 1e9,
+                  "hit_rate": vst["total_hits"] / max(vst["total_hits"] + vst["total_misses"], 1)}
+        vctx.close()
+        del vctx
+
     # HBM probe: the same prefix with an 8-token suffix (56 GQA rows per KV head:
     # 0.22 exp and 56 flop per key byte, below both ridges), where A1 streams the probe keys at
     # the HBM roofline; the score stage (library events) includes the small Q pack at n_s = 8
@@ -483,6 +515,7 @@ def run_ckv(args, rank, world):
                        "link_peak_gbs": link_peak, "link_peak_how": "pinned H2D cudaMemcpy 256 MiB, best of 5",
                        # exposed gather = t_layer(cold, prefetch on) - t_layer(all-hit)
                        "exposed_gather_us_per_layer": sum(cold_ms) / len(cold_ms) * 1e3 / L - ms_step * 1e3 / L},
+        "cold_cache_v_only": cold_v,
         "hbm_probe": hbm_probe,
         "e2e": {"value": bpl * L / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
                 "pipelined": "per-layer H2D / D2H streams overlapping the compute", "cuda_graph": bool(e2e_graphs),

@@ -68,6 +68,10 @@ typedef enum { CKV_NORM_PREFIX = 0, CKV_NORM_FULLROW = 1 } ckv_norm;
 #define CKV_FLAG_SIMT_ATTN 0x2u   /* force the SIMT attention kernel in bf16 mode */
 #define CKV_FLAG_CYCLIC_SHARDS 0x4u /* num_shards > 1: shard g owns chunks j with j mod W == g (balanced
                                        sharding) instead of a contiguous range */
+#define CKV_FLAG_V_ONLY_STORE 0x10u /* bf16, d = 128, c % 8 == 0: host records and cache slots hold V only;
+                                       the kept chunks' K is read from the HBM probe array (which holds every
+                                       prefix key anyway), halving host-link bytes per miss (SURVEY §8(a) A5
+                                       variant).  CKV_EUNSUPPORTED otherwise. */
 #define CKV_FLAG_GLOBAL_HEAP 0x8u   /* one HBM chunk cache of L * cache_slots slots shared by every layer
                                        ("a single global GPU heap"): victims are the lowest
                                        (S, layer, chunk) residents of any layer; default: per-layer pools */

@@ -10,6 +10,7 @@ from .ckv import (  # noqa: F401
     CKV_FLAG_GLOBAL_HEAP,
     CKV_FLAG_SIMT_ATTN,
     CKV_FLAG_SIMT_SCORE,
+    CKV_FLAG_V_ONLY_STORE,
     CKV_NORM_FULLROW,
     CKV_NORM_PREFIX,
     CkvError,

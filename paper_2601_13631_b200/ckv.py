@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libckv.so")
 CKV_BF16, CKV_FP32 = 0, 1
 CKV_NORM_PREFIX, CKV_NORM_FULLROW = 0, 1
 CKV_FLAG_SIMT_SCORE, CKV_FLAG_SIMT_ATTN, CKV_FLAG_CYCLIC_SHARDS, CKV_FLAG_GLOBAL_HEAP = 0x1, 0x2, 0x4, 0x8
+CKV_FLAG_V_ONLY_STORE = 0x10
 _STATUS = {0: "CKV_OK", 1: "CKV_EINVAL", 2: "CKV_ENOMEM", 3: "CKV_ECUDA", 5: "CKV_ESTATE", 7: "CKV_EUNSUPPORTED"}
 
 

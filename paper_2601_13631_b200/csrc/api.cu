@@ -315,7 +315,7 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
                          static_cast<const __nv_bfloat16*>(vs),
                          reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->kept_slots, ids,
                          n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->dense_kv,
-                         host_layer_dev(ctx, layer), st);
+                         host_layer_dev(ctx, layer), static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)), st);
       if (e == cudaSuccess) ctx->launches += 1;  // + the dense K/V compaction kernel
     }
     if (e == cudaErrorNotSupported) {
@@ -447,8 +447,16 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   if (ctx->subperiod > ctx->period) return bad("subperiod > period");
   if (ctx->period > 1 && ctx->W > 1) return (delete ctx, CKV_EUNSUPPORTED);
   ctx->rec_elems = (int64_t)2 * ctx->Hkv * ctx->c * ctx->d;
-  ctx->rec_bytes = ctx->rec_elems * ctx->esz;
   ctx->rec_swz = (ctx->dtype == CKV_BF16 && ctx->d == 128) ? 1 : 0;
+  if (c.flags & CKV_FLAG_V_ONLY_STORE) {
+    // V-only records need the tcgen05 attention path (its compaction reads K from the probe array)
+    const bool ok = ctx->rec_swz == 1 && ctx->c % 8 == 0 && ctx->c <= 128 && 128 % ctx->c == 0 &&
+                    !(c.flags & CKV_FLAG_SIMT_ATTN);
+    if (!ok) return (delete ctx, CKV_EUNSUPPORTED);
+    ctx->rec_swz = 2;
+    ctx->rec_elems = (int64_t)ctx->Hkv * ctx->c * ctx->d;
+  }
+  ctx->rec_bytes = ctx->rec_elems * ctx->esz;
 
   ckv_status st = CKV_OK;
   auto cudafail = [&](cudaError_t e, const char* what) {

@@ -99,7 +99,7 @@ struct LayerGeom {
   int m_loc;       // local chunks
   int n_loc;       // local prefix tokens
   int n_pad;       // probe-key row stride per KV head
-  int rec_swz;     // chunk-record layout: 0 plain, 1 swizzled (see rec_elem)
+  int rec_swz;     // chunk-record layout: 0 plain, 1 swizzled, 2 V-only swizzled (see rec_elem)
 };
 
 // Element offset inside one chunk record (one HBM slot / one host-store record).
@@ -107,10 +107,13 @@ struct LayerGeom {
 //  swizzled (bf16, d = 128): [Hkv][K|V][half][c][64] with each 128-byte row's 16-byte units
 //           XOR-swizzled by (row & 7) -- the exact shared-memory image the tcgen05 attention
 //           consumes, so one (chunk, kv head) K+V block is a single contiguous bulk copy.
+//  V-only   (swz 2, CKV_FLAG_V_ONLY_STORE): [Hkv][half][c][64] swizzled, V only (kv == 1); the
+//           kept chunks' K comes from the HBM probe array
 __host__ __device__ __forceinline__ int64_t rec_elem(int swz, int kv, int kvh, int p, int x, int Hkv, int c, int d) {
   if (!swz) return (((int64_t)kv * Hkv + kvh) * c + p) * d + x;
   const int half = x >> 6, xi = x & 63;
   const int u = (xi >> 3) ^ (p & 7);
+  if (swz == 2) return (((int64_t)kvh * 2 + half) * c + p) * 64 + u * 8 + (xi & 7);
   return ((((int64_t)kvh * 2 + kv) * 2 + half) * c + p) * 64 + u * 8 + (xi & 7);
 }
 
@@ -229,7 +232,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
                            const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
                            int nsplit, float* o_part, float* lse_part, void* dense_ws, const char* host_layer,
-                           cudaStream_t st);
+                           const __nv_bfloat16* probe_layer, cudaStream_t st);
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit,
                                 T* out, float* o_f32, float* lse_nat, cudaStream_t st);

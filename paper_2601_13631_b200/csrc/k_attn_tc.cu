@@ -98,8 +98,11 @@ __device__ __forceinline__ bool tile_present(const AttnParams& p, const Tiles& t
 // A kept chunk the planner marked as a miss (slot encoded as -(s + 2)) is read from the mapped
 // host store instead (A5 fused: whole records) and also written to its cache
 // slot s, so the layer has no separate gather launch on its critical path.
+// V-only store (rec_swz 2): the K pieces come from the HBM probe array ([Hkv][n_pad][128], rows of
+// the chunk's local tokens), swizzled on the way; the records (slots, host) hold V alone.
 __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __restrict__ pool,
                                                          const char* __restrict__ host_layer,
+                                                         const __nv_bfloat16* __restrict__ probe,
                                                          const int32_t* __restrict__ kept_ids,
                                                          int64_t rec_bytes, const int32_t* __restrict__ kept_slots,
                                                          const int32_t* __restrict__ n_kept_dev, int k_cap,
@@ -122,10 +125,29 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __re
       if (i >= n_kept) continue;
       const int slot = kept_slots[i];
       if (slot == -1) continue;  // not loaded (planner capacity failure, reported in the stats)
-      const int64_t off = (int64_t)kvh * 4 * piece + part * piece;
       const int key = i * g.c;
       uint4* dst = reinterpret_cast<uint4*>(dense + ((int64_t)kvh * T_cap + key / BN) * kKVBytes +
                                             part * kPartBytes + (key % BN) * 128);
+      if (g.rec_swz == 2 && part < 2) {  // K half `part` of the chunk's rows, from the probe array
+        const uint4* src = reinterpret_cast<const uint4*>(probe + ((int64_t)kvh * g.n_pad + (int64_t)kept_ids[i] * g.c) * 128);
+        const int nu = g.c * 8;  // 16-byte units: c rows x 8
+        for (int u0 = 0; u0 < nu; u0 += 32 * 4) {
+          uint4 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int idx = u0 + lane + 32 * q;  // row idx / 8, unit idx % 8 of this half
+            if (idx < nu) v[q] = __ldg(src + (idx >> 3) * 16 + part * 8 + (idx & 7));
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int idx = u0 + lane + 32 * q;
+            if (idx < nu) dst[(idx >> 3) * 8 + ((idx & 7) ^ ((idx >> 3) & 7))] = v[q];
+          }
+        }
+        continue;
+      }
+      // record offset of this piece: swizzled [Hkv][K|V][half] pieces, or V-only [Hkv][half]
+      const int64_t off = g.rec_swz == 2 ? ((int64_t)kvh * 2 + (part - 2)) * piece : (int64_t)kvh * 4 * piece + part * piece;
       if (slot >= 0) {
         const uint4* src = reinterpret_cast<const uint4*>(pool + (int64_t)slot * rec_bytes + off);
         const int nu = (int)(piece / 16);
@@ -504,7 +526,7 @@ int sm_count() {
 
 bool attn_tc_supported(const LayerGeom& g) {
   // chunk blocks (c rows, 8-row swizzle atoms) must tile 128 keys
-  return g.d == D && g.rec_swz == 1 && g.c >= 8 && g.c <= BN && (BN % g.c) == 0;
+  return g.d == D && (g.rec_swz == 1 || g.rec_swz == 2) && g.c >= 8 && g.c <= BN && (BN % g.c) == 0;
 }
 
 int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix) {
@@ -525,7 +547,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
                            const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
                            int nsplit, float* o_part, float* lse_part, void* dense_ws, const char* host_layer,
-                           cudaStream_t st) {
+                           const __nv_bfloat16* probe_layer, cudaStream_t st) {
   if (!attn_tc_supported(g) || !dense_ws) return cudaErrorNotSupported;
   AttnParams p;
   p.g = g;
@@ -543,11 +565,12 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   p.scale = kLog2e / sqrtf((float)g.d);
   p.o_part = o_part;
   p.lse_part = lse_part;
-  const int64_t rec_bytes = (int64_t)2 * g.Hkv * g.c * D * 2;
+  const int64_t rec_bytes = (int64_t)(g.rec_swz == 2 ? 1 : 2) * g.Hkv * g.c * D * 2;
   const int64_t n_warps = (int64_t)g.Hkv * k_cap * 4 + (include_suffix ? (int64_t)g.Hkv * g.ns * 2 : 0);
   const int cblocks = (int)std::min<int64_t>((n_warps + 7) / 8, 8 * sm_count());
   if (cudaError_t e_ = launch_kernel(compact_kv_kernel, cblocks, 256, 0, st, g,
                                      reinterpret_cast<char*>(const_cast<__nv_bfloat16*>(pool_layer)), host_layer,
+                                     probe_layer,
                                      kept_ids, rec_bytes, kept_slots,
                                              n_kept_dev, k_cap, k_suf, v_suf, include_suffix, p.NTp_cap, p.T_cap,
                                              static_cast<char*>(dense_ws))) return e_;

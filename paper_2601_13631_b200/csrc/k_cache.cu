@@ -121,7 +121,8 @@ __global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict
   pdl_wait();
   pdl_trigger();
   // one record per chunk j (layout: rec_elem), zero padding past n_loc
-  const int64_t per = (int64_t)2 * Hkv * c * d;
+  const int nkv = swz == 2 ? 1 : 2;  // V-only records hold V alone
+  const int64_t per = (int64_t)nkv * Hkv * c * d;
   const int64_t total = (int64_t)m_loc * per;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int j = (int)(e / per);
@@ -129,7 +130,7 @@ __global__ void pack_records_kernel(const T* __restrict__ k, const T* __restrict
     const int x = (int)(r % d); r /= d;
     const int p = (int)(r % c); r /= c;
     const int kvh = (int)(r % Hkv);
-    const int kv = (int)(r / Hkv);
+    const int kv = swz == 2 ? 1 : (int)(r / Hkv);
     const int64_t i = (int64_t)j * c + p;
     T val = from_f<T>(0.f);
     if (i < n_loc) val = (kv == 0 ? k : v)[(shard_token(i, t0, cyc_W, cyc_g, c) * Hkv + kvh) * d + x];

@@ -8,7 +8,8 @@ import pytest
 import torch
 
 import oracle as O
-from paper_2601_13631_b200 import CKV_FLAG_CYCLIC_SHARDS, CKV_FLAG_GLOBAL_HEAP, CKV_FLAG_SIMT_SCORE, CkvError, Context
+from paper_2601_13631_b200 import (CKV_FLAG_CYCLIC_SHARDS, CKV_FLAG_GLOBAL_HEAP, CKV_FLAG_SIMT_SCORE,
+                                   CKV_FLAG_V_ONLY_STORE, CkvError, Context)
 from synth import CONFIGS, ShapeConfig, make_prefix, make_request
 from tests.gpu_util import check_layer, make_ctx, run_layers, to_dev
 
@@ -107,6 +108,32 @@ def test_global_heap_layers_match_oracle():
     st = ctx.get_stats()
     assert st["total_misses"] > 0
     ctx.close()
+
+
+def test_v_only_store_matches_kv_store():
+    """CKV_FLAG_V_ONLY_STORE: records hold V only, K comes from the probe array; the dense tile
+    image is the same bytes, so ids and outputs are bit-identical to the K+V store, and every miss
+    moves half the bytes over the host link."""
+    cfg = C2_SMALL
+    k = _k(cfg)
+    base, prefix = make_ctx(cfg, prefetch=k // 2, cache_slots=k + k // 2)
+    vonly, _ = make_ctx(cfg, prefetch=k // 2, cache_slots=k + k // 2, flags=CKV_FLAG_V_ONLY_STORE)
+    for req in range(2):
+        for ctx in (base, vonly):
+            ctx.reset_cache()
+            ctx.reset_stats()
+        ra = run_layers(base, cfg, prefix, range(cfg.num_layers), request=req)
+        rb = run_layers(vonly, cfg, prefix, range(cfg.num_layers), request=req)
+        for a, b in zip(ra, rb):
+            assert np.array_equal(a["ids"], b["ids"]) and np.array_equal(a["out"], b["out"])
+        sa, sb = base.get_stats(), vonly.get_stats()
+        assert sa["total_misses"] > 0 and sa["total_misses"] == sb["total_misses"]
+        assert 2 * sb["total_link_bytes_delta"] == sa["total_link_bytes_delta"]
+    _check_all(vonly, cfg, prefix, rb, k)
+    with pytest.raises(CkvError):  # needs the tcgen05 attention path
+        Context(1, 4, 2, 64, 16, 256, 8, dtype="fp32", flags=CKV_FLAG_V_ONLY_STORE)
+    base.close()
+    vonly.close()
 
 
 def test_c3_full_size_two_layers():
