@@ -441,6 +441,10 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   ctx->P = c.cache_slots > 0 ? c.cache_slots : 2 * ctx->k + ctx->quota;
   if (ctx->P < ctx->k + ctx->quota) return bad("cache_slots < k + prefetch_chunks");
   ctx->global_heap = (c.flags & CKV_FLAG_GLOBAL_HEAP) != 0;
+  // one shared pool: a side-stream prefetch plan of layer l+1 would run concurrently with layer l's
+  // demand plan and compaction on the same tables and slots, so the global heap is demand-only
+  if (ctx->global_heap && (ctx->quota > 0 || ctx->period > 1 || ctx->W > 1))
+    return (delete ctx, CKV_EUNSUPPORTED);
   ctx->max_ns = c.max_suffix_len;
   ctx->period = c.period > 0 ? c.period : 1;
   ctx->subperiod = c.subperiod > 0 ? c.subperiod : 1;
@@ -810,6 +814,7 @@ ckv_status ckv_set_period(ckv_ctx* ctx, int32_t period, int32_t subperiod) {
   const int p = period > 0 ? period : 1, sp = subperiod > 0 ? subperiod : 1;
   if (sp > p) return fail(ctx, CKV_EINVAL, "subperiod > period");
   if (p > 1 && ctx->W > 1) return fail(ctx, CKV_EUNSUPPORTED, "period > 1 needs num_shards == 1");
+  if (p > 1 && ctx->global_heap) return fail(ctx, CKV_EUNSUPPORTED, "period > 1 needs per-layer cache pools");
   ctx->period = p;
   ctx->subperiod = sp;
   return CKV_OK;

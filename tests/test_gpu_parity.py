@@ -101,13 +101,15 @@ def test_global_heap_layers_match_oracle():
     evicted and reloaded (through the fused compaction gather); results stay the oracle's."""
     cfg = C2_SMALL
     k = _k(cfg)
-    ctx, prefix = make_ctx(cfg, prefetch=k // 2, cache_slots=k + k // 2, flags=CKV_FLAG_GLOBAL_HEAP)
+    ctx, prefix = make_ctx(cfg, prefetch=0, cache_slots=k + k // 4, flags=CKV_FLAG_GLOBAL_HEAP)
     for req in range(2):
         res = run_layers(ctx, cfg, prefix, range(cfg.num_layers), request=req)
         _check_all(ctx, cfg, prefix, res, k)
     st = ctx.get_stats()
     assert st["total_misses"] > 0
     ctx.close()
+    with pytest.raises(CkvError):  # the shared pool is demand-only
+        make_ctx(cfg, prefetch=k // 2, flags=CKV_FLAG_GLOBAL_HEAP, store=False)
 
 
 def test_v_only_store_matches_kv_store():
