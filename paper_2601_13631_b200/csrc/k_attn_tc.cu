@@ -533,6 +533,12 @@ int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix) {
   const int MT = (g.R + BM - 1) / BM;
   const int T_cap = (k_cap * g.c + BN - 1) / BN + (include_suffix ? (g.ns + BN - 1) / BN : 0);
   int s = sm_count() / (g.Hkv * MT);
+  static int force = -1;  // tuning knob CKV_ATTN_SPLITS (results unchanged, only the split count)
+  if (force < 0) {
+    const char* e = getenv("CKV_ATTN_SPLITS");
+    force = (e && atoi(e) > 0) ? atoi(e) : 0;
+  }
+  if (force > 0) s = force;
   if (s < 1) s = 1;
   if (s > T_cap) s = T_cap;
   return s < 1 ? 1 : s;

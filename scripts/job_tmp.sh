@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-for i in 1 2 3; do timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$i.log 2>&1; tail -1 gpurun_out/pytest_gpu_$i.log; grep FAILED gpurun_out/pytest_gpu_$i.log; done
+for S in 3 4 5 6 8 10; do echo "splits=$S $(CKV_ATTN_SPLITS=$S timeout 300 python bench.py --quick --no-cpu --steps 20 2>&1 | tail -1 | cut -c1-60)"; done
