@@ -75,8 +75,8 @@ typedef enum { CKV_NORM_PREFIX = 0, CKV_NORM_FULLROW = 1 } ckv_norm;
 #define CKV_FLAG_GLOBAL_HEAP 0x8u   /* one HBM chunk cache of L * cache_slots slots shared by every layer
                                        ("a single global GPU heap"): victims are the lowest
                                        (S, layer, chunk) residents of any layer; default: per-layer pools.
-                                       Demand loads only: needs prefetch_chunks == 0, period 1, one shard
-                                       (CKV_EUNSUPPORTED otherwise) */
+                                       The next layer's speculative plan then runs only after this layer's
+                                       compaction; needs period 1 and one shard (CKV_EUNSUPPORTED otherwise) */
 
 typedef struct {
   int32_t num_layers;      /* L >= 1 */

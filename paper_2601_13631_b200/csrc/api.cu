@@ -241,9 +241,11 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
 }
 
 // A6: speculative plan + gather of layer `layer` for the given ids, on the side stream.
-ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, cudaStream_t st) {
+// `recorded`: ev_ids was already recorded on st (global heap: after the compaction of the current layer).
+ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, cudaStream_t st,
+                          bool recorded = false) {
   if (ctx->quota <= 0 || layer >= ctx->L) return CKV_OK;
-  CK(cudaEventRecord(ctx->ev_ids, st));
+  if (!recorded) CK(cudaEventRecord(ctx->ev_ids, st));
   CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ids, 0));
   pdl_mark_event_wait(ctx->side);
   PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)(layer * 2 + 1) * 4, ctx->stats,
@@ -269,7 +271,8 @@ PlanOut demand_plan_out(ckv_ctx* ctx, int layer, int32_t* ids_out) {
 // A4 -> A5 -> A7 -> A8 -> A9 for the local selected ids.
 ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, const void* q,
                       const void* ks, const void* vs, int ns, int include_suffix, void* out, float* o_f32,
-                      float* lse_nat, int32_t* ids_out, bool planned, cudaStream_t st) {
+                      float* lse_nat, int32_t* ids_out, bool planned, cudaStream_t st,
+                      cudaEvent_t after_slots = nullptr) {
   // a prefetch of this layer that the stream already joined (before the score kernel) needs no
   // further event waits: they would only cut the programmatic launch edges of plan and attention
   const bool pf = ctx->pf_issued[layer] == ctx->epoch && ctx->pf_joined[layer] != ctx->epoch;
@@ -315,7 +318,9 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
                          static_cast<const __nv_bfloat16*>(vs),
                          reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->kept_slots, ids,
                          n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->dense_kv,
-                         host_layer_dev(ctx, layer), static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)), st);
+                         host_layer_dev(ctx, layer), static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)),
+                         after_slots, st);
+      if (e == cudaSuccess) after_slots = nullptr;  // recorded between the compaction and the attention
       if (e == cudaSuccess) ctx->launches += 1;  // + the dense K/V compaction kernel
     }
     if (e == cudaErrorNotSupported) {
@@ -332,6 +337,7 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
                                           o_f32, lse_nat, st));
   }
   PROF_END(5);
+  if (after_slots) CK(cudaEventRecord(after_slots, st));  // SIMT path: the attention read the slots
   ctx->last_layer = layer;
   return CKV_OK;
 }
@@ -441,10 +447,10 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   ctx->P = c.cache_slots > 0 ? c.cache_slots : 2 * ctx->k + ctx->quota;
   if (ctx->P < ctx->k + ctx->quota) return bad("cache_slots < k + prefetch_chunks");
   ctx->global_heap = (c.flags & CKV_FLAG_GLOBAL_HEAP) != 0;
-  // one shared pool: a side-stream prefetch plan of layer l+1 would run concurrently with layer l's
-  // demand plan and compaction on the same tables and slots, so the global heap is demand-only
-  if (ctx->global_heap && (ctx->quota > 0 || ctx->period > 1 || ctx->W > 1))
-    return (delete ctx, CKV_EUNSUPPORTED);
+  // one shared pool: the next layer's speculative plan is issued only after this layer's demand plan
+  // and compaction (ckv_reprefill_layer); periods (several in-flight prefetch plans) and shards are
+  // not combined with it
+  if (ctx->global_heap && (ctx->period > 1 || ctx->W > 1)) return (delete ctx, CKV_EUNSUPPORTED);
   ctx->max_ns = c.max_suffix_len;
   ctx->period = c.period > 0 ? c.period : 1;
   ctx->subperiod = c.subperiod > 0 ? c.subperiod : 1;
@@ -703,8 +709,11 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     }
     // intra-period loads (exact ids) for the period's other layers, then the speculative load of
     // the next period's first layer (A6), all on the side stream in layer order
-    for (int lp = layer + 1; lp <= pend && lp < ctx->L; ++lp)
-      if ((s = issue_prefetch(ctx, lp, ids, nids, st)) != CKV_OK) return s;
+    // (global heap: one shared pool, so the next layer's speculative plan may only run after this
+    // layer's demand plan and compaction -- issued below, after run_attend)
+    if (!ctx->global_heap)
+      for (int lp = layer + 1; lp <= pend && lp < ctx->L; ++lp)
+        if ((s = issue_prefetch(ctx, lp, ids, nids, st)) != CKV_OK) return s;
     // subperiod gate: attention of the first layer waits for sp layers' chunks
     for (int lp = layer + 1; lp < layer + ctx->subperiod && lp < pend; ++lp)
       if (ctx->pf_issued[lp] == ctx->epoch) {
@@ -713,9 +722,11 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
       }
   }
   // the demand planner also writes selected_ids (no separate copy node per layer)
+  const bool defer_pf = ctx->global_heap && first && ctx->quota > 0 && layer + 1 < ctx->L;
   if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, selected_ids,
-                      planned, st)) != CKV_OK)
+                      planned, st, defer_pf ? ctx->ev_ids : nullptr)) != CKV_OK)
     return s;
+  if (defer_pf && (s = issue_prefetch(ctx, layer + 1, ids, nids, st, true)) != CKV_OK) return s;
   if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;
 }

@@ -553,7 +553,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
                            const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
                            int nsplit, float* o_part, float* lse_part, void* dense_ws, const char* host_layer,
-                           const __nv_bfloat16* probe_layer, cudaStream_t st) {
+                           const __nv_bfloat16* probe_layer, cudaEvent_t after_compact, cudaStream_t st) {
   if (!attn_tc_supported(g) || !dense_ws) return cudaErrorNotSupported;
   AttnParams p;
   p.g = g;
@@ -582,6 +582,10 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                                              static_cast<char*>(dense_ws))) return e_;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (after_compact) {  // the cache slots of this layer are no longer read after this point
+    if ((e = cudaEventRecord(after_compact, st)) != cudaSuccess) return e;
+    pdl_mark_event_wait(st);  // an event node between the kernels: no programmatic edge across it
+  }
   static bool attr = false;
   if (!attr) {
     e = cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);

@@ -63,7 +63,7 @@ def main():
         ids = [torch.empty(k, dtype=torch.int32, device=dev) for _ in range(L)]
         mults = [float(x) for x in args.slots.split(",")]
         for heap, P, prefetch in [(h, int(k * f), pf) for h in args.heaps.split(",") for f in mults
-                                  for pf in (True, False) if not (h == "global" and pf)]:  # global: demand-only
+                                  for pf in (True, False)]:
             quota = min(k, P - k) if prefetch else 0
             ctx = Context(L, base.num_q_heads, base.num_kv_heads, base.head_dim, base.chunk_size, base.prefix_len,
                           base.suffix_len, dtype="bf16", budget_bp=bp, prefetch_chunks=quota, cache_slots=P,

@@ -98,18 +98,19 @@ def test_c2_shape_layers_prefetch_and_cache_invariance():
 
 def test_global_heap_layers_match_oracle():
     """Global heap with a pool too small for every layer's selection: chunks of other layers are
-    evicted and reloaded (through the fused compaction gather); results stay the oracle's."""
+    evicted and reloaded (through the fused compaction gather), with the next layer's speculative
+    plan issued only after this layer's compaction; results stay the oracle's."""
     cfg = C2_SMALL
     k = _k(cfg)
-    ctx, prefix = make_ctx(cfg, prefetch=0, cache_slots=k + k // 4, flags=CKV_FLAG_GLOBAL_HEAP)
+    ctx, prefix = make_ctx(cfg, prefetch=k // 2, cache_slots=k + k // 2, flags=CKV_FLAG_GLOBAL_HEAP)
     for req in range(2):
         res = run_layers(ctx, cfg, prefix, range(cfg.num_layers), request=req)
         _check_all(ctx, cfg, prefix, res, k)
     st = ctx.get_stats()
     assert st["total_misses"] > 0
     ctx.close()
-    with pytest.raises(CkvError):  # the shared pool is demand-only
-        make_ctx(cfg, prefetch=k // 2, flags=CKV_FLAG_GLOBAL_HEAP, store=False)
+    with pytest.raises(CkvError):  # several in-flight prefetch plans (periods) are not combined with it
+        make_ctx(cfg, prefetch=k // 2, flags=CKV_FLAG_GLOBAL_HEAP, store=False)[0].set_period(4, 1)
 
 
 def test_v_only_store_matches_kv_store():
