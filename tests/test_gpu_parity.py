@@ -263,6 +263,30 @@ def test_c4_shape_reduced():
     _check_all(ctx, cfg, prefix, res, k)
 
 
+def test_c4_full_size_layer_properties():
+    """C4 at its full size (14B shape, 128K prefix, c = 32, n_s = 256, 5%: k = 204 of 4096 chunks),
+    one layer in the configuration the bench family uses (tcgen05 paths), checked by properties
+    that hold at any size plus sampled outputs the oracle computes cheaply: prefix-only mass
+    conservation sum_j A_j = n_s * Hq, the ids are exactly the top-k of the GPU's
+    own A with the lower-index tie-break (bit-exact integer work), and the first 32 suffix rows
+    of every head equal the oracle's attention over the GPU's kept chunks + causal suffix."""
+    cfg = CONFIGS["c4_14b"].replace(num_layers=1)
+    k = _k(cfg)
+    ctx, prefix = make_ctx(cfg, prefetch=0)
+    assert ctx.m == 4096 and k == 204
+    res = run_layers(ctx, cfg, prefix, [0])[0]
+    A = res["A"].astype(np.float64)
+    assert abs(A.sum() - cfg.suffix_len * cfg.num_q_heads) < 1e-4 * cfg.suffix_len * cfg.num_q_heads
+    assert res["ids"].tolist() == O.select_topk(res["A"].astype(np.float32).astype(np.float64), k).tolist()
+    kp, vp = prefix[0]
+    ns_s = 32
+    toks = O.kept_token_index(res["ids"], cfg.prefix_len, cfg.chunk_size)
+    ref, _ = O.attention(res["qs"][:ns_s], res["ks"][:ns_s], res["vs"][:ns_s], kp, vp, toks, cfg.group)
+    from tests.gpu_util import TOL, row_rel_err
+    assert row_rel_err(res["out"][:ns_s], ref) < TOL["bf16"]
+    ctx.close()
+
+
 def test_probe_config_ns8():
     """Supplementary HBM-probe config (C3 shape, n_s = 8: 56 rows per KV head, one row tile)."""
     cfg = CONFIGS["probe_7b_ns8"].replace(num_layers=1)
