@@ -361,12 +361,13 @@ def test_global_heap_plan_matches_model(policy):
 
 
 # ---------------------------------------------------------------- sharded (logical, 1 GPU)
-@pytest.mark.parametrize("W,cyclic,n", [(2, False, 4000), (3, False, 4000), (4, False, 4000), (2, True, 4000),
-                                         (3, True, 4000), (3, True, 3990)])
-def test_sharded_logical_on_one_gpu(W, cyclic, n):
+@pytest.mark.parametrize("W,cyclic,n,vonly", [(2, False, 4000, False), (3, False, 4000, False), (4, False, 4000, False),
+                                               (2, True, 4000, False), (3, True, 4000, False), (3, True, 3990, False),
+                                               (2, True, 3990, True), (3, False, 4000, True)])
+def test_sharded_logical_on_one_gpu(W, cyclic, n, vonly):
     cfg = ShapeConfig("sh", 2, 8, 2, 128, n, 16, 10, 1000, "bf16")
     k = _k(cfg)
-    flags = CKV_FLAG_CYCLIC_SHARDS if cyclic else 0
+    flags = (CKV_FLAG_CYCLIC_SHARDS if cyclic else 0) | (CKV_FLAG_V_ONLY_STORE if vonly else 0)
     ctxs = [make_ctx(cfg, shard=g, W=W, prefetch=k // 2, flags=flags)[0] for g in range(W)]
     for l in range(cfg.num_layers):
         kp, vp = make_prefix(cfg, l)
