@@ -5,6 +5,8 @@
 //   A_j = sum_h sum_r 2^(lam2[h, r, j] - Lambda2[h, r])  (Eq. 1 with a_i the column sum
 //   of the row softmax over the query axis, Q2, Q4).
 // Reductions use a fixed order (no float atomics): run-to-run deterministic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "plan.cuh"
 
@@ -45,7 +47,8 @@ template <typename T>
 __global__ void __launch_bounds__(1024) row_lse_kernel(LayerGeom g, const float* __restrict__ lampart, int nsplit,
                                                        const T* __restrict__ q, const T* __restrict__ ks, int fullrow,
                                                        const float* __restrict__ lam_all, int W,
-                                                       float* __restrict__ Lam2, float* __restrict__ lam_local_out) {
+                                                       float* __restrict__ Lam2, float* __restrict__ lam_local_out,
+                                                       int transposed) {
   pdl_wait();
   pdl_trigger();
   __shared__ float sM[kSplitWarps][kRowsPerBlock + 1], sS[kSplitWarps][kRowsPerBlock + 1];
@@ -86,6 +89,25 @@ __global__ void __launch_bounds__(1024) row_lse_kernel(LayerGeom g, const float*
   sM[w][lane] = M;
   sS[w][lane] = S;
   __syncthreads();
+  if (!fullrow && transposed) {
+    // transposed merge: warp w merges row w's 32 split-group partials across its lanes (max, then
+    // rescaled sum, both by butterfly reductions -- a fixed order, so run-to-run deterministic)
+    const int row_w = blockIdx.x * kRowsPerBlock + w;
+    if (row_w >= nrows) return;
+    const float si = sS[lane][w], mi = si > 0.f ? sM[lane][w] : -INFINITY;
+    float Mt = mi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) Mt = fmaxf(Mt, __shfl_xor_sync(0xffffffffu, Mt, o));
+    float St = (Mt != -INFINITY && si > 0.f) ? si * fast_exp2(mi - Mt) : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) St += __shfl_xor_sync(0xffffffffu, St, o);
+    if (lane == 0) {
+      const float lse = (St > 0.f) ? Mt + fast_log2(St) : -INFINITY;
+      if (lam_all == nullptr && lam_local_out) lam_local_out[row_w] = lse;
+      Lam2[row_w] = lse;
+    }
+    return;
+  }
   if (w != 0) return;
   const int row_idx = blockIdx.x * kRowsPerBlock + lane;
   if (row_idx >= nrows) return;
@@ -191,8 +213,11 @@ cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit,
                            int fullrow, const float* lam_all, int W, float* Lam2, float* lam_local_out,
                            cudaStream_t st) {
   const int n = g.Hkv * g.R;
-  if (cudaError_t e_ = launch_kernel(row_lse_kernel<T>, (n + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kSplitWarps, 0, st, g, lampart, nsplit, q, k_suf, fullrow,
-                                                                             lam_all, W, Lam2, lam_local_out)) return e_;
+  static int tr = -1;  // A/B knob: CKV_LSE_SERIAL=1 keeps the one-warp serial merge
+  if (tr < 0) tr = (getenv("CKV_LSE_SERIAL") && getenv("CKV_LSE_SERIAL")[0] == '1') ? 0 : 1;
+  if (cudaError_t e_ = launch_kernel(row_lse_kernel<T>, (n + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kSplitWarps, 0, st,
+                                     g, lampart, nsplit, q, k_suf, fullrow, lam_all, W, Lam2, lam_local_out, tr))
+    return e_;
   return cudaGetLastError();
 }
 template cudaError_t launch_row_lse<float>(const LayerGeom&, const float*, int, const float*, const float*, int,
