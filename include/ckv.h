@@ -141,7 +141,10 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out);
 ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const void* v,
                             int64_t n_tokens, void* stream);
 
-/* One layer of the Re-Prefill hot path on one GPU (num_shards == 1), A1-A9.
+/* One layer of the Re-Prefill hot path, A1-A9: on one GPU (num_shards == 1), or on one rank of
+ * a position-sharded group (num_shards > 1, after ckv_exchange_open / ckv_exchange_attach: the
+ * exchanges of SURVEY §8(e) run inside the call over peer memory, see below; every rank
+ * returns the identical global ids and the identical merged `out`).
  *  q      device [n_suffix, Hq, d]  suffix queries (post-RoPE), cfg.dtype
  *  k_suf  device [n_suffix, Hkv, d] suffix keys;  v_suf same shape: suffix values
  *  out    device [n_suffix, Hq, d]  attention output, cfg.dtype
@@ -154,7 +157,7 @@ ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const vo
  * layers (exact ids) and the speculative load of the next period's first layer; the other
  * layers reuse the ids (selected_ids / chunk_scores report the period's).
  * Errors: CKV_EINVAL (null/range, 1 <= n_suffix <= max_suffix_len), CKV_ESTATE
- * (layer not stored, or num_shards > 1), CKV_ECUDA. */
+ * (layer not stored, or num_shards > 1 without an attached exchange), CKV_ECUDA. */
 ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const void* k_suf,
                                const void* v_suf, int32_t n_suffix, void* out,
                                int32_t* selected_ids, float* chunk_scores, void* stream);
@@ -191,6 +194,38 @@ ckv_status ckv_lse_merge_prepare(ckv_ctx* ctx, const float* o_part, const float*
                                  void* stream);
 ckv_status ckv_lse_merge_finish(ckv_ctx* ctx, const float* merge_buf, int32_t n_suffix,
                                 void* out, void* stream);
+
+/* ---- fused device-side exchange (SURVEY §8(e) + §8(f) NEXT-3) ----
+ * The same position-sharded algorithm as the split-phase calls above, but the exchanges run
+ * inside the library over peer memory (NVLink on a multi-GPU node), so a sharded layer is one
+ * ckv_reprefill_layer call per rank, capturable in one CUDA graph per rank:
+ * every ctx with num_shards = W > 1 owns an exchange WINDOW (device memory, identical layout on
+ * every rank).  Per layer, after each producing kernel the library broadcasts (or, for the
+ * partial outputs, scatters by row slice) its result straight into the peers' windows and
+ * increments a per-exchange counter in every peer's window (release at system scope); the
+ * consuming stream waits for the counter to reach W with a stream memory operation (no SM is
+ * held while waiting) and re-arms it.  Four exchanges per layer:
+ *   1. row normalisers  lam_g [Hq*n_s] float  -> all ranks     (global Lambda, rank order)
+ *   2. candidates       cand_g [k] uint64     -> all ranks     (identical merged top-k)
+ *   3. partial outputs  (O_g, lse_g) rows of slice s -> rank s (reduce-scatter over rows:
+ *                       rank s merges rows [s*ceil(n_s*Hq/W), ...) of every rank's partial)
+ *   4. merged rows      out slice s (cfg.dtype) -> all ranks   (all-gather), copied into `out`
+ * Bytes over the peer links per rank and layer (W ranks, n_s*Hq = N rows):
+ *   4*N*(W-1) + 8*k*(W-1) + (W-1)/W * N*(4d + 4) + (W-1)/W * N*d*e.
+ * Setup, once per ctx, after every rank's ckv_create:
+ *   multi-process (one process per GPU): ckv_exchange_handle on every rank -> all-gather the
+ *     64-byte handles in rank order (e.g. torch.distributed) -> ckv_exchange_open(handles);
+ *   one process driving several ranks (tests; several GPUs or logical ranks on one GPU):
+ *     ckv_exchange_attach(ctxs) with the W contexts in rank order.
+ * The peers must call ckv_reprefill_layer for the same layers in the same order with the
+ * same n_suffix (it is collective); each rank's stream blocks until its peers contribute.
+ * Errors: CKV_EINVAL (null, wrong count, num_shards == 1), CKV_ESTATE (already attached),
+ * CKV_ECUDA (IPC / peer-access failure), CKV_EUNSUPPORTED (W > 8). */
+#define CKV_EXCHANGE_HANDLE_BYTES 64
+ckv_status ckv_exchange_handle(ckv_ctx* ctx, void* handle_out /* host, 64 bytes */);
+ckv_status ckv_exchange_open(ckv_ctx* ctx, const void* handles /* host, W * 64 bytes, rank order */);
+ckv_status ckv_exchange_attach(ckv_ctx* ctx, ckv_ctx* const* ctxs /* host, W contexts, rank order */,
+                               int32_t num_ctxs);
 
 /* Change the Period p and subperiod sp (same meaning and limits as ckv_config.period /
  * .subperiod) between requests (before the next layer-0 call).  CKV_EINVAL / CKV_EUNSUPPORTED

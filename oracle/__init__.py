@@ -21,6 +21,10 @@ from .ckv_oracle import (  # noqa: F401
     chunk_scores,
     select_topk,
     score_gap,
+    parity_gate,
+    valid_relaxed_set,
+    GAP_GATE,
+    FLOOR_REL,
     kept_token_index,
     attention,
     lse_merge,

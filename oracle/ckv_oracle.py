@@ -142,13 +142,45 @@ def select_topk(A, k: int) -> np.ndarray:
 
 
 def score_gap(A, k: int) -> float:
-    """(A_(k) - A_(k+1)) / A_(k) of the sorted scores (Q11 gate); inf when k = m."""
+    """(A_(k) - A_(k+1)) / A_(k) of the scores sorted descending (SURVEY §8(c) Q11);
+    inf when k = m (no (k+1)-th score), 0 when A_(k) <= 0."""
     A = np.sort(_f64(A))[::-1]
-    if k >= A.shape[0]:
+    if not 1 <= k <= A.shape[0]:
+        raise ValueError("k out of range")
+    if k == A.shape[0]:
         return float("inf")
     if A[k - 1] <= 0:
         return 0.0
     return float((A[k - 1] - A[k]) / A[k - 1])
+
+
+GAP_GATE = 1e-3      # Q11: relative k/k+1 gap above which the selected set is unique in practice
+FLOOR_REL = 1e-30    # Q11: A_(k+1) at or below this share of sum(A) is fp32 underflow noise
+
+
+def parity_gate(A, k: int, gate: float = GAP_GATE, floor: float = FLOOR_REL) -> bool:
+    """True when the top-k set must be reproduced bit-exactly:
+    k = m, or gap (A_(k) - A_(k+1)) / A_(k) > gate AND A_(k+1) > floor * sum(A).
+    Otherwise several sets are correct (near-ties, or scores at the fp32 underflow floor)."""
+    A = _f64(A)
+    if k == A.shape[0]:
+        return True
+    s = np.sort(A)[::-1]
+    return bool(score_gap(A, k) > gate and s[k] > floor * A.sum())
+
+
+def valid_relaxed_set(A, k: int, ids, gate: float = GAP_GATE) -> bool:
+    """Q11 relaxed validity of a selected set when parity_gate is False: |ids| = k distinct
+    in-range ids, every chosen chunk scores >= A_(k)(1 - gate), and every chunk scoring
+    > A_(k)(1 + gate) is chosen -- only true near-ties of the k-th score may differ."""
+    A = _f64(A)
+    ids = np.asarray(ids, dtype=np.int64)
+    m = A.shape[0]
+    if ids.shape[0] != k or len(set(ids.tolist())) != k or ids.min() < 0 or ids.max() >= m:
+        return False
+    Ak = np.sort(A)[::-1][k - 1]
+    must = np.nonzero(A > Ak * (1 + gate))[0]
+    return bool(np.all(A[ids] >= Ak * (1 - gate)) and set(must.tolist()) <= set(ids.tolist()))
 
 
 def coverage_ratio(a, b) -> float:

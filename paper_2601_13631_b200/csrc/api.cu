@@ -59,6 +59,14 @@ struct ckv_ctx {
   int32_t* ticket = nullptr;     // grid ticket of the fused select kernel
   void* tmap_cache = nullptr;
   void* dense_kv = nullptr;  // tcgen05 attention: dense K/V tiles of the current layer
+  // fused device-side exchange (num_shards > 1; xchg.cuh)
+  char* xwin = nullptr;        // this rank's exchange window
+  XLayout xl{};
+  XPeers xp{};                 // window bases of all ranks (valid once attached)
+  bool x_attached = false;
+  std::vector<void*> x_opened;  // IPC-mapped peer windows (closed in ckv_destroy)
+  float* lam_loc = nullptr;     // [Hq * max_ns] this shard's row normalisers
+  uint64_t* cand_loc = nullptr; // [k] this shard's candidates
 
   cudaStream_t side = nullptr;
   cudaEvent_t ev_ids = nullptr;
@@ -272,7 +280,7 @@ PlanOut demand_plan_out(ckv_ctx* ctx, int layer, int32_t* ids_out) {
 ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, const void* q,
                       const void* ks, const void* vs, int ns, int include_suffix, void* out, float* o_f32,
                       float* lse_nat, int32_t* ids_out, bool planned, cudaStream_t st,
-                      cudaEvent_t after_slots = nullptr) {
+                      cudaEvent_t after_slots = nullptr, const XPartDst* xpd = nullptr) {
   // a prefetch of this layer that the stream already joined (before the score kernel) needs no
   // further event waits: they would only cut the programmatic launch edges of plan and attention
   const bool pf = ctx->pf_issued[layer] == ctx->epoch && ctx->pf_joined[layer] != ctx->epoch;
@@ -308,7 +316,7 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
                                ctx->rec_elems, ctx->kept_slots, ids, n_ids_dev, ctx->k, include_suffix, nsplit,
                                ctx->o_part, ctx->lse_part, st));
     LK(launch_attn_combine<float>(g, ctx->o_part, ctx->lse_part, nsplit, static_cast<float*>(out), o_f32, lse_nat,
-                                  st));
+                                  st, xpd));
   } else {
     cudaError_t e = cudaErrorNotSupported;
     if (ctx->attn_kind == 1) {
@@ -334,7 +342,7 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
     CK(e);
     ++ctx->launches;
     LK(launch_attn_combine<__nv_bfloat16>(g, ctx->o_part, ctx->lse_part, nsplit, static_cast<__nv_bfloat16*>(out),
-                                          o_f32, lse_nat, st));
+                                          o_f32, lse_nat, st, xpd));
   }
   PROF_END(5);
   if (after_slots) CK(cudaEventRecord(after_slots, st));  // SIMT path: the attention read the slots
@@ -361,6 +369,9 @@ void free_all(ckv_ctx* ctx) {
                       ctx->o_part, ctx->lse_part, ctx->stats, ctx->tmap_cache, ctx->dense_kv, ctx->epoch_dev, ctx->ticket};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
+  for (void* p : ctx->x_opened) cudaIpcCloseMemHandle(p);
+  for (void* p : {(void*)ctx->xwin, (void*)ctx->lam_loc, (void*)ctx->cand_loc})
+    if (p) cudaFree(p);
   if (ctx->host_store) cudaFreeHost(ctx->host_store);
   for (auto e : ctx->ev_pplan)
     if (e) cudaEventDestroy(e);
@@ -370,6 +381,78 @@ void free_all(ckv_ctx* ctx) {
   for (auto e : ctx->prof_pool)
     if (e) cudaEventDestroy(e);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+}
+
+// One layer on one rank of a position-sharded group with the fused device-side exchange
+// (xchg.cuh): every collective is a peer-memory write + counter
+// increment by this rank and a stream wait on its own counter -- no host round trip, no NCCL.
+ckv_status reprefill_sharded(ckv_ctx* ctx, int layer, const void* q, const void* k_suf, const void* v_suf, int ns,
+                             void* out, int32_t* selected_ids, float* chunk_scores, cudaStream_t st) {
+  const XPeers& xp = ctx->xp;
+  const XLayout& xl = ctx->xl;
+  const int W = ctx->W, self = ctx->shard;
+  char* win = ctx->xwin;
+  auto flag = [&](int f) { return static_cast<void*>(win + xl.flags + sizeof(uint32_t) * f); };
+  const size_t fl = xl.flags;
+  if (layer == 0) {
+    ++ctx->epoch;
+    LK(launch_epoch_inc(ctx->epoch_dev, st));
+  }
+  const int N = ns * ctx->Hq;  // output rows (r, h)
+  // 1. A1 on the local shard -> shard-local row normalisers; broadcast into slot `self`
+  int nsplit = 0;
+  ckv_status s = run_score(ctx, layer, q, k_suf, ns, ctx->lam_loc, &nsplit, st);
+  if (s != CKV_OK) return s;
+  LK(launch_xchg_put(xp, ctx->lam_loc, sizeof(float) * N, xl.lam + sizeof(float) * (size_t)self * N,
+                     fl + sizeof(uint32_t) * XF_LAM, st));
+  CK(xchg_wait(st, flag(XF_LAM), W));
+  // 2. global Lambda (rank order; FULLROW adds the causal suffix) -> local A_j -> candidates
+  LayerGeom g = geom(ctx, ns);
+  const float* lam_all = reinterpret_cast<const float*>(win + xl.lam);
+  PROF_BEGIN(1);
+  if (ctx->dtype == CKV_FP32)
+    LK(launch_row_lse<float>(g, nullptr, 0, static_cast<const float*>(q), static_cast<const float*>(k_suf),
+                             ctx->fullrow, lam_all, W, ctx->Lam2, nullptr, st));
+  else
+    LK(launch_row_lse<__nv_bfloat16>(g, nullptr, 0, static_cast<const __nv_bfloat16*>(q),
+                                     static_cast<const __nv_bfloat16*>(k_suf), ctx->fullrow, lam_all, W, ctx->Lam2,
+                                     nullptr, st));
+  PROF_END(1);
+  PROF_BEGIN(2);
+  LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
+  PROF_END(2);
+  PROF_BEGIN(6);
+  LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, ctx->j0, ctx->cyc_W > 0 ? ctx->cyc_W : 1,
+                        nullptr, ctx->cand_loc, ctx->k, nullptr, st));
+  PROF_END(6);
+  LK(launch_xchg_put(xp, ctx->cand_loc, sizeof(uint64_t) * ctx->k, xl.cand + sizeof(uint64_t) * (size_t)self * ctx->k,
+                     fl + sizeof(uint32_t) * XF_CAND, st));
+  CK(xchg_wait(st, flag(XF_CAND), W));
+  // 3. identical merged top-k on every rank; local plan / gather / attention (suffix on rank W-1);
+  //    the combine writes each partial row straight into the window of the rank merging its slice
+  int32_t* ids = ctx->ids_buf[layer & 1];
+  int32_t* nids = ctx->n_ids_buf[layer & 1];
+  LK(launch_topk_merge(reinterpret_cast<const uint64_t*>(win + xl.cand), W * ctx->k, ctx->k, ctx->m, ctx->j0, ctx->j1,
+                       ctx->cyc_W, ctx->flag, ctx->ids_glob, ids, nids, st));
+  if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st)) != CKV_OK) return s;
+  const int rps = (N + W - 1) / W;
+  XPartDst xd{xp, xl.part_o, xl.part_lse, rps, xl.rps_max, ctx->d};
+  if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, ns, self == W - 1, nullptr, nullptr, nullptr, nullptr,
+                      false, st, nullptr, &xd)) != CKV_OK)
+    return s;
+  LK(launch_xchg_put(xp, nullptr, 0, 0, fl + sizeof(uint32_t) * XF_PART, st));
+  CK(xchg_wait(st, flag(XF_PART), W));
+  // 4. merge this rank's slice over the W partials, broadcast the merged rows; copy out
+  if (ctx->dtype == CKV_FP32)
+    LK(launch_xchg_merge<float>(xp, xl, N, rps, ctx->d, st));
+  else
+    LK(launch_xchg_merge<__nv_bfloat16>(xp, xl, N, rps, ctx->d, st));
+  LK(launch_xchg_put(xp, nullptr, 0, 0, fl + sizeof(uint32_t) * XF_OUT, st));
+  CK(xchg_wait(st, flag(XF_OUT), W));
+  CK(cudaMemcpyAsync(out, win + xl.outs, (size_t)N * ctx->d * ctx->esz, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(selected_ids, ctx->ids_glob, sizeof(int32_t) * ctx->k, cudaMemcpyDeviceToDevice, st));
+  if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
+  return CKV_OK;
 }
 
 }  // namespace
@@ -403,6 +486,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   if (c.dtype != CKV_BF16 && c.dtype != CKV_FP32) return bad("dtype");
   if (c.chunk_size < 1 || c.prefix_len < 1 || c.max_suffix_len < 1) return bad("chunk_size/prefix_len/max_suffix_len");
   if (c.num_shards < 1 || c.shard_index < 0 || c.shard_index >= c.num_shards) return bad("shard_index/num_shards");
+  if (c.num_shards > kMaxPeers) return (delete ctx, CKV_EUNSUPPORTED);  // one node: <= 8 GPUs
   if (c.score_norm != CKV_NORM_PREFIX && c.score_norm != CKV_NORM_FULLROW) return bad("score_norm");
   ctx->L = c.num_layers;
   ctx->Hq = c.num_q_heads;
@@ -450,11 +534,11 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   // one shared pool: the next layer's speculative plan is issued only after this layer's demand plan
   // and compaction (ckv_reprefill_layer); periods (several in-flight prefetch plans) and shards are
   // not combined with it
-  if (ctx->global_heap && (ctx->period > 1 || ctx->W > 1)) return (delete ctx, CKV_EUNSUPPORTED);
   ctx->max_ns = c.max_suffix_len;
   ctx->period = c.period > 0 ? c.period : 1;
   ctx->subperiod = c.subperiod > 0 ? c.subperiod : 1;
   if (ctx->subperiod > ctx->period) return bad("subperiod > period");
+  if (ctx->global_heap && (ctx->period > 1 || ctx->W > 1)) return (delete ctx, CKV_EUNSUPPORTED);
   if (ctx->period > 1 && ctx->W > 1) return (delete ctx, CKV_EUNSUPPORTED);
   ctx->rec_elems = (int64_t)2 * ctx->Hkv * ctx->c * ctx->d;
   ctx->rec_swz = (ctx->dtype == CKV_BF16 && ctx->d == 128) ? 1 : 0;
@@ -565,6 +649,13 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
     CKC(cudaMalloc(&ctx->dense_kv, nb));
     CKC(cudaMemset(ctx->dense_kv, 0, nb));
   }
+  if (ctx->W > 1) {  // exchange window (fused device-side exchange, xchg.cuh)
+    ctx->xl = make_xlayout(ctx->W, ctx->Hq, ctx->max_ns, ctx->k, ctx->d, ctx->esz);
+    CKC(cudaMalloc(reinterpret_cast<void**>(&ctx->xwin), ctx->xl.total));
+    CKC(cudaMemset(ctx->xwin, 0, ctx->xl.total));
+    CKC(dalloc(&ctx->lam_loc, (size_t)ctx->Hq * ctx->max_ns));
+    CKC(dalloc(&ctx->cand_loc, (size_t)ctx->k));
+  }
   CKC(cudaDeviceSynchronize());
 #undef CKC
   (void)st;
@@ -644,10 +735,13 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
   ctx->err.clear();
   ckv_status s = check_layer_call(ctx, layer, n_suffix);
   if (s != CKV_OK) return s;
-  if (ctx->W != 1) return fail(ctx, CKV_ESTATE, "ckv_reprefill_layer needs num_shards == 1; use ckv_shard_*");
   if (!q || !k_suf || !v_suf || !out || !selected_ids) return fail(ctx, CKV_EINVAL, "null argument");
+  if (ctx->W != 1 && !ctx->x_attached)
+    return fail(ctx, CKV_ESTATE, "num_shards > 1: attach the exchange (ckv_exchange_open / _attach) or use ckv_shard_*");
   CK(cudaSetDevice(ctx->cfg.device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (ctx->W != 1)
+    return reprefill_sharded(ctx, layer, q, k_suf, v_suf, n_suffix, out, selected_ids, chunk_scores, st);
   if (layer == 0) {
     ++ctx->epoch;
     LK(launch_epoch_inc(ctx->epoch_dev, st));
@@ -663,7 +757,7 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     // The persistent score kernel needs every SM: side-stream prefetch work for this layer must
     // not still be resident when it starts (one late CTA delays the whole statically partitioned
     // launch), so the prefetch is joined here rather than only before the attention.
-    static const bool side_sync = !(getenv("CKV_SIDE_SYNC") && getenv("CKV_SIDE_SYNC")[0] == '0');
+    static const bool side_sync = !(tuning_env("CKV_SIDE_SYNC") && tuning_env("CKV_SIDE_SYNC")[0] == '0');
     if (side_sync && ctx->pf_issued[layer] == ctx->epoch) {
       CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
       pdl_mark_event_wait(st);
@@ -672,41 +766,12 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     int nsplit = 0;
     if ((s = run_score(ctx, layer, q, k_suf, n_suffix, nullptr, &nsplit, st)) != CKV_OK) return s;
     LayerGeom g = geom(ctx, n_suffix);
-    // measured on B200 (C3, graph replay): 96.3 us/layer fused vs 92.2 separate (the separate kernels'
-    // launches overlap through PDL; the fused tail runs the same single-CTA work) -> opt-in only
-    static const bool fuse_select = getenv("CKV_FUSED_SELECT") && getenv("CKV_FUSED_SELECT")[0] == '1';
-    if (fuse_select && chunk_sum_select_supported(g)) {
-      // A2 chunk sums + A3 top-k (+ A4 plan + A9 when this layer's prefetch is joined) in one launch
-      planned = ctx->pf_issued[layer] != ctx->epoch || ctx->pf_joined[layer] == ctx->epoch;
-      SelectPlanArgs a{ctx->A, ctx->k, ids, nids, ctx->ticket, planned ? 1 : 0, cache_layer(ctx, layer), ctx->epoch,
-                       ctx->rec_bytes, ctx->scratch_main, demand_plan_out(ctx, layer, selected_ids)};
-      PROF_BEGIN(2);
-      LK(launch_chunk_sum_select(g, ctx->lam2, ctx->Lam2, ctx->Apart, a, st));
-      PROF_END(2);
-    } else {
-      PROF_BEGIN(2);
-      LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
-      PROF_END(2);
-      PROF_BEGIN(6);
-      // A3 + A4 in one CTA when this layer's prefetch is already joined (or none was issued)
-      // measured on B200 (C3, graph replay): 90.5 us/layer fused vs 89.0 separate -> opt-in only
-      static const bool topk_plan = getenv("CKV_TOPK_PLAN") && getenv("CKV_TOPK_PLAN")[0] == '1';
-      cudaError_t e = cudaErrorNotSupported;
-      if (topk_plan && (ctx->pf_issued[layer] != ctx->epoch || ctx->pf_joined[layer] == ctx->epoch)) {
-        SelectPlanArgs a{ctx->A, ctx->k, ids, nids, nullptr, 1, cache_layer(ctx, layer), ctx->epoch,
-                         ctx->rec_bytes, ctx->scratch_main, demand_plan_out(ctx, layer, selected_ids)};
-        e = launch_topk_plan(ctx->Apart, ctx->Hkv, ctx->m_loc, a, st);
-        if (e == cudaSuccess) {
-          planned = true;
-          ++ctx->launches;
-        }
-      }
-      if (e == cudaErrorNotSupported)
-        LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, nullptr, 0, nids, st));
-      else
-        CK(e);
-      PROF_END(6);
-    }
+    PROF_BEGIN(2);
+    LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
+    PROF_END(2);
+    PROF_BEGIN(6);
+    LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, nullptr, 0, nids, st));
+    PROF_END(6);
     // intra-period loads (exact ids) for the period's other layers, then the speculative load of
     // the next period's first layer (A6), all on the side stream in layer order
     // (global heap: one shared pool, so the next layer's speculative plan may only run after this
@@ -816,6 +881,72 @@ ckv_status ckv_lse_merge_finish(ckv_ctx* ctx, const float* merge_buf, int32_t n_
   else
     LK(launch_lse_merge_finish<__nv_bfloat16>(n_suffix * ctx->Hq, ctx->d, merge_buf,
                                               static_cast<__nv_bfloat16*>(out), st));
+  return CKV_OK;
+}
+
+ckv_status ckv_exchange_handle(ckv_ctx* ctx, void* handle_out) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!handle_out) return fail(ctx, CKV_EINVAL, "null handle_out");
+  if (ctx->W < 2 || !ctx->xwin) return fail(ctx, CKV_EINVAL, "num_shards == 1: no exchange window");
+  static_assert(sizeof(cudaIpcMemHandle_t) == CKV_EXCHANGE_HANDLE_BYTES, "IPC handle size");
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ctx->xwin));
+  memcpy(handle_out, &h, sizeof h);
+  return CKV_OK;
+}
+
+ckv_status ckv_exchange_open(ckv_ctx* ctx, const void* handles) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!handles) return fail(ctx, CKV_EINVAL, "null handles");
+  if (ctx->W < 2 || !ctx->xwin) return fail(ctx, CKV_EINVAL, "num_shards == 1: no exchange window");
+  if (ctx->x_attached) return fail(ctx, CKV_ESTATE, "exchange already attached");
+  CK(cudaSetDevice(ctx->cfg.device));
+  XPeers xp{};
+  xp.W = ctx->W;
+  xp.self = ctx->shard;
+  for (int g = 0; g < ctx->W; ++g) {
+    if (g == ctx->shard) {
+      xp.base[g] = ctx->xwin;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char*>(handles) + (size_t)g * sizeof h, sizeof h);
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->x_opened.push_back(p);
+    xp.base[g] = static_cast<char*>(p);
+  }
+  ctx->xp = xp;
+  ctx->x_attached = true;
+  return CKV_OK;
+}
+
+ckv_status ckv_exchange_attach(ckv_ctx* ctx, ckv_ctx* const* ctxs, int32_t num_ctxs) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!ctxs || num_ctxs != ctx->W) return fail(ctx, CKV_EINVAL, "need num_shards contexts in rank order");
+  if (ctx->W < 2 || !ctx->xwin) return fail(ctx, CKV_EINVAL, "num_shards == 1: no exchange window");
+  if (ctx->x_attached) return fail(ctx, CKV_ESTATE, "exchange already attached");
+  XPeers xp{};
+  xp.W = ctx->W;
+  xp.self = ctx->shard;
+  for (int g = 0; g < ctx->W; ++g) {
+    const ckv_ctx* o = ctxs[g];
+    if (!o || o->W != ctx->W || o->shard != g || !o->xwin || o->xl.total != ctx->xl.total)
+      return fail(ctx, CKV_EINVAL, "context %d is not rank %d of this group", g, g);
+    if (o->cfg.device != ctx->cfg.device) {  // several GPUs in one process: map the peer
+      CK(cudaSetDevice(ctx->cfg.device));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(o->cfg.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else CK(e);
+    }
+    xp.base[g] = o->xwin;
+  }
+  ctx->xp = xp;
+  ctx->x_attached = true;
   return CKV_OK;
 }
 
@@ -1013,29 +1144,6 @@ bool pdl_take_event_wait(cudaStream_t st) {
     }
   return false;
 }
-static bool name_listed(const void* kern, const char* list_env) {
-  if (!list_env || !*list_env) return false;
-  const char* name = nullptr;
-  if (cudaFuncGetName(&name, kern) != cudaSuccess || !name) return false;
-  std::string list(list_env);
-  size_t pos = 0;
-  while (pos <= list.size()) {
-    size_t e = list.find(',', pos);
-    if (e == std::string::npos) e = list.size();
-    const std::string tok = list.substr(pos, e - pos);
-    if (!tok.empty() && strstr(name, tok.c_str())) return true;
-    pos = e + 1;
-  }
-  return false;
-}
-bool pdl_skip_kernel(const void* kern) {
-  static const char* skip = getenv("CKV_PDL_SKIP");
-  return name_listed(kern, skip);
-}
-bool knocked_out(const void* kern) {
-  static const char* ko = getenv("CKV_KNOCKOUT");
-  return name_listed(kern, ko);
-}
 // Debug timeline (CKV_TIMELINE=1): an event after every kernel launch (also inside graph capture,
 // as event-record nodes -- they break the programmatic edges, so this measures a PDL-free
 // schedule); ckv_destroy prints the last 400 entries (end time of each kernel, us, relative).
@@ -1047,7 +1155,7 @@ struct TlEntry {
 static std::vector<TlEntry> g_tl;
 static size_t g_tl_pos = 0;
 void timeline_mark(const void* kern, cudaStream_t st) {
-  static const bool on = getenv("CKV_TIMELINE") && getenv("CKV_TIMELINE")[0] == '1';
+  static const bool on = tuning_env("CKV_TIMELINE") && tuning_env("CKV_TIMELINE")[0] == '1';
   if (!on) return;
   if (g_tl.empty()) {
     g_tl.resize(400);
@@ -1083,7 +1191,7 @@ void timeline_dump() {
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("CKV_PDL");
+    const char* e = tuning_env("CKV_PDL");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;

@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include "xchg.cuh"
+
 namespace ckv {
 
 // ---- programmatic dependent launch (PDL) ----
@@ -20,24 +22,32 @@ namespace ckv {
 // prefetches may precede pdl_wait().
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-bool pdl_enabled();  // CKV_PDL=0 disables the launch attribute (A/B measurements)
+bool pdl_enabled();  // tuning build: CKV_PDL=0 disables the launch attribute (A/B measurements)
 // A kernel that follows a cross-stream event wait is launched without the attribute (the
 // programmatic relaxation must not weaken the event dependency); api.cu marks such streams.
 void pdl_mark_event_wait(cudaStream_t st);
 bool pdl_take_event_wait(cudaStream_t st);  // true (and cleared) if st was marked
-bool pdl_skip_kernel(const void* kern);     // debug: CKV_PDL_SKIP=name,name,... (substring match)
-bool knocked_out(const void* kern);         // timing experiments only: CKV_KNOCKOUT=name,... not launched
-void timeline_mark(const void* kern, cudaStream_t st);  // debug: CKV_TIMELINE=1 event after each launch
+void timeline_mark(const void* kern, cudaStream_t st);  // tuning build: CKV_TIMELINE=1 event after each launch
+// Environment knobs exist only in the tuning build (-DCKV_TUNING, `build.py --tuning` ->
+// libckv_tuning.so, used by scripts/ for A/B measurements).  The product library reads no
+// environment variable: tuning_env() returns nullptr there, so every knob takes its default.
+inline const char* tuning_env(const char* name) {
+#ifdef CKV_TUNING
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                                  Args&&... args) {
-  if (knocked_out(reinterpret_cast<const void*>(kern))) return cudaSuccess;  // results invalid (timing only)
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   const bool after_wait = pdl_take_event_wait(st);
   attr[0].val.programmaticStreamSerializationAllowed =
-      (pdl_enabled() && !after_wait && !pdl_skip_kernel(reinterpret_cast<const void*>(kern))) ? 1 : 0;
+      (pdl_enabled() && !after_wait) ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -181,26 +191,6 @@ struct PlanOut {
   int mark_miss = 0;  // kept_slots of a miss = -(slot + 2): the consumer (compact_kv) loads it from the
                       // host store itself and fills the slot (no separate gather launch)
 };
-// A2 chunk sums -> A3 top-k -> A4 plan in one launch (k_reduce.cu)
-struct SelectPlanArgs {
-  float* A;           // [m_loc] out: A_j
-  int k;              // budget chunks
-  int32_t* ids;       // [k] out: selected ids, ascending
-  int32_t* n_ids;     // [1] out
-  int32_t* ticket;    // [1] zero-initialised grid ticket (reset by the last CTA)
-  int plan;           // also run the demand plan of this layer
-  CacheLayer cl;
-  int epoch;
-  int64_t rec_bytes;
-  int32_t* scratch;
-  PlanOut out;
-};
-bool chunk_sum_select_supported(const LayerGeom& g);
-// A3 top-k + A4 demand plan in one single-CTA launch (k_cache.cu); cudaErrorNotSupported if m or the
-// pool is too large (nothing launched)
-cudaError_t launch_topk_plan(const float* Apart, int nparts, int m, const SelectPlanArgs& a, cudaStream_t st);
-cudaError_t launch_chunk_sum_select(const LayerGeom& g, const float* lam2, const float* Lam2, float* Apart,
-                                    const SelectPlanArgs& a, cudaStream_t st);
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t* scratch64,
                               int32_t* scratch32, PlanOut out, cudaStream_t st);
@@ -235,7 +225,13 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                            const __nv_bfloat16* probe_layer, cudaEvent_t after_compact, cudaStream_t st);
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit,
-                                T* out, float* o_f32, float* lse_nat, cudaStream_t st);
+                                T* out, float* o_f32, float* lse_nat, cudaStream_t st, const XPartDst* xd = nullptr);
+// fused exchange (k_xchg.cu, xchg.cuh)
+cudaError_t launch_xchg_put(const XPeers& xp, const void* src, size_t bytes, size_t dst_off, size_t flag_off,
+                            cudaStream_t st);
+template <typename T>
+cudaError_t launch_xchg_merge(const XPeers& xp, const XLayout& xl, int N, int rps, int d, cudaStream_t st);
+cudaError_t xchg_wait(cudaStream_t st, void* flag_dev, uint32_t target);
 cudaError_t launch_lse_merge_prepare(int rows, int d, const float* o, const float* lse, const float* lse_max,
                                      float* buf, cudaStream_t st);
 template <typename T>

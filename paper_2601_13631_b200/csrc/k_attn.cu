@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(NT) attn_simt_kernel(LayerGeom g, const T* __r
 template <typename T>
 __global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_part, const float* __restrict__ lse_part,
                                     int nsplit, T* __restrict__ out, float* __restrict__ o_f32,
-                                    float* __restrict__ lse_nat) {
+                                    float* __restrict__ lse_nat, XPartDst xd) {
   pdl_wait();
   pdl_trigger();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // kvh * R + rho
@@ -215,6 +215,14 @@ __global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_par
   for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
   const int64_t obase = ((int64_t)r * g.Hq + h) * g.d;
   const float inv = den > 0.f ? 1.f / den : 0.f;
+  // fp32 row destination: the caller's o_f32, or (fused exchange) slot `self` of the window of the
+  // rank that merges this row's slice (reduce-scatter over output rows, xchg.cuh)
+  if (xd.xp.W > 0) {
+    const int row_out = r * g.Hq + h, s = row_out / xd.rps, lr = row_out - s * xd.rps;
+    char* wb = xd.xp.base[s];
+    o_f32 = reinterpret_cast<float*>(wb + xd.part_o) + ((size_t)xd.xp.self * xd.rps_max + lr) * g.d - obase;
+    lse_nat = reinterpret_cast<float*>(wb + xd.part_lse) + (size_t)xd.xp.self * xd.rps_max + lr - row_out;
+  }
   if ((g.d & 127) == 0 && nsplit <= 8) {
     // all split loads issued before the weighted sum (independent 16-byte loads in flight)
     for (int x = lane * 4; x < g.d; x += 128) {
@@ -329,8 +337,12 @@ cudaError_t launch_attn_simt(const LayerGeom& g, const T* q, const T* k_suf, con
 
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit, T* out,
-                                float* o_f32, float* lse_nat, cudaStream_t st) {
-  if (cudaError_t e_ = launch_kernel(attn_combine_kernel<T>, (g.Hkv * g.R + 7) / 8, 256, 0, st, g, o_part, lse_part, nsplit, out, o_f32, lse_nat)) return e_;
+                                float* o_f32, float* lse_nat, cudaStream_t st, const XPartDst* xd) {
+  XPartDst x{};
+  if (xd) x = *xd;
+  if (cudaError_t e_ = launch_kernel(attn_combine_kernel<T>, (g.Hkv * g.R + 7) / 8, 256, 0, st, g, o_part, lse_part,
+                                     nsplit, out, o_f32, lse_nat, x))
+    return e_;
   return cudaGetLastError();
 }
 
@@ -351,7 +363,7 @@ cudaError_t launch_lse_merge_finish(int rows, int d, const float* buf, T* out, c
                                            const int32_t*, const int32_t*, const int32_t*, int, int, int, float*,   \
                                            float*, cudaStream_t);                                                   \
   template cudaError_t launch_attn_combine<T>(const LayerGeom&, const float*, const float*, int, T*, float*, float*, \
-                                              cudaStream_t);                                                        \
+                                              cudaStream_t, const XPartDst*);                                                        \
   template cudaError_t launch_lse_merge_finish<T>(int, int, const float*, T*, cudaStream_t);
 CKV_INST(float)
 CKV_INST(__nv_bfloat16)

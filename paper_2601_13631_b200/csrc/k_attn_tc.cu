@@ -535,7 +535,7 @@ int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix) {
   int s = sm_count() / (g.Hkv * MT);
   static int force = -1;  // tuning knob CKV_ATTN_SPLITS (results unchanged, only the split count)
   if (force < 0) {
-    const char* e = getenv("CKV_ATTN_SPLITS");
+    const char* e = tuning_env("CKV_ATTN_SPLITS");
     force = (e && atoi(e) > 0) ? atoi(e) : 0;
   }
   if (force > 0) s = force;
@@ -596,7 +596,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   static int trace_mode = -1;
   static unsigned long long* trace_buf = nullptr;
   if (trace_mode < 0) {
-    const char* ev = getenv("CKV_ATTN_TRACE");
+    const char* ev = tuning_env("CKV_ATTN_TRACE");
     trace_mode = (ev && ev[0] == '1') ? 1 : 0;
     if (trace_mode) cudaMalloc(&trace_buf, 7 * 32 * sizeof(unsigned long long));
   }

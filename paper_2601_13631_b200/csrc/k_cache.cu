@@ -33,19 +33,6 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
                       smem_keys ? plan_skeys : nullptr);
 }
 
-// A3 top-k followed by this layer's A4 demand plan (+ A9) in the same CTA: one launch boundary
-// less on the layer's critical path (the chunk sums stay a separate, wide kernel).
-template <int KPT>
-__global__ void __launch_bounds__(NT) topk_plan_kernel(const float* __restrict__ Apart, SelectPlanArgs a, int nparts,
-                                                       int m) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ PlanSmem ps;
-  topk_body<NT, KPT>(a.A, Apart, nparts, m, a.k, 0, 1, a.ids, nullptr, 0, a.n_ids, ps.ss);
-  __syncthreads();
-  cache_plan_body<NT>(a.cl, a.ids, min(a.k, m), 0, 0, a.epoch, a.rec_bytes, a.scratch, a.out, ps);
-}
-
 // Whole-record copy host store -> HBM slot: work items are 4 KiB segments of records so a
 // few misses still keep many 16-B loads in flight over the host link.
 constexpr int GATHER_SEG = 4096;
@@ -168,28 +155,11 @@ cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const in
   return cudaGetLastError();
 }
 
-cudaError_t launch_topk_plan(const float* Apart, int nparts, int m, const SelectPlanArgs& a, cudaStream_t st) {
-  if (a.cl.P > NT * kPlanKPT) return cudaErrorNotSupported;  // large pools: the standalone planner
-  cudaError_t e_;
-  if (m <= NT)
-    e_ = launch_kernel(topk_plan_kernel<1>, 1, NT, 0, st, Apart, a, nparts, m);
-  else if (m <= 2 * NT)
-    e_ = launch_kernel(topk_plan_kernel<2>, 1, NT, 0, st, Apart, a, nparts, m);
-  else if (m <= 4 * NT)
-    e_ = launch_kernel(topk_plan_kernel<4>, 1, NT, 0, st, Apart, a, nparts, m);
-  else if (m <= 8 * NT)
-    e_ = launch_kernel(topk_plan_kernel<8>, 1, NT, 0, st, Apart, a, nparts, m);
-  else
-    return cudaErrorNotSupported;
-  if (e_) return e_;
-  return cudaGetLastError();
-}
-
 cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
                           char* pool_layer, int64_t rec_bytes, cudaStream_t st) {
   static int blocks = 0;
   if (!blocks) {  // tuning knob (CKV_GATHER_BLOCKS), default GATHER_BLOCKS
-    const char* e = getenv("CKV_GATHER_BLOCKS");
+    const char* e = tuning_env("CKV_GATHER_BLOCKS");
     blocks = (e && atoi(e) > 0) ? atoi(e) : GATHER_BLOCKS;
   }
   if (cudaError_t e_ = launch_kernel(gather_kernel, blocks, GATHER_THREADS, 0, st, gather_list, n_load, host_layer_dev,

@@ -180,32 +180,6 @@ __global__ void chunk_sum_kernel(LayerGeom g, const float* __restrict__ lam2, co
   chunk_sum_warp(g, lam2, Lam2, Apart, warp, threadIdx.x & 31);
 }
 
-// A2 chunk sums -> A3 top-k -> A4 demand plan (+ A9) in one launch: every CTA sums its chunks;
-// the last CTA to finish (atomic ticket after a release fence) reads all partials and runs the
-// top-k and the planner, so the layer's selection costs one kernel boundary instead of three.
-template <int KPT>
-__global__ void __launch_bounds__(1024) chunk_sum_select_kernel(LayerGeom g, const float* __restrict__ lam2,
-                                                                const float* __restrict__ Lam2,
-                                                                float* __restrict__ Apart, SelectPlanArgs a) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ PlanSmem ps;
-  __shared__ int s_last;
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (warp < g.m_loc * g.Hkv) chunk_sum_warp(g, lam2, Lam2, Apart, warp, threadIdx.x & 31);
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(a.ticket, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  topk_body<1024, KPT>(a.A, Apart, g.Hkv, g.m_loc, a.k, 0, 1, a.ids, nullptr, 0, a.n_ids, ps.ss);
-  __syncthreads();
-  if (threadIdx.x == 0) *a.ticket = 0;  // ready for the next launch (stream-ordered)
-  if (a.plan)
-    cache_plan_body<1024>(a.cl, a.ids, min(a.k, g.m_loc), 0, 0, a.epoch, a.rec_bytes, a.scratch, a.out, ps);
-}
-
 }  // namespace
 
 template <typename T>
@@ -214,7 +188,7 @@ cudaError_t launch_row_lse(const LayerGeom& g, const float* lampart, int nsplit,
                            cudaStream_t st) {
   const int n = g.Hkv * g.R;
   static int tr = -1;  // A/B knob: CKV_LSE_SERIAL=1 keeps the one-warp serial merge
-  if (tr < 0) tr = (getenv("CKV_LSE_SERIAL") && getenv("CKV_LSE_SERIAL")[0] == '1') ? 0 : 1;
+  if (tr < 0) tr = (tuning_env("CKV_LSE_SERIAL") && tuning_env("CKV_LSE_SERIAL")[0] == '1') ? 0 : 1;
   if (cudaError_t e_ = launch_kernel(row_lse_kernel<T>, (n + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kSplitWarps, 0, st,
                                      g, lampart, nsplit, q, k_suf, fullrow, lam_all, W, Lam2, lam_local_out, tr))
     return e_;
@@ -225,26 +199,6 @@ template cudaError_t launch_row_lse<float>(const LayerGeom&, const float*, int, 
 template cudaError_t launch_row_lse<__nv_bfloat16>(const LayerGeom&, const float*, int, const __nv_bfloat16*,
                                                    const __nv_bfloat16*, int, const float*, int, float*, float*,
                                                    cudaStream_t);
-
-bool chunk_sum_select_supported(const LayerGeom& g) { return g.m_loc <= 8 * 1024; }
-
-cudaError_t launch_chunk_sum_select(const LayerGeom& g, const float* lam2, const float* Lam2, float* Apart,
-                                    const SelectPlanArgs& a, cudaStream_t st) {
-  const int blocks = (g.m_loc * g.Hkv + 31) / 32;
-  cudaError_t e_;
-  if (g.m_loc <= 1024)
-    e_ = launch_kernel(chunk_sum_select_kernel<1>, blocks, 1024, 0, st, g, lam2, Lam2, Apart, a);
-  else if (g.m_loc <= 2048)
-    e_ = launch_kernel(chunk_sum_select_kernel<2>, blocks, 1024, 0, st, g, lam2, Lam2, Apart, a);
-  else if (g.m_loc <= 4096)
-    e_ = launch_kernel(chunk_sum_select_kernel<4>, blocks, 1024, 0, st, g, lam2, Lam2, Apart, a);
-  else if (g.m_loc <= 8192)
-    e_ = launch_kernel(chunk_sum_select_kernel<8>, blocks, 1024, 0, st, g, lam2, Lam2, Apart, a);
-  else
-    return cudaErrorNotSupported;
-  if (e_) return e_;
-  return cudaGetLastError();
-}
 
 cudaError_t launch_chunk_sum(const LayerGeom& g, const float* lam2, const float* Lam2, float* Apart,
                              cudaStream_t st) {

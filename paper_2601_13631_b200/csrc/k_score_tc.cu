@@ -44,7 +44,6 @@ struct TcParams {
   int q_direct;  // 1: Q tiles straight from q [ns][Hq][128] by a 3-D map (n_s % 128 == 0), no pack
   int n_units;  // Hkv * NKT * MT
   float scale;  // log2(e) / sqrt(d)
-  int dephase;  // tuning: start delay (cycles) of odd column-quarter warps
 };
 
 // In-place pairwise tree: after the call a[0..N/G) hold sums of consecutive groups of G.
@@ -177,35 +176,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (pr != cur) {
           const int kb = kcount & 1;
           ptx::mbar_wait_sleep(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
-          if constexpr (NP >= 13) {  // tuning: no K traffic
-            ptx::mbar_arrive(&k_full[kb]);
-          } else {
-            ptx::mbar_expect_tx(&k_full[kb], kKBytes);
-            const int y = kvh * p.g.n_pad + kt * BN;
-            uint8_t* dst = kbuf0 + kb * kKBytes;
-            ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
-            ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
-          }
+          ptx::mbar_expect_tx(&k_full[kb], kKBytes);
+          const int y = kvh * p.g.n_pad + kt * BN;
+          uint8_t* dst = kbuf0 + kb * kKBytes;
+          ptx::tma_load_2d(dst, &tmK, &k_full[kb], 0, y);
+          ptx::tma_load_2d(dst + kKBytes / 2, &tmK, &k_full[kb], 64, y);
           cur = pr;
           ++kcount;
         }
         const int qs = qcount % kQStages;
         ptx::mbar_wait_sleep(&q_empty[qs], ((qcount / kQStages) & 1) ^ 1);
         if (qcount == 0) pdl_wait();  // Q is the previous kernel's output (the probe keys are not)
-        if constexpr (NP >= 12) {  // tuning: no Q traffic
-          ptx::mbar_arrive(&q_full[qs]);
+        ptx::mbar_expect_tx(&q_full[qs], kQBytes);
+        uint8_t* dq = qbuf0 + qs * kQBytes;
+        if (p.q_direct) {  // a 128-row tile is 128 consecutive tokens of one query head
+          const int rho0 = mt * BM, gq = rho0 / p.g.ns, r0 = rho0 - gq * p.g.ns, head = kvh * p.g.G + gq;
+          ptx::tma_load_3d(dq, &tmQ, &q_full[qs], 0, head, r0);
+          ptx::tma_load_3d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, head, r0);
         } else {
-          ptx::mbar_expect_tx(&q_full[qs], kQBytes);
-          uint8_t* dq = qbuf0 + qs * kQBytes;
-          if (p.q_direct) {  // a 128-row tile is 128 consecutive tokens of one query head
-            const int rho0 = mt * BM, gq = rho0 / p.g.ns, r0 = rho0 - gq * p.g.ns, head = kvh * p.g.G + gq;
-            ptx::tma_load_3d(dq, &tmQ, &q_full[qs], 0, head, r0);
-            ptx::tma_load_3d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, head, r0);
-          } else {
-            const int yq = kvh * p.R_pad + mt * BM;
-            ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
-            ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
-          }
+          const int yq = kvh * p.R_pad + mt * BM;
+          ptx::tma_load_2d(dq, &tmQ, &q_full[qs], 0, yq);
+          ptx::tma_load_2d(dq + kQBytes / 2, &tmQ, &q_full[qs], 64, yq);
         }
         ++qcount;
       }
@@ -232,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t qa = ptx::smem_u32(qbuf0 + qs * kQBytes);
         const uint32_t ka = ptx::smem_u32(kbuf0 + kb * kKBytes);
 #pragma unroll
-        for (int k = 0; k < (NP == 14 ? 0 : D / 16); ++k) {  // 14: tuning, epilogue alone
+        for (int k = 0; k < D / 16; ++k) {
           const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
           const uint32_t off_k = (k >> 2) * (kKBytes / 2) + (k & 3) * 32;
           ptx::mma_bf16(d_tmem, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k), idesc,
@@ -256,11 +247,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const int nfull = p.g.n_loc / BN;  // key tiles without a ragged tail
     int acount = 0;
-    if (p.dephase > 0 && (half & 1)) {  // start half of the warps of every SMSP later (de-phase)
-      const long long t0 = clock64();
-      while (clock64() - t0 < p.dephase) {
-      }
-    }
     UnitIter it(u0, p.MT, p.NKT);
     for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT)) {
       const int mt = it.mt(p.MT), kvh = it.kvh, kt = it.kt;
@@ -278,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = rho < p.g.R;
       // both 32-key groups are read from TMEM, then the accumulator is released at once
       float v[64];
-      if constexpr (NP < 11 || NP == 14) {
+      {
         uint32_t r0[32], r1[32];
         const uint32_t ta = tmem_base + (uint32_t)(ab * BN + half * (BN / kColSplit)) + lane_off;
         ptx::tmem_ld32_nowait(ta, r0);
@@ -297,11 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int key0 = kt * BN + half * (BN / kColSplit);
       float* lamrow = p.lam2 + ((size_t)kvh * p.g.m_loc + key0 / C) * p.g.R + rho;
       float* lp = p.lampart + ((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho;
-      if constexpr (NP >= 11 && NP <= 13) {  // tuning skeleton: pipeline only
-        if (row_ok) *lp = 0.f;
-      } else if constexpr (NP == 10) {  // tuning: TMEM drain only
-        if (row_ok) *lp = v[0] + v[63];
-      } else if (kt >= nfull) {  // warp-uniform: the last key tile only
+      if (kt >= nfull) {  // warp-uniform: the last key tile only
         epilogue_unit<C, NP, true>(p, v, key0, lamrow, lp, row_ok);
       } else {
         epilogue_unit<C, NP, false>(p, v, key0, lamrow, lp, row_ok);
@@ -363,9 +345,9 @@ cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPa
 int poly_share() {
   static int np = -1;
   if (np < 0) {
-    const char* e = getenv("CKV_SCORE_POLY");
+    const char* e = tuning_env("CKV_SCORE_POLY");
     np = e ? atoi(e) : 1;  // measured on B200: 1 of 8 exponentials on the FMA pipe is fastest
-    if (np < 0 || (np > 3 && np < 10) || np > 14) np = 0;
+    if (np < 0 || np > 3) np = 0;
   }
   return np;
 }
@@ -374,11 +356,6 @@ template <int C>
 cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
   switch (poly_share()) {
     case 3: return launch_cp<C, 3>(tmK, tmQ, p, grid, st);
-    case 10: return launch_cp<C, 10>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
-    case 11: return launch_cp<C, 11>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
-    case 12: return launch_cp<C, 12>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
-    case 14: return launch_cp<C, 14>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
-    case 13: return launch_cp<C, 13>(tmK, tmQ, p, grid, st);  // tuning only: results invalid
     case 2: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
     case 1: return launch_cp<C, 1>(tmK, tmQ, p, grid, st);
     default: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
@@ -410,14 +387,6 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   p.R_pad = p.MT * BM;
   p.n_units = g.Hkv * p.NKT * p.MT;
   p.scale = kLog2e / sqrtf((float)g.d);
-  {
-    static int dp = -1;
-    if (dp < 0) {
-      const char* e = getenv("CKV_SCORE_DEPHASE");
-      dp = e ? atoi(e) : 0;
-    }
-    p.dephase = dp;
-  }
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
   p.q_direct = (g.ns % BM) == 0 ? 1 : 0;
   if (!p.q_direct)

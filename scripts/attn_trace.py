@@ -1,5 +1,6 @@
 """Debug: per-event timeline of CTA 0 of the tcgen05 attention kernel (CKV_ATTN_TRACE=1)."""
 import os, sys
+os.environ.setdefault("CKV_LIBRARY", "tuning")  # env knobs exist only in the tuning build
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["CKV_ATTN_TRACE"] = "1"
 import torch

@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 for B in 32 64 148 296 592; do
-  CKV_GATHER_BLOCKS=$B timeout 300 python scripts/ra_study.py --requests 3 --out gpurun_out/gs_$B.json > /dev/null 2>&1
+  CKV_LIBRARY=tuning CKV_GATHER_BLOCKS=$B timeout 300 python scripts/ra_study.py --requests 3 --out gpurun_out/gs_$B.json > /dev/null 2>&1
   python - "$B" <<'PY'
 import json, statistics, sys
 B = sys.argv[1]

@@ -1,5 +1,6 @@
 """A/B timing of the tcgen05 score kernel variants (CKV_SCORE_POLY = share of exp2 on the FMA pipe)."""
 import os, sys, json
+os.environ.setdefault("CKV_LIBRARY", "tuning")  # env knobs exist only in the tuning build
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import oracle as O

@@ -1,5 +1,6 @@
 """Debug: kernel-end timeline of one graph-replayed C3 step (CKV_TIMELINE=1, printed at close)."""
 import os, sys
+os.environ.setdefault("CKV_LIBRARY", "tuning")  # env knobs exist only in the tuning build
 os.environ["CKV_TIMELINE"] = "1"
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch

@@ -8,10 +8,11 @@ can regenerate exactly the same values independently.  Seed 42 is the paper's
 Structure of the values (no method arithmetic here, only the recipe):
 
 * Prefix keys carry two per-layer unit "topic" directions u1, u2 per KV head.
-  Chunk j of layer l has two salience fields s1[l, j], s2[l, j] that follow an
-  AR(1) process across layers (correlation ``rho``), so adjacent layers select
-  overlapping chunk sets (the paper's cross-layer similarity).
-  Chunk 0 gets a sink boost and the last chunk a recency boost.
+  Chunk j of layer l has two salience fields s1[l, j], s2[l, j] (logit offsets on a
+  geometric rank profile, see salience()) whose latent ranks follow an AR(1) process
+  across layers (correlation ``rho``), so adjacent layers select overlapping chunk sets
+  (the paper's cross-layer similarity).  Chunk 0 gets a sink boost
+  and the last chunk a recency boost.
     Kp[i, h] = N(0, I) + (s1[j(i)] * u1[h] + s2[j(i)] * u2[h]) * sqrt(d) / gamma
 * A request's suffix queries point at a mixture of the two topics with a
   request-specific angle theta (so different requests share part of their
@@ -96,9 +97,25 @@ def _finish(x: np.ndarray, dtype: str) -> np.ndarray:
     return bf16_round(x) if dtype == "bf16" else x
 
 
+SPAN = 64.0   # logit range (nats) of the chunk-salience profile; see salience()
+TOP = 2.0     # logit offset of the most salient ordinary chunk
+
+
 def salience(cfg: ShapeConfig, layer: int, seed: int = SEED, rho: float = 0.9,
-             amp: float = 1.0, sink: float = 2.0, recency: float = 1.0):
-    """Two AR(1)-across-layers salience fields of length m for `layer`."""
+             span: float = SPAN, sink: float = 2.0, recency: float = 1.0):
+    """Two chunk-salience fields (logit offsets, nats) of length m for `layer`.
+
+    Each field is a latent Gaussian z[l, j] following an AR(1) process across layers
+    (correlation rho: adjacent layers select overlapping sets) mapped
+    through its CDF onto a GEOMETRIC rank profile: s = TOP - span * (1 - Phi(z)), so the
+    attention mass of chunk ranks decays exponentially (about span/m nats per rank; C3:
+    0.031) and the top-10% of chunks holds most of a row's mass ("only a small set of important
+    tokens ... is required").  The per-rank log-spacing is what keeps the k-th and (k+1)-th chunk
+    scores apart (the Q11 gate of SURVEY §8(c): >= 95% of C3 draws strict, DESIGN.md §4);
+    a Zipf profile rank^-1 would space them 1/k ~ 0.5% apart and fail the gate in ~1 draw
+    of 5.  Chunk 0 gets a sink boost and the last chunk a recency boost above the top."""
+    from scipy.special import ndtr  # standard normal CDF
+
     m = cfg.num_chunks
     out = []
     for t in (_T_SAL1, _T_SAL2):
@@ -106,9 +123,9 @@ def salience(cfg: ShapeConfig, layer: int, seed: int = SEED, rho: float = 0.9,
         for l in range(1, layer + 1):
             eps = _rng(seed, t, l).standard_normal(m)
             z = rho * z + math.sqrt(1.0 - rho * rho) * eps
-        s = amp * z
-        s[0] += sink
-        s[-1] += recency
+        s = TOP - span * (1.0 - ndtr(z))
+        s[0] = TOP + sink
+        s[-1] = TOP + recency
         out.append(s)
     return out[0], out[1]
 

@@ -12,7 +12,7 @@ from synth import make_prefix, make_request
 
 TOL = {"bf16": 2e-2, "fp32": 1e-4}          # north_star output tolerances (Q12)
 A_TOL = {"bf16": 2e-4, "fp32": 2e-5}          # chunk-score rel. tolerance (fp32 accumulation + ex2.approx)
-GAP_GATE = 1e-3                                # north_star: exact ids when the k/k+1 gap > 1e-3 relative
+GAP_GATE = O.GAP_GATE                          # north_star: exact ids when the k/k+1 gap > 1e-3 relative
 
 
 def to_dev(x, dtype):
@@ -55,16 +55,16 @@ def check_layer(res_gpu_ids, res_gpu_out, res_gpu_A, qs, ks, vs, kp, vp, cfg, k,
         diag["A_rel"] = float(rel.max())
         assert diag["A_rel"] < A_TOL[dtype], diag
     m = ref["A"].shape[0]
-    strict = (k == m) or (ref["gap"] > GAP_GATE)
+    strict = O.parity_gate(ref["A"], k)
     assert len(ids) == k and np.all(np.diff(ids) > 0) and ids.min() >= 0 and ids.max() < m
     if strict:
         assert ids.tolist() == ref["ids"].tolist(), diag
         ref_out = ref["out"]
     else:
-        # Q11: sets may legitimately differ; every chosen chunk must be near the k-th score,
-        # and the output must match the oracle's attention over the GPU's own set
-        Ak = np.sort(ref["A"])[::-1][k - 1]
-        assert np.all(ref["A"][ids] >= Ak * (1 - GAP_GATE)), diag
+        # Q11: only true near-ties of the k-th score may differ (every chunk clearly above A_(k)
+        # must be chosen, every chosen one must be near or above it); the output must match the
+        # oracle's attention over the GPU's own set
+        assert O.valid_relaxed_set(ref["A"], k, ids), diag
         ref_out = O.reprefill_layer(qs, ks, vs, kp, vp, cfg.chunk_size, k, cfg.group, norm=norm, sel=ids)["out"]
     diag["strict"] = strict
     diag["out_rel"] = row_rel_err(res_gpu_out, ref_out)

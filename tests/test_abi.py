@@ -52,3 +52,23 @@ def test_null_context_is_safe():
     assert lib.ckv_last_error(None) == b"null context"
     lib.ckv_destroy(None)
     assert lib.ckv_k(None) == -1
+
+
+def test_config_validation_needs_no_gpu():
+    # argument checks run before any CUDA call (include/ckv.h: errors are reported, nothing enqueued)
+    from paper_2601_13631_b200 import CKV_FLAG_GLOBAL_HEAP, CkvError, Context
+    with pytest.raises(CkvError, match="EUNSUPPORTED"):  # one shared pool + periods (ckv.h CKV_FLAG_GLOBAL_HEAP)
+        Context(4, 4, 2, 64, 16, 256, 8, dtype="fp32", flags=CKV_FLAG_GLOBAL_HEAP, period=4)
+    with pytest.raises(CkvError, match="EUNSUPPORTED"):  # one shared pool + shards
+        Context(4, 4, 2, 64, 16, 256, 8, dtype="fp32", flags=CKV_FLAG_GLOBAL_HEAP, num_shards=2)
+    with pytest.raises(CkvError, match="EINVAL"):
+        Context(4, 4, 2, 64, 16, 256, 8, dtype="fp32", period=2, subperiod=3)
+    with pytest.raises(CkvError, match="EINVAL"):
+        Context(1, 3, 2, 64, 16, 256, 8, dtype="fp32")  # Hq % Hkv != 0
+
+
+def test_product_library_has_no_tuning_knobs():
+    # timing-only modes and env knobs live in the tuning build only (build.py --tuning)
+    data = open(ckv.LIB_PATH, "rb").read()
+    for knob in (b"CKV_KNOCKOUT", b"CKV_SCORE_POLY", b"CKV_PDL_SKIP", b"CKV_ATTN_TRACE", b"CKV_TIMELINE"):
+        assert knob not in data, knob

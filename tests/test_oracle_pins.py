@@ -170,6 +170,53 @@ def test_topk_brute_force_subsets(seed):
         assert O.select_topk(A, k).tolist() == brute.best_subset(A.tolist(), k)
 
 
+def _q11_golden():
+    import json, os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "q11_gate.json")) as f:
+        return json.load(f)
+
+
+def test_score_gap_worked_examples():
+    # Q11 gap, hand-computed values (tests/golden/q11_gate.json)
+    for e in _q11_golden()["score_gap"]:
+        want = math.inf if e["gap"] == "inf" else e["gap"]
+        assert O.score_gap(np.array(e["A"], float), e["k"]) == pytest.approx(want, rel=1e-15), e
+
+
+def test_parity_gate_worked_examples():
+    for e in _q11_golden()["parity_gate"]:
+        assert O.parity_gate(np.array(e["A"], float), e["k"]) is e["strict"], e
+
+
+def test_relaxed_set_worked_examples():
+    for e in _q11_golden()["valid_relaxed_set"]:
+        assert O.valid_relaxed_set(np.array(e["A"], float), e["k"], e["ids"]) is e["valid"], e
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gate_brute_force_subsets(seed):
+    # brute force over every k-subset (m <= 9): when the gate is strict the ONLY valid set is
+    # the top-k set; always, the oracle's top-k set is valid; a set whose sum of scores is below
+    # the best by more than the near-tie allowance k * 2e-3 * A_(k) is never valid
+    import itertools
+    g = np.random.default_rng(100 + seed)
+    m = int(g.integers(3, 10))
+    A = g.random(m)
+    if seed % 2:  # plant a near-tie at some rank
+        i, j = g.choice(m, 2, replace=False)
+        A[j] = A[i] * (1 + 1e-4)
+    for k in range(1, m):
+        best = O.select_topk(A, k).tolist()
+        assert O.valid_relaxed_set(A, k, best)
+        Ak = np.sort(A)[::-1][k - 1]
+        for S in itertools.combinations(range(m), k):
+            ok = O.valid_relaxed_set(A, k, list(S))
+            if O.parity_gate(A, k):
+                assert ok == (list(S) == best), (A, k, S)
+            if A[list(S)].sum() < A[best].sum() - k * 2e-3 * Ak:
+                assert not ok
+
+
 def test_topk_nesting():
     A = np.random.default_rng(9).integers(0, 20, 40).astype(float)
     prev = set()
