@@ -6,13 +6,18 @@
 Workload (config.workload): Qwen2.5-7B shape, 28 layers, 28 Q / 4 KV heads, d = 128,
 32K-token prefix, chunk 16, 128-token suffix, 10% budget (k = 204), bf16, inter-layer
 speculative prefetch on (quota k), HBM chunk cache of k + quota + k/2 slots per layer
-(~25% of the 2048 chunks of a layer),
-R = 8 distinct requests cycling over the shared prefix (synthetic, seed 42).
-A step = one request's Re-Prefill over all 28 layers (A1-A9 each layer).
+(~25% of the 2048 chunks of a layer).  Requests: a steady-state stream over 16 distinct
+requests sharing the prefix (Zipf(1) popularity, seed 42; 16 untimed draws warm the cache),
+so selected chunks that are not resident cross the host link inside the timed region
+(synthetic, seed 42).  A step = one request's Re-Prefill over all 28 layers (A1-A9 each layer).
 value = effective KV GB/s = (probe-K + kept K+V + suffix K+V bytes per layer) x layers
-        / step time; us_per_layer is reported beside it.
+        / step time; us_per_layer is reported beside it; `all_hit` is the same layer with every
+        selected chunk resident (compute only), `cold_cache` with an empty cache.
 Inputs larger than L2: each step streams 28 x 33.5 MB of probe keys (0.94 GB > 126 MB L2).
-N > 1: the prefix is sharded by position across ranks (strong scaling, NCCL exchanges).
+N > 1: the prefix is sharded by position across ranks (strong scaling); the exchanges run
+inside libckv over peer memory (--exchange fused, default) or as host-issued torch.distributed
+collectives (--exchange collective).  Without torchrun, --gpus N re-launches itself under
+torch.distributed.run with N ranks.
 """
 from __future__ import annotations
 
@@ -31,7 +36,8 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 CFG_NAME = "c3_7b"
-N_REQUESTS = 8
+N_DISTINCT = 16   # distinct requests sharing the prefix (each its own query topic mix)
+WARM_CACHE = 16   # untimed request draws that bring the HBM chunk cache to its steady state
 
 
 def load_peaks():
@@ -169,12 +175,20 @@ def run_reference(args, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def request_sequence(n, seed=42):
+    """Seeded request stream over the N_DISTINCT requests sharing the prefix: Zipf(1) popularity
+    (the multi-request shared-prefix setting of PAPER.md:419-455 / SURVEY §8(d))."""
+    g = np.random.default_rng(seed)
+    pop = 1.0 / np.arange(1, N_DISTINCT + 1)
+    return g.choice(N_DISTINCT, size=n, p=pop / pop.sum()).tolist()
+
+
 def run_ckv(args, rank, world):
     import torch
     import torch.distributed as dist
 
     import paper_2601_13631_b200 as ckv
-    from paper_2601_13631_b200.sharded import ShardedReprefill
+    from paper_2601_13631_b200.sharded import ShardedReprefill, open_exchange
     from synth import CONFIGS, make_prefix, make_request
 
     local_rank = int(os.environ.get("LOCAL_RANK", rank)) if args.local_gpu is None else args.local_gpu
@@ -197,17 +211,18 @@ def run_ckv(args, rank, world):
     for l in range(cfg.num_layers):
         kp, vp = make_prefix(cfg, l)
         ctx.store_prefix(l, torch.from_numpy(kp).to(dev, dt), torch.from_numpy(vp).to(dev, dt))
-    reqs_host = []
-    for r in range(N_REQUESTS):
-        per = []
-        for l in range(cfg.num_layers):
-            per.append([torch.from_numpy(x).to(dt).pin_memory() for x in make_request(cfg, l, r)])
-        reqs_host.append(per)
-    reqs = [[[t.to(dev) for t in lay] for lay in per] for per in reqs_host]
     L = cfg.num_layers
+    reqs_host = [[[torch.from_numpy(x).to(dt).pin_memory() for x in make_request(cfg, l, r)] for l in range(L)]
+                 for r in range(N_DISTINCT)]
+    reqs = [[[t.to(dev) for t in lay] for lay in per] for per in reqs_host]
     outs = [torch.empty(cfg.suffix_len, cfg.num_q_heads, cfg.head_dim, dtype=dt, device=dev) for _ in range(L)]
     ids = [torch.empty(k, dtype=torch.int32, device=dev) for _ in range(L)]
-    runner = ShardedReprefill(ctx) if world > 1 else None
+    runner = None
+    if world > 1:
+        if args.exchange == "fused":
+            open_exchange(ctx)  # peer windows; every exchange then runs inside ckv_reprefill_layer
+        else:
+            runner = ShardedReprefill(ctx)  # host-issued torch.distributed collectives (baseline)
 
     def layer_call(l, q, ks, vs):
         if runner is None:
@@ -215,10 +230,9 @@ def run_ckv(args, rank, world):
         else:
             runner.reprefill_layer(l, q, ks, vs, out=outs[l], ids=ids[l])
 
-    def step(i):
-        per = reqs[i % N_REQUESTS]
+    def run_request(r):
         for l in range(L):
-            layer_call(l, *per[l])
+            layer_call(l, *reqs[r][l])
 
     stream = torch.cuda.current_stream()
 
@@ -239,79 +253,103 @@ def run_ckv(args, rank, world):
             ms = float(t.item())
         return ms
 
+    # the request stream: WARM_CACHE untimed draws bring the HBM chunk cache to its steady state
+    # ("warm up"), then the W warm-up and K timed steps follow the same stream
+    seq = request_sequence(WARM_CACHE + args.warmup + 2 * args.steps)
+    for r in seq[:WARM_CACHE]:
+        run_request(r)
+    off = WARM_CACHE
     for i in range(args.warmup):
-        step(i)
+        run_request(seq[off + i])
+    off += args.warmup
     torch.cuda.synchronize()
-    # host cost of enqueueing one eager step (launch-bound check)
-    t0 = time.perf_counter()
-    step(0)
+    t0 = time.perf_counter()  # host cost of enqueueing one eager step (launch-bound check)
+    run_request(seq[off])
     host_ms = (time.perf_counter() - t0) * 1e3
     torch.cuda.synchronize()
     launches0 = ctx.kernel_launches
-    ms_eager = timed(step, args.steps) / args.steps
+    ms_eager = timed(lambda i: run_request(seq[off + i]), args.steps) / args.steps
     launches = ctx.kernel_launches - launches0
 
-    # one CUDA graph per request input set: the 28-layer step replays without host launches
-    graphs = None
-    if args.graph and world == 1:
-        graphs = []
-        for r in range(N_REQUESTS):
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                step(r)
-            graphs.append(g)
-        for g in graphs:
-            g.replay()
-        torch.cuda.synchronize()
+    # one CUDA graph per distinct request: a 28-layer step replays without host launches
+    graphs, graph_note = None, None
+    if args.graph and runner is None:
+        try:
+            graphs = []
+            for r in range(N_DISTINCT):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    run_request(r)
+                graphs.append(g)
+            for r in seq[:N_DISTINCT]:
+                graphs[r].replay()
+            torch.cuda.synchronize()
+        except Exception as ex:  # e.g. a driver without stream-memop capture (W > 1): eager
+            graphs, graph_note = None, f"capture failed: {ex}"[:200]
+            torch.cuda.synchronize()
 
-    def graph_step(i):
-        graphs[i % N_REQUESTS].replay()
+    def play(r):
+        if graphs:
+            graphs[r].replay()
+        else:
+            run_request(r)
 
-    main_step = graph_step if graphs else step
+    # headline: the steady-state request stream (the HBM cache holds ~25% of a layer's chunks, so
+    # misses cross the host link inside the timed region: A1-A9 of the north star, gather included)
+    off2 = off + args.steps
     ctx.reset_stats()
     with ClockSampler(local_rank) as clk:
-        ms = timed(main_step, args.steps)
+        ms = timed(lambda i: play(seq[off2 + i]), args.steps)
     stats = ctx.get_stats()
     ms_step = ms / args.steps
     bpl = bytes_per_layer(cfg, k)
     value = bpl * L / (ms_step * 1e-3) / 1e9
+    # all-hit: one request repeated (its chunks stay resident) -- the compute-only layer time
+    for _ in range(3):
+        play(0)
+    ctx.reset_stats()
+    ms_hit = timed(lambda i: play(0), args.steps) / args.steps
+    hit_stats = ctx.get_stats()
+    torch.cuda.synchronize()
+    ids_cpu = [t.cpu().numpy() for t in ids]  # request 0's ids per layer
+    cov = [len(set(ids_cpu[l].tolist()) & set(ids_cpu[l - 1].tolist())) / k for l in range(1, L)]
     if args.quick:  # tuning runs: the warm graph-replayed step only
         if rank == 0:
-            print(json.dumps({"us_per_layer": ms_step * 1e3 / L, "value": value, "eager_us_per_layer":
-                              ms_eager * 1e3 / L, "clocks": clk.summary()}))
+            print(json.dumps({"us_per_layer": ms_step * 1e3 / L, "value": value, "all_hit_us_per_layer":
+                              ms_hit * 1e3 / L, "eager_us_per_layer": ms_eager * 1e3 / L, "clocks": clk.summary(),
+                              "hit_rate": stats["total_hits"] / max(stats["total_hits"] + stats["total_misses"], 1)}))
         return
 
     # stage profile pass (eager; CUDA events on the launching stream, inside the library)
     ctx.profile(True)
-    ms_prof = timed(step, args.steps)
+    ms_prof = timed(lambda i: run_request(seq[off2 + i]), args.steps)
     prof = ctx.profile_read()
     ctx.profile(False)
 
     # end-to-end through the public API with host buffers: H2D of the step's inputs from
-    # pinned memory and D2H of its outputs inside the timed region
+    # pinned memory and D2H of its outputs inside the timed region, pipelined with the compute:
+    # layer l's inputs go up on an H2D stream (event per layer, waited on by the compute stream
+    # just before layer l) and layer l's output comes down on a D2H stream as soon as layer l is
+    # done; one CUDA graph per distinct request
     host_out = [torch.empty(outs[0].shape, dtype=dt).pin_memory() for _ in range(L)]
     host_ids = [torch.empty(k, dtype=torch.int32).pin_memory() for _ in range(L)]
-
-    # the step's copies are pipelined with its compute: layer l's inputs go up on an H2D stream
-    # (event per layer, waited on by the compute stream just before layer l) and layer l's output
-    # comes down on a D2H stream as soon as layer l is done; the whole step is one CUDA graph
     h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     ev_in = [torch.cuda.Event() for _ in range(L)]
     ev_out = [torch.cuda.Event() for _ in range(L)]
+    dev_in = [[torch.empty_like(t) for t in lay] for lay in reqs[0]]  # the step's device input buffers
 
     def e2e_body(r):
         main = torch.cuda.current_stream()
-        per_h, per_d = reqs_host[r], reqs[r]
         h2d_s.wait_stream(main)
         d2h_s.wait_stream(main)
         with torch.cuda.stream(h2d_s):
             for l in range(L):
-                for dst, src in zip(per_d[l], per_h[l]):
+                for dst, src in zip(dev_in[l], reqs_host[r][l]):
                     dst.copy_(src, non_blocking=True)
                 ev_in[l].record(h2d_s)
         for l in range(L):
             main.wait_event(ev_in[l])
-            layer_call(l, *per_d[l])
+            layer_call(l, *dev_in[l])
             ev_out[l].record(main)
             d2h_s.wait_event(ev_out[l])
             with torch.cuda.stream(d2h_s):
@@ -324,25 +362,26 @@ def run_ckv(args, rank, world):
     if graphs:
         try:
             e2e_graphs = []
-            for r in range(N_REQUESTS):
+            for r in range(N_DISTINCT):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
                     e2e_body(r)
                 e2e_graphs.append(g)
-            for g in e2e_graphs:
-                g.replay()
             torch.cuda.synchronize()
         except Exception as ex:  # capture of the multi-stream step failed: run it eagerly
             print(f"[bench] e2e graph capture failed ({ex}); eager e2e", file=sys.stderr)
             e2e_graphs = None
 
-    def e2e_step(i):
+    def e2e_step(r):
         if e2e_graphs:
-            e2e_graphs[i % N_REQUESTS].replay()
+            e2e_graphs[r].replay()
         else:
-            e2e_body(i % N_REQUESTS)
+            e2e_body(r)
 
-    ms_e2e = timed(e2e_step, args.steps) / args.steps
+    off3 = off2 + args.steps
+    for i in range(2):
+        e2e_step(seq[off2 + i])
+    ms_e2e = timed(lambda i: e2e_step(seq[off3 - args.steps + i]), args.steps) / args.steps
 
     # cold HBM cache: every step starts from an empty chunk cache (all selected chunks cross the
     # host link; speculative prefetch still overlaps the next layer's loads)
@@ -351,12 +390,13 @@ def run_ckv(args, rank, world):
     for i in range(min(args.steps, 5)):
         ctx.reset_cache()
         torch.cuda.synchronize()
-        cold_ms.append(timed(main_step, 1))
+        cold_ms.append(timed(lambda _: play(0), 1))
     cold_stats = ctx.get_stats()
     cold_layers = max(cold_stats["total_layers"], 1)
 
     # V-only store variant (CKV_FLAG_V_ONLY_STORE): the kept chunks' K comes from
-    # the HBM probe array, so every miss moves half the bytes; same cold-cache protocol
+    # the HBM probe array, so every miss moves half the bytes; same cold-cache protocol and the
+    # same mode (one CUDA graph per step) as the K+V cold line
     cold_v = None
     if world == 1:
         vctx = ckv.Context(cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.chunk_size,
@@ -367,23 +407,29 @@ def run_ckv(args, rank, world):
             kp, vp = make_prefix(cfg, l)
             vctx.store_prefix(l, torch.from_numpy(kp).to(dev, dt), torch.from_numpy(vp).to(dev, dt))
 
-        def vstep(i):
+        def vstep():
             for l in range(L):
-                vctx.reprefill_layer(l, *reqs[i % N_REQUESTS][l], out=outs[l], ids=ids[l])
-        for i in range(3):
-            vstep(i)
+                vctx.reprefill_layer(l, *reqs[0][l], out=outs[l], ids=ids[l])
+        for _ in range(3):
+            vstep()
+        vgraph = None
+        if graphs:
+            vgraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(vgraph):
+                vstep()
         vms = []
         vctx.reset_stats()
         for i in range(min(args.steps, 5)):
             vctx.reset_cache()
             torch.cuda.synchronize()
-            vms.append(timed(vstep, 1))
+            vms.append(timed(lambda _: vgraph.replay() if vgraph else vstep(), 1))
         vst = vctx.get_stats()
         vlink = vst["total_link_bytes_delta"] + vst["total_link_bytes_spec"]
-        cold_v = {"us_per_layer": sum(vms) / len(vms) * 1e3 / L, "eager": True,
+        cold_v = {"us_per_layer": sum(vms) / len(vms) * 1e3 / L, "cuda_graph": bool(vgraph),
                   "link_bytes_per_layer": vlink / max(vst["total_layers"], 1),
                   "link_gbs": vlink / (sum(vms) * 1e-3) / 1e9,
                   "hit_rate": vst["total_hits"] / max(vst["total_hits"] + vst["total_misses"], 1)}
+        del vgraph
         vctx.close()
         del vctx
 
@@ -412,27 +458,30 @@ def run_ckv(args, rank, world):
                      "frac": kbytes / (t8 * 1e-3) / 1e9 / hbm_peak}
 
     # the paper's own configuration: Periods of p = 8 layers, subperiod sp = 4:
-    # chunk ids are identified on 1 layer in 8, the Period's other layers are prefetched
+    # chunk ids are identified on 1 layer in 8, the Period's other layers are prefetched; same
+    # steady-state request stream as the headline
     period_line = None
-    if world == 1 and args.graph:
+    if world == 1 and graphs:
         ctx.set_period(8, 4)
-        pgraphs = []
-        for r in range(N_REQUESTS):
-            step(r)  # warm the cache for this configuration
+        for r in seq[:WARM_CACHE]:
+            run_request(r)  # warm the cache for this configuration
         torch.cuda.synchronize()
-        for r in range(N_REQUESTS):
+        pgraphs = []
+        for r in range(N_DISTINCT):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
-                step(r)
+                run_request(r)
             pgraphs.append(g)
-        for g in pgraphs:
-            g.replay()
+        for r in seq[off:off + args.warmup]:
+            pgraphs[r].replay()
         ctx.reset_stats()
-        ms_p = timed(lambda i: pgraphs[i % N_REQUESTS].replay(), args.steps) / args.steps
+        ms_p = timed(lambda i: pgraphs[seq[off2 + i]].replay(), args.steps) / args.steps
         pst = ctx.get_stats()
         period_line = {"period": 8, "subperiod": 4, "ms_per_step": ms_p, "us_per_layer": ms_p * 1e3 / L,
                        "value": bpl * L / (ms_p * 1e-3) / 1e9, "unit": "GB/s",
-                       "hit_rate": pst["total_hits"] / max(pst["total_hits"] + pst["total_misses"], 1)}
+                       "hit_rate": pst["total_hits"] / max(pst["total_hits"] + pst["total_misses"], 1),
+                       "link_bytes_per_layer": (pst["total_link_bytes_delta"] + pst["total_link_bytes_spec"])
+                       / max(pst["total_layers"], 1)}
         ctx.set_period(1, 1)
         del pgraphs
 
@@ -476,45 +525,70 @@ def run_ckv(args, rank, world):
         t = oracle_layer_seconds(cfg, k)
         cpu = {"value": bpl / t / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
                "sample": f"1 layer (layer 0, request 0) of {CFG_NAME}, fp64 NumPy, {t:.2f} s"}
+    gate = None
+    gp = os.path.join(ROOT, "profiles", "r2_gate_rate_c3.json")
+    if os.path.exists(gp):
+        with open(gp) as f:
+            gs = json.load(f)["summary"]
+        gate = {"pass_rate": gs["gate_pass_rate"], "draws": gs["draws"],
+                "source": "profiles/r2_gate_rate_c3.json (fp64 oracle, scripts/gate_rate.py)"}
     n_lay = max(stats["total_layers"], 1)
+    mufu = mufu_roofline(cfg, world, score_avg, clk.summary())
+    tensor = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+              "peak_source": f"{peak_src} bf16_tflops_sustained"}
+
+    def hit_rate(st):
+        return st["total_hits"] / max(st["total_hits"] + st["total_misses"], 1)
+
     line = {
         "metric": "Re-Prefill effective KV GB/s (Qwen2.5-7B shape, 32K prefix)",
         "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "us_per_layer": ms_step * 1e3 / L,
-        "eager": {"ms_per_step": ms_eager, "host_enqueue_ms_per_step": host_ms, "cuda_graph": bool(graphs)},
+        "eager": {"ms_per_step": ms_eager, "host_enqueue_ms_per_step": host_ms, "cuda_graph": bool(graphs),
+                  "graph_note": graph_note},
         "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seed 42, SURVEY §8(d) recipe)",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seed 42, DESIGN.md §4 recipe)",
         "config": {"workload": CFG_NAME, "layers": L, "prefix_len": cfg.prefix_len, "chunk": cfg.chunk_size,
                    "suffix": cfg.suffix_len, "heads": f"{cfg.num_q_heads}/{cfg.num_kv_heads}",
                    "head_dim": cfg.head_dim, "budget_chunks": k, "prefetch_quota": quota,
-                   "requests": N_REQUESTS, "cache_slots_per_layer": cache_slots, "parallelism": (f"prefix-shard{world}" + ("-cyclic" if args.cyclic else "")) if world > 1 else "single",
+                   "requests": f"steady-state stream: {N_DISTINCT} distinct requests, Zipf(1) popularity, "
+                               f"{WARM_CACHE} untimed cache warm-up draws",
+                   "cache_slots_per_layer": cache_slots,
+                   "parallelism": (f"prefix-shard{world}" + ("-cyclic" if args.cyclic else "") +
+                                   f"-{args.exchange}") if world > 1 else "single",
                    "l2": "inputs larger than L2 (0.94 GB of probe keys streamed per step)",
                    "bytes_per_layer": bpl},
-        "roofline": {"kernel": "score_partial (A1)", "bound": "tensor", "achieved": achieved, "peak": peak,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": f"{peak_src} bf16_tflops_sustained", "score_kernel_kind":
-                         ["simt", "tcgen05"][ctx.score_kernel_kind], "avg_launch_ms": score_avg,
+        # the kernel that dominates the step is A1; its binding roofline is the MUFU (one exp2 per
+        # logit, 16 ex2/clk/SM x 148 SMs at the SM clock sampled in the timed region);
+        # the tensor-pipe fraction is reported beside it
+        "roofline": {"kernel": "score_partial (A1)", "bound": "alu", "achieved": mufu["achieved"],
+                     "peak": mufu["peak"], "unit": "Tex2/s", "frac": mufu["frac"], "traffic": traffic,
+                     "peak_source": "derived: 16 ex2/clk/SM x 148 SMs x sampled SM clock (DESIGN.md §6)",
+                     "score_kernel_kind": ["simt", "tcgen05"][ctx.score_kernel_kind], "avg_launch_ms": score_avg,
+                     "algorithmic": mufu["algorithmic"], "tensor": tensor,
                      "hbm_achieved_gbs": (cfg.prefix_len / world) * cfg.num_kv_heads * cfg.head_dim * 2
-                     / (score_avg * 1e-3) / 1e9,
-                     # the roofline that binds A1 first: one exp2 per logit on the MUFU pipe,
-                     # 16 ex2/clk/SM x 148 SMs at the SM clock sampled during the timed region
-                     "binding": mufu_roofline(cfg, world, score_avg, clk.summary())},
+                     / (score_avg * 1e-3) / 1e9},
         "stage_ms_per_step": step_stage_ms, "profiled_ms_per_step": ms_prof / args.steps,
-        "cache": {"hit_rate": stats["total_hits"] / max(stats["total_hits"] + stats["total_misses"], 1),
-                  "misses_per_layer": stats["total_misses"] / n_lay,
+        "cache": {"hit_rate": hit_rate(stats), "misses_per_layer": stats["total_misses"] / n_lay,
                   "spec_loads_per_layer": stats["total_spec_loads"] / n_lay,
                   "spec_used_per_layer": stats["total_spec_used"] / n_lay,
-                  "link_bytes_per_layer": (stats["total_link_bytes_delta"] + stats["total_link_bytes_spec"]) / n_lay},
+                  "link_bytes_per_layer": (stats["total_link_bytes_delta"] + stats["total_link_bytes_spec"]) / n_lay,
+                  "link_gbs": (stats["total_link_bytes_delta"] + stats["total_link_bytes_spec"]) / (ms * 1e-3) / 1e9},
+        "all_hit": {"us_per_layer": ms_hit * 1e3 / L, "value": bpl * L / (ms_hit * 1e-3) / 1e9, "unit": "GB/s",
+                    "hit_rate": hit_rate(hit_stats), "note": "request 0 repeated: every selected chunk resident"},
+        "selection": {"coverage_prev_mean": float(np.mean(cov)), "coverage_prev_min": float(np.min(cov)),
+                      "gap_gate": gate},
         "paper_period": period_line,
         "cold_cache": {"ms_per_step": sum(cold_ms) / len(cold_ms), "us_per_layer": sum(cold_ms) / len(cold_ms) * 1e3 / L,
-                       "hit_rate": cold_stats["total_hits"] / max(cold_stats["total_hits"] + cold_stats["total_misses"], 1),
+                       "hit_rate": hit_rate(cold_stats),
                        "link_bytes_per_layer": (cold_stats["total_link_bytes_delta"] + cold_stats["total_link_bytes_spec"])
                        / cold_layers,
                        "link_gbs": (cold_stats["total_link_bytes_delta"] + cold_stats["total_link_bytes_spec"])
                        / (sum(cold_ms) * 1e-3) / 1e9,
                        "link_peak_gbs": link_peak, "link_peak_how": "pinned H2D cudaMemcpy 256 MiB, best of 5",
                        # exposed gather = t_layer(cold, prefetch on) - t_layer(all-hit)
-                       "exposed_gather_us_per_layer": sum(cold_ms) / len(cold_ms) * 1e3 / L - ms_step * 1e3 / L},
+                       "exposed_gather_us_per_layer": sum(cold_ms) / len(cold_ms) * 1e3 / L - ms_hit * 1e3 / L,
+                       "cuda_graph": bool(graphs)},
         "cold_cache_v_only": cold_v,
         "hbm_probe": hbm_probe,
         "e2e": {"value": bpl * L / (ms_e2e * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": ms_e2e,
@@ -532,6 +606,21 @@ def run_ckv(args, rank, world):
         dist.destroy_process_group()
 
 
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with N ranks
+    (the driver's own launch line); NCCL INFO logging shows the communicator's rank count."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -545,11 +634,21 @@ def main():
                     "contiguous ranges (balanced kept chunks, SURVEY §8(f) NEXT-3)")
     ap.add_argument("--quick", action="store_true", help="tuning: print only the warm graph-step time")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
+    ap.add_argument("--exchange", default="fused", choices=["fused", "collective"],
+                    help="N > 1: fused device-side exchange inside libckv (default) or host-issued "
+                         "torch.distributed collectives (ShardedReprefill, the NCCL baseline)")
     ap.add_argument("--local-gpu", type=int, default=None, help="pin every rank to this GPU (functional runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ckv" else args.warmup
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.impl == "reference":
         run_reference(args, rank, world)
     else:

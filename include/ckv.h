@@ -297,6 +297,10 @@ ckv_status ckv_load_chunks(ckv_ctx* ctx, int32_t layer, const int32_t* ids, int3
  *   hits, loads, victims, 0) are written; no data is copied. */
 ckv_status ckv_test_topk(ckv_ctx* ctx, const float* A, int32_t m, int32_t k, int32_t* ids,
                          void* stream);
+/* ckv_test_exchange_flags: the XF_COUNT (4) exchange counters of this rank's window (host
+ *   uint32 [4]: row normalisers, candidates, partial outputs, merged rows), read on a private
+ *   non-blocking stream (does not wait for the caller's stream).  num_shards > 1 only. */
+ckv_status ckv_test_exchange_flags(ckv_ctx* ctx, uint32_t* flags_out);
 ckv_status ckv_test_cache_step(ckv_ctx* ctx, int32_t layer, const int32_t* ids, int32_t k,
                                int32_t prefetch, const float* A, int32_t* loads,
                                int32_t* victims, int32_t* counts, void* stream);

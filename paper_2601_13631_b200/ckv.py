@@ -67,6 +67,9 @@ SIGNATURES = {
     "ckv_lse_merge_prepare": (ctypes.c_int, [_P, _P, _P, _P, _I32, _P, _P]),
     "ckv_lse_merge_finish": (ctypes.c_int, [_P, _P, _I32, _P, _P]),
     "ckv_reset_cache": (ctypes.c_int, [_P, _P]),
+    "ckv_exchange_handle": (ctypes.c_int, [_P, _P]),
+    "ckv_exchange_open": (ctypes.c_int, [_P, _P]),
+    "ckv_exchange_attach": (ctypes.c_int, [_P, ctypes.POINTER(_P), _I32]),
     "ckv_set_period": (ctypes.c_int, [_P, _I32, _I32]),
     "ckv_set_cache_policy": (ctypes.c_int, [_P, _I32, _P]),
     "ckv_block_cover": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P, _P]),
@@ -79,6 +82,7 @@ SIGNATURES = {
     "ckv_score_kernel_kind": (_I32, [_P]),
     "ckv_attn_kernel_kind": (_I32, [_P]),
     "ckv_test_topk": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P]),
+    "ckv_test_exchange_flags": (ctypes.c_int, [_P, _P]),
     "ckv_test_cache_step": (ctypes.c_int, [_P, _I32, _P, _I32, _I32, _P, _P, _P, _P, _P]),
     "ckv_profile": (ctypes.c_int, [_P, _I32]),
     "ckv_profile_read": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)]),
@@ -205,6 +209,30 @@ class Context:
     def lse_merge_finish(self, merge_buf, n_suffix, out, stream=None):
         self._check(self.lib.ckv_lse_merge_finish(self.h, _ptr(merge_buf), n_suffix, _ptr(out), _stream(stream)),
                     "ckv_lse_merge_finish")
+
+    # ---- fused device-side exchange (num_shards > 1; include/ckv.h) ----
+    EXCHANGE_HANDLE_BYTES = 64
+
+    def exchange_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(self.EXCHANGE_HANDLE_BYTES)
+        self._check(self.lib.ckv_exchange_handle(self.h, buf), "ckv_exchange_handle")
+        return buf.raw
+
+    def exchange_open(self, handles):
+        """handles: the W 64-byte handles of all ranks, in rank order (multi-process)."""
+        blob = b"".join(handles)
+        assert len(blob) == self.EXCHANGE_HANDLE_BYTES * self.W
+        self._check(self.lib.ckv_exchange_open(self.h, blob), "ckv_exchange_open")
+
+    def exchange_attach(self, ctxs):
+        """ctxs: the W Contexts of the group in rank order (one process driving every rank)."""
+        arr = (ctypes.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+        self._check(self.lib.ckv_exchange_attach(self.h, arr, len(ctxs)), "ckv_exchange_attach")
+
+    def test_exchange_flags(self):
+        f = (ctypes.c_uint32 * 4)()
+        self._check(self.lib.ckv_test_exchange_flags(self.h, f), "ckv_test_exchange_flags")
+        return list(f)
 
     def set_period(self, period, subperiod=1):
         self._check(self.lib.ckv_set_period(self.h, period, subperiod), "ckv_set_period")

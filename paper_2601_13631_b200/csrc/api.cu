@@ -394,6 +394,10 @@ ckv_status reprefill_sharded(ckv_ctx* ctx, int layer, const void* q, const void*
   char* win = ctx->xwin;
   auto flag = [&](int f) { return static_cast<void*>(win + xl.flags + sizeof(uint32_t) * f); };
   const size_t fl = xl.flags;
+  static const bool xtrace = tuning_env("CKV_XCHG_TRACE") != nullptr;  // tuning build: host-side step trace
+#define XTRACE(msg) \
+  if (xtrace) fprintf(stderr, "[xchg rank %d layer %d] %s\n", self, layer, msg)
+  XTRACE("enter");
   if (layer == 0) {
     ++ctx->epoch;
     LK(launch_epoch_inc(ctx->epoch_dev, st));
@@ -403,9 +407,12 @@ ckv_status reprefill_sharded(ckv_ctx* ctx, int layer, const void* q, const void*
   int nsplit = 0;
   ckv_status s = run_score(ctx, layer, q, k_suf, ns, ctx->lam_loc, &nsplit, st);
   if (s != CKV_OK) return s;
+  XTRACE("scored");
   LK(launch_xchg_put(xp, ctx->lam_loc, sizeof(float) * N, xl.lam + sizeof(float) * (size_t)self * N,
                      fl + sizeof(uint32_t) * XF_LAM, st));
+  XTRACE("lam put");
   CK(xchg_wait(st, flag(XF_LAM), W));
+  XTRACE("lam wait enqueued");
   // 2. global Lambda (rank order; FULLROW adds the causal suffix) -> local A_j -> candidates
   LayerGeom g = geom(ctx, ns);
   const float* lam_all = reinterpret_cast<const float*>(win + xl.lam);
@@ -427,7 +434,9 @@ ckv_status reprefill_sharded(ckv_ctx* ctx, int layer, const void* q, const void*
   PROF_END(6);
   LK(launch_xchg_put(xp, ctx->cand_loc, sizeof(uint64_t) * ctx->k, xl.cand + sizeof(uint64_t) * (size_t)self * ctx->k,
                      fl + sizeof(uint32_t) * XF_CAND, st));
+  XTRACE("cand put");
   CK(xchg_wait(st, flag(XF_CAND), W));
+  XTRACE("cand wait enqueued");
   // 3. identical merged top-k on every rank; local plan / gather / attention (suffix on rank W-1);
   //    the combine writes each partial row straight into the window of the rank merging its slice
   int32_t* ids = ctx->ids_buf[layer & 1];
@@ -441,7 +450,9 @@ ckv_status reprefill_sharded(ckv_ctx* ctx, int layer, const void* q, const void*
                       false, st, nullptr, &xd)) != CKV_OK)
     return s;
   LK(launch_xchg_put(xp, nullptr, 0, 0, fl + sizeof(uint32_t) * XF_PART, st));
+  XTRACE("part signal");
   CK(xchg_wait(st, flag(XF_PART), W));
+  XTRACE("part wait enqueued");
   // 4. merge this rank's slice over the W partials, broadcast the merged rows; copy out
   if (ctx->dtype == CKV_FP32)
     LK(launch_xchg_merge<float>(xp, xl, N, rps, ctx->d, st));
@@ -449,9 +460,12 @@ ckv_status reprefill_sharded(ckv_ctx* ctx, int layer, const void* q, const void*
     LK(launch_xchg_merge<__nv_bfloat16>(xp, xl, N, rps, ctx->d, st));
   LK(launch_xchg_put(xp, nullptr, 0, 0, fl + sizeof(uint32_t) * XF_OUT, st));
   CK(xchg_wait(st, flag(XF_OUT), W));
+  XTRACE("out wait enqueued");
   CK(cudaMemcpyAsync(out, win + xl.outs, (size_t)N * ctx->d * ctx->esz, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(selected_ids, ctx->ids_glob, sizeof(int32_t) * ctx->k, cudaMemcpyDeviceToDevice, st));
   if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
+  XTRACE("done");
+#undef XTRACE
   return CKV_OK;
 }
 
@@ -565,6 +579,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
     if (e_ != cudaSuccess) return cudafail(e_, #expr); \
   } while (0)
   CKC(cudaSetDevice(c.device));
+  CKC(preload_kernels());  // no lazy module load later on the hot path (see common.cuh)
   const int R_max = ctx->G * ctx->max_ns;
   ctx->nsplit_score_max = ctx->m_loc < 4096 ? ctx->m_loc : 4096;
   {
@@ -950,6 +965,19 @@ ckv_status ckv_exchange_attach(ckv_ctx* ctx, ckv_ctx* const* ctxs, int32_t num_c
   return CKV_OK;
 }
 
+ckv_status ckv_test_exchange_flags(ckv_ctx* ctx, uint32_t* flags_out) {
+  if (!ctx) return CKV_EINVAL;
+  ctx->err.clear();
+  if (!flags_out || !ctx->xwin) return fail(ctx, CKV_EINVAL, "no exchange window");
+  CK(cudaSetDevice(ctx->cfg.device));
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  CK(cudaMemcpyAsync(flags_out, ctx->xwin + ctx->xl.flags, sizeof(uint32_t) * XF_COUNT, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaStreamDestroy(s));
+  return CKV_OK;
+}
+
 ckv_status ckv_set_period(ckv_ctx* ctx, int32_t period, int32_t subperiod) {
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
@@ -1129,6 +1157,21 @@ void ckv_destroy(ckv_ctx* ctx) {
 }  // extern "C"
 
 namespace ckv {
+static std::vector<const void*>& kernel_registry() {
+  static std::vector<const void*> r;
+  return r;
+}
+int register_kernels(std::initializer_list<const void*> ks) {
+  for (const void* k : ks) kernel_registry().push_back(k);
+  return (int)kernel_registry().size();
+}
+cudaError_t preload_kernels() {  // on the current device
+  for (const void* k : kernel_registry()) {
+    cudaFuncAttributes a;
+    if (cudaError_t e = cudaFuncGetAttributes(&a, k)) return e;
+  }
+  return cudaSuccess;
+}
 static cudaStream_t g_pdl_marked[8];
 static int g_pdl_n_marked = 0;
 void pdl_mark_event_wait(cudaStream_t st) {

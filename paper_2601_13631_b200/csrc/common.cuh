@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <initializer_list>
+
 #include "xchg.cuh"
 
 namespace ckv {
@@ -27,7 +29,13 @@ bool pdl_enabled();  // tuning build: CKV_PDL=0 disables the launch attribute (A
 // programmatic relaxation must not weaken the event dependency); api.cu marks such streams.
 void pdl_mark_event_wait(cudaStream_t st);
 bool pdl_take_event_wait(cudaStream_t st);  // true (and cleared) if st was marked
-void timeline_mark(const void* kern, cudaStream_t st);  // tuning build: CKV_TIMELINE=1 event after each launch
+void timeline_mark(const void* kern, cudaStream_t st);
+// Every kernel of the library is registered at load time (static initialisers, no CUDA call) and
+// loaded by ckv_create (cudaFuncGetAttributes): with CUDA's lazy module loading, the first launch
+// of a kernel can block the host until the device is idle, which deadlocks a host thread that
+// drives several ranks whose streams wait on each other (fused exchange, xchg.cuh).
+int register_kernels(std::initializer_list<const void*> ks);
+cudaError_t preload_kernels();  // tuning build: CKV_TIMELINE=1 event after each launch
 // Environment knobs exist only in the tuning build (-DCKV_TUNING, `build.py --tuning` ->
 // libckv_tuning.so, used by scripts/ for A/B measurements).  The product library reads no
 // environment variable: tuning_env() returns nullptr there, so every knob takes its default.

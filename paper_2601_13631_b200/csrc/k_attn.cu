@@ -312,6 +312,11 @@ __global__ void lse_merge_finish_kernel(int rows, int d, const float* __restrict
     out[(int64_t)i * d + x] = from_f<T>(den > 0.f ? buf[(int64_t)i * (d + 1) + x] / den : 0.f);
 }
 
+const int kReg = register_kernels({(const void*)attn_simt_kernel<float>, (const void*)attn_simt_kernel<__nv_bfloat16>,
+                                   (const void*)attn_combine_kernel<float>, (const void*)attn_combine_kernel<__nv_bfloat16>,
+                                   (const void*)lse_merge_prepare_kernel, (const void*)lse_merge_finish_kernel<float>,
+                                   (const void*)lse_merge_finish_kernel<__nv_bfloat16>});
+
 }  // namespace
 
 template <typename T>

@@ -522,6 +522,8 @@ int sm_count() {
   return n;
 }
 
+const int kReg = register_kernels({(const void*)compact_kv_kernel, (const void*)attn_tc_kernel});
+
 }  // namespace
 
 bool attn_tc_supported(const LayerGeom& g) {

@@ -129,6 +129,11 @@ __global__ void epoch_inc_kernel(int32_t* e) {
   pdl_wait();
   pdl_trigger(); *e += 1; }
 
+const int kReg = register_kernels({(const void*)cache_plan_kernel, (const void*)gather_kernel,
+                                   (const void*)cache_update_kernel, (const void*)pack_probe_kernel<float>,
+                                   (const void*)pack_probe_kernel<__nv_bfloat16>, (const void*)pack_records_kernel<float>,
+                                   (const void*)pack_records_kernel<__nv_bfloat16>, (const void*)epoch_inc_kernel});
+
 }  // namespace
 
 cudaError_t launch_epoch_inc(int32_t* epoch_dev, cudaStream_t st) {

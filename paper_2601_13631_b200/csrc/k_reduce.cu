@@ -180,6 +180,9 @@ __global__ void chunk_sum_kernel(LayerGeom g, const float* __restrict__ lam2, co
   chunk_sum_warp(g, lam2, Lam2, Apart, warp, threadIdx.x & 31);
 }
 
+const int kReg = register_kernels({(const void*)row_lse_kernel<float>, (const void*)row_lse_kernel<__nv_bfloat16>,
+                                   (const void*)chunk_sum_kernel});
+
 }  // namespace
 
 template <typename T>

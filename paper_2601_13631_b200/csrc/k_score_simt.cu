@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(NT) score_simt_kernel(LayerGeom g, const T* __
   }
 }
 
+const int kReg = register_kernels({(const void*)score_simt_kernel<float>, (const void*)score_simt_kernel<__nv_bfloat16>});
+
 }  // namespace
 
 template <typename T>

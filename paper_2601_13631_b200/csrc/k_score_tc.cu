@@ -46,20 +46,76 @@ struct TcParams {
   float scale;  // log2(e) / sqrt(d)
 };
 
-// In-place pairwise tree: after the call a[0..N/G) hold sums of consecutive groups of G.
-template <int N, int G>
-__device__ __forceinline__ void tree_sum(float* a) {
-  if constexpr (G > 1) {
-    tree_sum<N, G / 2>(a);
-#pragma unroll
-    for (int i = 0; i < N / G; ++i) a[i] = a[2 * i] + a[2 * i + 1];
-  }
+// ---- packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two fp32 lanes per instruction) ----
+__device__ __forceinline__ uint64_t f2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_split(uint64_t r, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_sub(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
 }
 
-template <int C, int NP, bool MASK>
+// 2^x for a pair of x <= 0 on the FMA pipe: x clamped to -125 (flushes like ex2.approx.ftz
+// would, to within 2^-125), round-to-nearest split x = i + f with the 1.5 * 2^23 trick,
+// degree-4 minimax polynomial of 2^f on [-0.5, 0.5] (max rel. error 2.7e-6 in fp32), and i
+// added to the exponent field in the integer domain ((bits(r) << 23) == i << 23 mod 2^32).
+__device__ __forceinline__ uint64_t exp2_poly_x2(uint64_t x) {
+  float a, b;
+  f2_split(x, a, b);
+  x = f2(fmaxf(a, -125.f), fmaxf(b, -125.f));
+  const uint64_t M = f2(12582912.f, 12582912.f);
+  const uint64_t r = f2_add(x, M);
+  const uint64_t f = f2_sub(x, f2_sub(r, M));
+  uint64_t q = f2_fma(f, f2(9.570068679749966e-3f, 9.570068679749966e-3f),
+                      f2(5.5917806923389435e-2f, 5.5917806923389435e-2f));
+  q = f2_fma(q, f, f2(0.240247443318367f, 0.240247443318367f));
+  q = f2_fma(q, f, f2(0.6931218504905701f, 0.6931218504905701f));
+  q = f2_fma(q, f, f2(0.9999992847442627f, 0.9999992847442627f));
+  float qa, qb, ra, rb;
+  f2_split(q, qa, qb);
+  f2_split(r, ra, rb);
+  return f2(__int_as_float(__float_as_int(qa) + (__float_as_int(ra) << 23)),
+            __int_as_float(__float_as_int(qb) + (__float_as_int(rb) << 23)));
+}
+
+// Sum of 2*NP consecutive values held as NP packed pairs (pairwise tree on FADD2, then one
+// FADD of the two lanes); NP a power of two.
+template <int NP>
+__device__ __forceinline__ float pair_sum(uint64_t* P) {
+#pragma unroll
+  for (int h = NP / 2; h >= 1; h /= 2) {
+#pragma unroll
+    for (int i = 0; i < h; ++i) P[i] = f2_add(P[i], P[i + h]);
+  }
+  float a, b;
+  f2_split(P[0], a, b);
+  return a + b;
+}
+
+// One warp's 64 key columns of one row tile (this thread: one suffix row): a single max over
+// the 64 scores is the reference for every exponential (no running rescale).  Per score the
+// issue slots are: 1/2 FMNMX3 (max), 1/2 FFMA2 (scale and shift), 1/2 FADD2 (chunk sums) and
+// either one MUFU.EX2 or, for NPX of every 8 pairs, the FFMA2 polynomial above -- the split
+// balances the MUFU pipe (16 ex2/clk/SM) against the issue slots (4 warp-instructions/clk/SM).
+template <int C, int NPX, bool MASK>
 __device__ __forceinline__ void epilogue_unit(const TcParams& p, float (&v)[64], int key0, float* lamrow,
                                               float* lampart_out, bool row_ok) {
-  const float sc = p.scale;
   if constexpr (MASK) {  // only the shard's last key tile (a separate instantiation)
 #pragma unroll
     for (int j = 0; j < 64; ++j)
@@ -75,26 +131,49 @@ __device__ __forceinline__ void epilogue_unit(const TcParams& p, float (&v)[64],
   m[3] = fmaxf(fmaxf(m[3], m[4]), m[5]);
   m[6] = fmaxf(m[6], m[21]);
   const float gm = fmaxf(fmaxf(m[0], m[3]), m[6]);
-  const float ms = (gm == -INFINITY) ? 0.f : gm * sc;
+  const float ms = (gm == -INFINITY) ? 0.f : gm * p.scale;
+  const uint64_t SC = f2(p.scale, p.scale), NMS = f2(-ms, -ms);
+  uint64_t P[32];
 #pragma unroll
-  for (int j = 0; j < 64; ++j) {
-    const float t = fmaf(v[j], sc, -ms);
-    v[j] = (NP < 8 && (j & 7) < NP) ? exp2_poly(t) : fast_exp2(t);  // NP of every 8 on the FMA pipe
+  for (int j = 0; j < 32; ++j) {
+    const uint64_t t = f2_fma(f2(v[2 * j], v[2 * j + 1]), SC, NMS);
+    if ((j & 7) < NPX) {
+      P[j] = exp2_poly_x2(t);
+    } else {
+      float a, b;
+      f2_split(t, a, b);
+      P[j] = f2(fast_exp2(a), fast_exp2(b));
+    }
   }
   constexpr int CG = C < 64 ? C : 64;  // keys per chunk piece inside these 64 columns
-  tree_sum<64, CG>(v);                 // v[0 .. 64/CG) = chunk (piece) sums
-  float cs[64 / CG];
+  constexpr int NC = 64 / CG;          // chunk pieces
+  float cs[NC];
+  if constexpr (CG == 1) {
 #pragma unroll
-  for (int i = 0; i < 64 / CG; ++i) cs[i] = v[i];
-  tree_sum<64 / CG, 64 / CG>(v);
-  const float total = v[0];
+    for (int j = 0; j < 32; ++j) f2_split(P[j], cs[2 * j], cs[2 * j + 1]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NC; ++i) cs[i] = pair_sum<CG / 2>(P + i * (CG / 2));
+  }
+  float tot;
+  {
+    float t2[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) t2[i] = cs[i];
+#pragma unroll
+    for (int h = NC / 2; h >= 1; h /= 2) {
+#pragma unroll
+      for (int i = 0; i < h; ++i) t2[i] += t2[i + h];
+    }
+    tot = t2[0];
+  }
   if (!row_ok) return;
 #pragma unroll
-  for (int i = 0; i < 64 / CG; ++i) {
+  for (int i = 0; i < NC; ++i) {
     if (MASK && key0 / C + i >= p.g.m_loc) break;
     lamrow[(size_t)i * p.g.R] = (cs[i] > 0.f) ? ms + fast_log2(cs[i]) : -INFINITY;
   }
-  *lampart_out = (total > 0.f) ? ms + fast_log2(total) : -INFINITY;
+  *lampart_out = (tot > 0.f) ? ms + fast_log2(tot) : -INFINITY;
 }
 
 // Unit index bookkeeping without integer division in the loops: unit u = pr * MT + r covers
@@ -341,26 +420,40 @@ cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPa
   return cudaGetLastError();
 }
 
-// share of exponentials evaluated by exp2_poly (of every 8); CKV_SCORE_POLY overrides (tuning)
-int poly_share() {
+// pairs of every 8 (i.e. exponentials of every 16) evaluated by the FFMA2 polynomial instead of
+// MUFU.EX2; the tuning build's CKV_SCORE_POLY overrides it for A/B sweeps
+constexpr int kPolyPairs = 3;
+int poly_pairs() {
   static int np = -1;
   if (np < 0) {
     const char* e = tuning_env("CKV_SCORE_POLY");
-    np = e ? atoi(e) : 1;  // measured on B200: 1 of 8 exponentials on the FMA pipe is fastest
-    if (np < 0 || np > 3) np = 0;
+    np = e ? atoi(e) : kPolyPairs;
+    if (np < 0 || np > 8) np = kPolyPairs;
   }
   return np;
 }
 
 template <int C>
 cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
-  switch (poly_share()) {
-    case 3: return launch_cp<C, 3>(tmK, tmQ, p, grid, st);
-    case 2: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
+#ifdef CKV_TUNING
+  switch (poly_pairs()) {
+    case 0: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
     case 1: return launch_cp<C, 1>(tmK, tmQ, p, grid, st);
-    default: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
+    case 2: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
+    case 4: return launch_cp<C, 4>(tmK, tmQ, p, grid, st);
+    case 5: return launch_cp<C, 5>(tmK, tmQ, p, grid, st);
+    case 6: return launch_cp<C, 6>(tmK, tmQ, p, grid, st);
+    default: break;
   }
+#endif
+  (void)poly_pairs;
+  return launch_cp<C, kPolyPairs>(tmK, tmQ, p, grid, st);
 }
+
+#define CKV_SC(C) (const void*)score_tc_kernel<C, kPolyPairs>
+const int kReg = register_kernels({CKV_SC(1), CKV_SC(2), CKV_SC(4), CKV_SC(8), CKV_SC(16), CKV_SC(32), CKV_SC(64),
+                                   (const void*)pack_q_kernel});
+#undef CKV_SC
 
 }  // namespace
 

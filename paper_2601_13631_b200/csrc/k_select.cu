@@ -128,6 +128,11 @@ __global__ void __launch_bounds__(NT) block_cover_kernel(const int32_t* __restri
   if (threadIdx.x == 0) *n_blocks = base;
 }
 
+const int kReg = register_kernels({(const void*)topk_scores_kernel<1>, (const void*)topk_scores_kernel<2>,
+                                   (const void*)topk_scores_kernel<4>, (const void*)topk_scores_kernel<8>,
+                                   (const void*)topk_scores_big_kernel, (const void*)topk_merge_kernel,
+                                   (const void*)block_cover_kernel});
+
 }  // namespace
 
 cudaError_t launch_block_cover(const int32_t* ids, int n_ids, int u, int B, int64_t n, int32_t* blocks,

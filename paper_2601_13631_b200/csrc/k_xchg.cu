@@ -5,9 +5,9 @@
 //                      own window) and broadcast the merged rows (caller dtype) into every
 //                      rank's output image: the reduce-scatter + all-gather of the PAPER.md:99
 //                      softmax split over shards
-//   xchg_wait          stream memory operation: wait until own counter >= W, re-arm to 0
-#include <cuda.h>
-
+//   wait_reset_kernel  one thread waits (acquire) until the own counter reaches W, re-arms it
+//                      (one warp of one SM while waiting; as an ordinary kernel node the whole
+//                      exchange stays PDL-ordered and capturable in a CUDA graph)
 #include "common.cuh"
 #include "xchg.cuh"
 
@@ -69,17 +69,27 @@ __global__ void __launch_bounds__(256) merge_slice_kernel(XPeers xp, XLayout xl,
   }
 }
 
-using PFN_wait32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-using PFN_write32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-
-template <typename F>
-F driver_fn(const char* name) {
-  void* p = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-    return nullptr;
-  return reinterpret_cast<F>(p);
+// One thread spins (acquire, system scope) until this rank's counter reaches `target` -- all W
+// ranks have published -- then re-arms it.  It does not trigger its dependents early: the next
+// kernel starts only once the wait is over (and its griddepcontrol.wait sees the data).
+__global__ void wait_reset_kernel(uint32_t* flag, uint32_t target) {
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    uint32_t v;
+    int ns = 32;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if (v >= target) break;
+      __nanosleep(ns);
+      if (ns < 256) ns *= 2;
+    }
+    *flag = 0u;
+    __threadfence_system();
+  }
 }
+
+const int kReg = register_kernels({(const void*)put_signal_kernel, (const void*)merge_slice_kernel<float>,
+                                   (const void*)merge_slice_kernel<__nv_bfloat16>, (const void*)wait_reset_kernel});
 
 }  // namespace
 
@@ -103,16 +113,9 @@ template cudaError_t launch_xchg_merge<float>(const XPeers&, const XLayout&, int
 template cudaError_t launch_xchg_merge<__nv_bfloat16>(const XPeers&, const XLayout&, int, int, int, cudaStream_t);
 
 cudaError_t xchg_wait(cudaStream_t st, void* flag_dev, uint32_t target) {
-  static PFN_wait32 wait = driver_fn<PFN_wait32>("cuStreamWaitValue32");
-  static PFN_write32 write = driver_fn<PFN_write32>("cuStreamWriteValue32");
-  if (!wait || !write) return cudaErrorNotSupported;
-  const CUdeviceptr a = reinterpret_cast<CUdeviceptr>(flag_dev);
-  if (wait(reinterpret_cast<CUstream>(st), a, target, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
-    return cudaErrorUnknown;
-  if (write(reinterpret_cast<CUstream>(st), a, 0u, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
-    return cudaErrorUnknown;
-  pdl_mark_event_wait(st);  // the next kernel must not launch programmatically across the wait
-  return cudaSuccess;
+  if (cudaError_t e = launch_kernel(wait_reset_kernel, 1, 32, 0, st, static_cast<uint32_t*>(flag_dev), target))
+    return e;
+  return cudaGetLastError();
 }
 
 }  // namespace ckv

@@ -1,6 +1,15 @@
-"""Position-sharded Re-Prefill over W GPUs: one libckv context per rank,
-collectives over torch.distributed (NCCL on GPUs; the exchange pattern is also
-exercised on CPU with gloo by tests/test_dist_gloo.py through a backend stub).
+"""Position-sharded Re-Prefill over W GPUs: one libckv context per rank.
+
+Two ways to run the exchanges of a sharded layer:
+
+* fused (the product path): ``open_exchange(ctx)`` shares the ranks'
+  exchange windows once (64-byte IPC handles all-gathered over torch.distributed); from then
+  on ``ctx.reprefill_layer`` runs the whole sharded layer inside libckv -- producers write
+  into the peers' windows over NVLink and the streams wait on device counters, no host
+  round trip and no NCCL call per layer;
+* ``ShardedReprefill``: the split-phase C-ABI calls with the collectives issued from the
+  host over torch.distributed (NCCL on GPUs, gloo in the CPU / one-GPU tests) -- the
+  NCCL-collective baseline the fused path is compared against.
 
 Per layer, with q / k_suf / v_suf replicated on every rank:
   1. ckv_shard_score       local row normalisers  lam_g [Hq*n_s]            (A1 + A2 local)
@@ -19,6 +28,15 @@ from __future__ import annotations
 
 import torch
 import torch.distributed as dist
+
+
+def open_exchange(ctx, group=None):
+    """Attach ctx (shard_index = rank, num_shards = world size) to its peers' exchange windows:
+    all-gather the 64-byte handles in rank order, then ckv_exchange_open (collective)."""
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, ctx.exchange_handle(), group=group)
+    ctx.exchange_open(handles)
+    dist.barrier(group=group)
 
 
 class ShardedReprefill:

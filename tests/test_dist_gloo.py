@@ -112,3 +112,39 @@ def test_sharded_protocol_gloo(W, cyclic):
         got, want, err = ret[r]
         assert got == want
         assert err < 1e-5
+
+
+class _HandleCtx:
+    """Stand-in exposing the exchange-handle part of the Context API (64-byte IPC handles)."""
+
+    EXCHANGE_HANDLE_BYTES = 64
+
+    def __init__(self, rank, W):
+        self.rank, self.W, self.opened = rank, W, None
+
+    def exchange_handle(self):
+        return bytes([self.rank + 1]) * self.EXCHANGE_HANDLE_BYTES
+
+    def exchange_open(self, handles):
+        self.opened = list(handles)
+
+
+def _handle_worker(rank, W, port, ret):
+    from paper_2601_13631_b200.sharded import open_exchange
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=W)
+    ctx = _HandleCtx(rank, W)
+    open_exchange(ctx)
+    ret[rank] = ctx.opened
+    dist.destroy_process_group()
+
+
+def test_open_exchange_gathers_handles_in_rank_order():
+    # the fused path's one-time setup (sharded.open_exchange): every rank receives all W window
+    # handles in rank order before ckv_exchange_open (include/ckv.h)
+    W, port = 3, _free_port()
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(_handle_worker, args=(W, port, ret), nprocs=W, join=True)
+    for r in range(W):
+        assert ret[r] == [bytes([g + 1]) * 64 for g in range(W)]
