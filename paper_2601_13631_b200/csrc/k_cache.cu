@@ -34,12 +34,15 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
 }
 
 // Whole-record copy host store -> HBM slot: work items are 4 KiB segments of records so a
-// few misses still keep many 16-B loads in flight over the host link.
+// few misses still keep many 16-B loads in flight over the host link.  Small CTAs (4 warps,
+// <= 64 registers): one fits on an SM beside a persistent score / attention CTA (576 threads x
+// 96 registers), so a side-stream prefetch never holds an SM the next layer's persistent
+// kernels need (a blocked SM would delay their whole statically partitioned launch).
 constexpr int GATHER_SEG = 4096;
-constexpr int GATHER_THREADS = 256;
-constexpr int GATHER_BLOCKS = 64;
+constexpr int GATHER_THREADS = 128;
+constexpr int GATHER_BLOCKS = 128;
 
-__global__ void __launch_bounds__(GATHER_THREADS) gather_kernel(const int32_t* __restrict__ list,
+__global__ void __launch_bounds__(GATHER_THREADS, 8) gather_kernel(const int32_t* __restrict__ list,
                                                                 const int32_t* __restrict__ n_load,
                                                                 const char* __restrict__ host_layer,
                                                                 char* __restrict__ pool_layer, int64_t rec_bytes) {

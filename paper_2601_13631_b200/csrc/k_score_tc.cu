@@ -44,6 +44,8 @@ struct TcParams {
   int q_direct;  // 1: Q tiles straight from q [ns][Hq][128] by a 3-D map (n_s % 128 == 0), no pack
   int n_units;  // Hkv * NKT * MT
   float scale;  // log2(e) / sqrt(d)
+  int epi_sleep;  // epilogue warps wait for their accumulator with a suspend-time hint
+  unsigned long long* trace;  // tuning build (CKV_SCORE_TRACE=1): %globaltimer events of CTA 0, else null
 };
 
 // ---- packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two fp32 lanes per instruction) ----
@@ -202,6 +204,17 @@ struct UnitIter {
   }
 };
 
+// tuning build only: event e of unit i (< 32) of CTA 0
+__device__ __forceinline__ void trace_ev(const TcParams& p, int e, int i) {
+#ifdef CKV_TUNING
+  if (p.trace && blockIdx.x == 0 && i < 32) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[e * 32 + i] = t;
+  }
+#endif
+}
+
 template <int C, int NP>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ, TcParams p) {
@@ -219,6 +232,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kQStages);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef CKV_TUNING
+  if (p.trace && threadIdx.x == 0) {  // per-CTA start (slot 5) / end (slot 6) events
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[5 * 32 + blockIdx.x] = t;
+  }
+#endif
   // units: (kv head, key tile) pairs x row tiles; the row-tile order is rotated by the pair index
   // (a bijection inside every pair, whichever CTAs share it) so the CTAs working on one KV head
   // at a time do not all fetch the same Q tile from L2 at once
@@ -230,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
       ptx::mbar_init(&acc_full[i], 1);
-      ptx::mbar_init(&acc_empty[i], kEpiWarps);
+      ptx::mbar_init(&acc_empty[i], kEpiWarps / 2);  // one epilogue group per buffer
     }
     for (int i = 0; i < kQStages; ++i) {
       ptx::mbar_init(&q_full[i], 1);
@@ -295,8 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int qs = qcount % kQStages;
         ptx::mbar_wait_sleep(&q_full[qs], (qcount / kQStages) & 1);
+        trace_ev(p, 0, acount);  // Q (and K) of the unit landed
         const int ab = acount & 1;
         ptx::mbar_wait_sleep(&acc_empty[ab], ((acount >> 1) & 1) ^ 1);
+        trace_ev(p, 1, acount);  // accumulator free: MMAs issued
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + ab * BN;
         const uint32_t qa = ptx::smem_u32(qbuf0 + qs * kQBytes);
@@ -319,59 +341,83 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     pdl_wait();
     pdl_trigger();  // after this CTA's own dependency is resolved (see common.cuh)
+    // Two epilogue groups of 8 warps, one per accumulator buffer: group g drains the units
+    // whose accumulator is buffer g (every other unit), so the groups run one MMA apart and the
+    // exp2 phase of one overlaps the TMEM-load / max / sum / store phases of the other (with
+    // every warp on every unit, all sixteen hit the MUFU pipe at once and leave it idle after).
+    // In a group, the 2 warps of each TMEM lane quadrant take 128 columns each, in two passes
+    // of 64; the accumulator is released after the second pass's TMEM load.
     const int e = warp - 2;
-    const int quad = warp & 3;
-    const int half = e >> 2;  // column quarter
+    const int quad = warp & 3;                // TMEM lane quadrant (warp id % 4)
+    const int grp = (e >> 2) & 1;             // accumulator buffer drained by this warp
+    const int chalf = e >> 3;                 // 128-column half of the 256 columns
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const int nfull = p.g.n_loc / BN;  // key tiles without a ragged tail
     int acount = 0;
     UnitIter it(u0, p.MT, p.NKT);
-    for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT)) {
-      const int mt = it.mt(p.MT), kvh = it.kvh, kt = it.kt;
+    for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT), ++acount) {
       const int ab = acount & 1;
-      ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
+      if (ab != grp) continue;
+      const int mt = it.mt(p.MT), kvh = it.kvh, kt = it.kt;
+      if (p.epi_sleep)
+        ptx::mbar_wait_sleep(&acc_full[ab], (acount >> 1) & 1);
+      else
+        ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
       ptx::tc_fence_after();
+      if (lane == 0 && e < 8 && (e & 3) == 0) trace_ev(p, 2, acount);  // group's first warp: MMA done
       if (mt * BM + quad * 32 >= p.g.R) {  // warp-uniform: this lane quadrant is all padding rows
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
-        ++acount;
         continue;
       }
       const int rho = mt * BM + row_in_tile;
       const bool row_ok = rho < p.g.R;
-      // both 32-key groups are read from TMEM, then the accumulator is released at once
-      float v[64];
-      {
-        uint32_t r0[32], r1[32];
-        const uint32_t ta = tmem_base + (uint32_t)(ab * BN + half * (BN / kColSplit)) + lane_off;
-        ptx::tmem_ld32_nowait(ta, r0);
-        ptx::tmem_ld32_nowait(ta + 32, r1);
-        ptx::tmem_wait_ld_tied(r0);
-        ptx::tmem_wait_ld_tied(r1);
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const int cq = chalf * 2 + pass;  // 64-column quarter of the key tile
+        float v[64];
+        {
+          uint32_t r0[32], r1[32];
+          const uint32_t ta = tmem_base + (uint32_t)(ab * BN + cq * (BN / kColSplit)) + lane_off;
+          ptx::tmem_ld32_nowait(ta, r0);
+          ptx::tmem_ld32_nowait(ta + 32, r1);
+          ptx::tmem_wait_ld_tied(r0);
+          ptx::tmem_wait_ld_tied(r1);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          v[j] = __uint_as_float(r0[j]);
-          v[32 + j] = __uint_as_float(r1[j]);
+          for (int j = 0; j < 32; ++j) {
+            v[j] = __uint_as_float(r0[j]);
+            v[32 + j] = __uint_as_float(r1[j]);
+          }
+        }
+        if (pass == 1) {  // both quarters read: release the accumulator to the MMA warp
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
+          if (lane == 0 && e < 8 && (e & 3) == 0) trace_ev(p, 3, acount);
+        }
+        const int key0 = kt * BN + cq * (BN / kColSplit);
+        float* lamrow = p.lam2 + ((size_t)kvh * p.g.m_loc + key0 / C) * p.g.R + rho;
+        float* lp = p.lampart + ((size_t)kvh * p.nsplit + kt * kColSplit + cq) * p.g.R + rho;
+        if (kt >= nfull) {  // warp-uniform: the last key tile only
+          epilogue_unit<C, NP, true>(p, v, key0, lamrow, lp, row_ok);
+        } else {
+          epilogue_unit<C, NP, false>(p, v, key0, lamrow, lp, row_ok);
         }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
-      const int key0 = kt * BN + half * (BN / kColSplit);
-      float* lamrow = p.lam2 + ((size_t)kvh * p.g.m_loc + key0 / C) * p.g.R + rho;
-      float* lp = p.lampart + ((size_t)kvh * p.nsplit + kt * kColSplit + half) * p.g.R + rho;
-      if (kt >= nfull) {  // warp-uniform: the last key tile only
-        epilogue_unit<C, NP, true>(p, v, key0, lamrow, lp, row_ok);
-      } else {
-        epilogue_unit<C, NP, false>(p, v, key0, lamrow, lp, row_ok);
-      }
-      ++acount;
+      if (lane == 0 && e < 8 && (e & 3) == 0) trace_ev(p, 4, acount);  // epilogue of the unit done
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
+#ifdef CKV_TUNING
+  if (p.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[5 * 32 + 160 + blockIdx.x] = t;
+  }
+#endif
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem_base);
@@ -480,6 +526,19 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   p.R_pad = p.MT * BM;
   p.n_units = g.Hkv * p.NKT * p.MT;
   p.scale = kLog2e / sqrtf((float)g.d);
+  p.trace = nullptr;
+  p.epi_sleep = 1;
+#ifdef CKV_TUNING
+  if (const char* es = tuning_env("CKV_SCORE_EPI_SLEEP")) p.epi_sleep = atoi(es);
+#endif
+#ifdef CKV_TUNING
+  static unsigned long long* trace_buf = nullptr;
+  if (tuning_env("CKV_SCORE_TRACE")) {
+    if (!trace_buf) cudaMalloc(&trace_buf, (5 * 32 + 320) * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_buf, 0, (5 * 32 + 320) * sizeof(unsigned long long), st);
+    p.trace = trace_buf;
+  }
+#endif
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
   p.q_direct = (g.ns % BM) == 0 ? 1 : 0;
   if (!p.q_direct)
@@ -494,16 +553,47 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
     return cudaErrorInvalidValue;
   }
   const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
+  cudaError_t el;
   switch (g.c) {
-    case 1: return launch_c<1>(tmK, tmQ, p, grid, st);
-    case 2: return launch_c<2>(tmK, tmQ, p, grid, st);
-    case 4: return launch_c<4>(tmK, tmQ, p, grid, st);
-    case 8: return launch_c<8>(tmK, tmQ, p, grid, st);
-    case 16: return launch_c<16>(tmK, tmQ, p, grid, st);
-    case 32: return launch_c<32>(tmK, tmQ, p, grid, st);
-    case 64: return launch_c<64>(tmK, tmQ, p, grid, st);
+    case 1: el = launch_c<1>(tmK, tmQ, p, grid, st); break;
+    case 2: el = launch_c<2>(tmK, tmQ, p, grid, st); break;
+    case 4: el = launch_c<4>(tmK, tmQ, p, grid, st); break;
+    case 8: el = launch_c<8>(tmK, tmQ, p, grid, st); break;
+    case 16: el = launch_c<16>(tmK, tmQ, p, grid, st); break;
+    case 32: el = launch_c<32>(tmK, tmQ, p, grid, st); break;
+    case 64: el = launch_c<64>(tmK, tmQ, p, grid, st); break;
     default: return cudaErrorNotSupported;
   }
+#ifdef CKV_TUNING
+  if (p.trace && el == cudaSuccess) {  // synchronous dump of CTA 0's events (us since its first)
+    unsigned long long h[5][32], cta[320];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, p.trace, sizeof h, cudaMemcpyDeviceToHost);
+    cudaMemcpy(cta, p.trace + 5 * 32, sizeof cta, cudaMemcpyDeviceToHost);
+    {
+      unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+      for (int b = 0; b < grid; ++b) {
+        s0 = cta[b] < s0 ? cta[b] : s0;
+        s1 = cta[b] > s1 ? cta[b] : s1;
+        e0 = cta[160 + b] < e0 ? cta[160 + b] : e0;
+        e1 = cta[160 + b] > e1 ? cta[160 + b] : e1;
+      }
+      fprintf(stderr, "[score trace] CTA start spread %.2f us, end %.2f..%.2f us after first start; CTA0 start %.2f end %.2f\n",
+              (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, (e1 - s0) * 1e-3, (cta[0] - s0) * 1e-3, (cta[160] - s0) * 1e-3);
+    }
+    unsigned long long t0 = ~0ull;
+    for (auto& r : h)
+      for (unsigned long long t : r)
+        if (t && t < t0) t0 = t;
+    const char* nm[5] = {"q_land", "acc_free", "mma_done", "release", "epi_done"};
+    for (int ev = 0; ev < 5; ++ev) {
+      fprintf(stderr, "[score trace] %-8s", nm[ev]);
+      for (int i = 0; i < 32; ++i) fprintf(stderr, " %6.2f", h[ev][i] ? (h[ev][i] - t0) * 1e-3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+  }
+#endif
+  return el;
 }
 
 }  // namespace ckv

@@ -52,10 +52,16 @@ def main():
             rows.append(row)
             print(json.dumps(row), flush=True)
     rate = sum(r["strict"] for r in rows) / len(rows)
+    # per layer: size of the union of the requests' selected sets (what an HBM cache must hold to
+    # serve every request of the stream without host loads)
+    unions = {}
+    for (l, r), ids in prev.items():
+        unions.setdefault(l, set()).update(int(x) for x in ids)
     cov = [r["coverage_prev"] for r in rows if "coverage_prev" in r]
     summ = {"cfg": a.cfg, "k": k, "draws": len(rows), "gate_pass_rate": rate,
             "coverage_prev_mean": float(np.mean(cov)) if cov else None,
-            "topk_share_mean": float(np.mean([r["topk_share"] for r in rows])), "seconds": time.time() - t0}
+            "topk_share_mean": float(np.mean([r["topk_share"] for r in rows])),
+            "union_per_layer_mean": float(np.mean([len(u) for u in unions.values()])), "seconds": time.time() - t0}
     print(json.dumps(summ))
     if a.out:
         with open(a.out, "w") as f:

@@ -1,20 +1,13 @@
 #!/bin/bash
-# compute-sanitizer memcheck / racecheck on small configurations (GPU box).
+# compute-sanitizer memcheck / racecheck / synccheck on small configurations (GPU box) ->
+# gpurun_out/{memcheck,racecheck,synccheck}.log  (scripts/san_case.py)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-cat > /tmp/san_case.py << 'PY'
-import os, sys
-sys.path.insert(0, os.getcwd())
-import torch
-from synth import ShapeConfig, CONFIGS
-from tests.gpu_util import make_ctx, run_layers
-for cfg in (CONFIGS["c1_0.5b"], ShapeConfig("s", 2, 8, 2, 128, 3001, 16, 40, 1000, "bf16")):
-    ctx, prefix = make_ctx(cfg, prefetch=8, k=16 if cfg.dtype == "bf16" else 0)
-    run_layers(ctx, cfg, prefix, range(cfg.num_layers))
-    run_layers(ctx, cfg, prefix, range(cfg.num_layers), request=1)
-    ctx.close()
-print("sanitize case done")
-PY
-timeout 900 compute-sanitizer --tool memcheck --leak-check no python /tmp/san_case.py > gpurun_out/memcheck.log 2>&1
-echo "memcheck rc=$?" >> gpurun_out/memcheck.log
-tail -5 gpurun_out/memcheck.log
+export CUDA_DEVICE_MAX_CONNECTIONS=32
+for T in memcheck racecheck synccheck; do
+  extra=""
+  [ "$T" == "memcheck" ] && extra="--leak-check no"
+  timeout 1200 compute-sanitizer --tool $T $extra python scripts/san_case.py > gpurun_out/$T.log 2>&1
+  echo "$T rc=$?" >> gpurun_out/$T.log
+  tail -3 gpurun_out/$T.log
+done

@@ -7,19 +7,20 @@ can regenerate exactly the same values independently.  Seed 42 is the paper's
 
 Structure of the values (no method arithmetic here, only the recipe):
 
-* Prefix keys carry two per-layer unit "topic" directions u1, u2 per KV head.
-  Chunk j of layer l has two salience fields s1[l, j], s2[l, j] (logit offsets on a
+* Prefix keys carry N_TOPICS = 4 per-layer unit "topic" directions u_t per KV head.
+  Chunk j of layer l has one salience field s_t[l, j] per topic (logit offsets on a
   geometric rank profile, see salience()) whose latent ranks follow an AR(1) process
   across layers (correlation ``rho``), so adjacent layers select overlapping chunk sets
   (the paper's cross-layer similarity).  Chunk 0 gets a sink boost
   and the last chunk a recency boost.
-    Kp[i, h] = N(0, I) + (s1[j(i)] * u1[h] + s2[j(i)] * u2[h]) * sqrt(d) / gamma
-* A request's suffix queries point at a mixture of the two topics with a
-  request-specific angle theta (so different requests share part of their
-  chunk sets -- something for the attention-guided cache to retain):
-    Qs[r, h] = gamma * (cos(theta) u1[h//G] + sin(theta) u2[h//G]) + N(0, I)
-  so the prefix logit q.k/sqrt(d) has mean ~ cos(theta) s1 + sin(theta) s2
-  and O(1) noise: softmax rows are neither uniform nor one-hot.
+    Kp[i, h] = N(0, I) + sum_t s_t[j(i)] * u_t[h] * sqrt(d) / gamma
+* A request's suffix queries point at a request-specific mixture of the topics, a unit
+  weight vector w >= 0 (|N(0, I_4)| normalised), so different requests share part of
+  their chunk sets (sink, recency, the topics they weigh alike -- something for the
+  attention-guided cache to retain) and differ in the rest:
+    Qs[r, h] = gamma * sum_t w_t u_t[h//G] + N(0, I)
+  so the prefix logit q.k/sqrt(d) has mean ~ sum_t w_t s_t and O(1) noise: softmax
+  rows are neither uniform nor one-hot.
 * Prefix V, suffix K and suffix V are N(0, 1).
 
 All values are rounded once to bf16 (round-to-nearest-even) for bf16 configs;
@@ -35,7 +36,9 @@ import numpy as np
 SEED = 42
 
 # tensor ids for the Philox key
-_T_SAL1, _T_SAL2, _T_TOPIC, _T_KP, _T_VP, _T_QS, _T_KS, _T_VS, _T_THETA = range(9)
+_T_TOPIC, _T_KP, _T_VP, _T_QS, _T_KS, _T_VS, _T_MIX = range(2, 9)
+_T_SAL = 16      # salience field t uses tensor id _T_SAL + t
+N_TOPICS = 4
 
 
 @dataclasses.dataclass(frozen=True)
@@ -103,7 +106,7 @@ TOP = 2.0     # logit offset of the most salient ordinary chunk
 
 def salience(cfg: ShapeConfig, layer: int, seed: int = SEED, rho: float = 0.9,
              span: float = SPAN, sink: float = 2.0, recency: float = 1.0):
-    """Two chunk-salience fields (logit offsets, nats) of length m for `layer`.
+    """N_TOPICS chunk-salience fields (logit offsets, nats) of length m for `layer`.
 
     Each field is a latent Gaussian z[l, j] following an AR(1) process across layers
     (correlation rho: adjacent layers select overlapping sets) mapped
@@ -118,7 +121,7 @@ def salience(cfg: ShapeConfig, layer: int, seed: int = SEED, rho: float = 0.9,
 
     m = cfg.num_chunks
     out = []
-    for t in (_T_SAL1, _T_SAL2):
+    for t in range(_T_SAL, _T_SAL + N_TOPICS):
         z = _rng(seed, t, 0).standard_normal(m)
         for l in range(1, layer + 1):
             eps = _rng(seed, t, l).standard_normal(m)
@@ -127,14 +130,22 @@ def salience(cfg: ShapeConfig, layer: int, seed: int = SEED, rho: float = 0.9,
         s[0] = TOP + sink
         s[-1] = TOP + recency
         out.append(s)
-    return out[0], out[1]
+    return out
 
 
 def _topics(cfg: ShapeConfig, layer: int, seed: int):
+    """[N_TOPICS, Hkv, d] unit topic directions of one layer."""
     g = _rng(seed, _T_TOPIC, layer)
-    u = g.standard_normal((2, cfg.num_kv_heads, cfg.head_dim))
+    u = g.standard_normal((N_TOPICS, cfg.num_kv_heads, cfg.head_dim))
     u /= np.linalg.norm(u, axis=-1, keepdims=True)
-    return u[0], u[1]
+    return u
+
+
+def request_mix(request: int, seed: int = SEED) -> np.ndarray:
+    """Unit topic weights w >= 0 of one request (|N(0, I)| normalised, uniform on the positive
+    orthant of the sphere)."""
+    w = np.abs(_rng(seed, _T_MIX, 0, request).standard_normal(N_TOPICS))
+    return w / np.linalg.norm(w)
 
 
 GAMMA = 4.0
@@ -143,12 +154,13 @@ GAMMA = 4.0
 def make_prefix(cfg: ShapeConfig, layer: int, seed: int = SEED, **sal_kw):
     """Prefix K, V of one layer, token-major [n, Hkv, d] (float32 holding bf16 values)."""
     n, hkv, d, c = cfg.prefix_len, cfg.num_kv_heads, cfg.head_dim, cfg.chunk_size
-    s1, s2 = salience(cfg, layer, seed, **sal_kw)
-    u1, u2 = _topics(cfg, layer, seed)
+    sal = salience(cfg, layer, seed, **sal_kw)
+    u = _topics(cfg, layer, seed)
     tok_chunk = np.arange(n) // c
     k = _rng(seed, _T_KP, layer).standard_normal((n, hkv, d), dtype=np.float32)
     scale = math.sqrt(d) / GAMMA
-    k += (s1[tok_chunk, None, None] * u1[None] + s2[tok_chunk, None, None] * u2[None]).astype(np.float32) * np.float32(scale)
+    for t in range(N_TOPICS):
+        k += (sal[t][tok_chunk, None, None] * u[t][None]).astype(np.float32) * np.float32(scale)
     v = _rng(seed, _T_VP, layer).standard_normal((n, hkv, d), dtype=np.float32)
     return _finish(k, cfg.dtype), _finish(v, cfg.dtype)
 
@@ -158,9 +170,8 @@ def make_request(cfg: ShapeConfig, layer: int, request: int = 0, seed: int = SEE
     """Suffix Q [n_s, Hq, d], K, V [n_s, Hkv, d] of one request at one layer."""
     ns = cfg.suffix_len if suffix_len is None else suffix_len
     hq, hkv, d, G = cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.group
-    theta = _rng(seed, _T_THETA, 0, request).uniform(0.0, math.pi / 2)
-    u1, u2 = _topics(cfg, layer, seed)
-    dirn = math.cos(theta) * u1 + math.sin(theta) * u2  # [Hkv, d]
+    w = request_mix(request, seed)
+    dirn = np.tensordot(w, _topics(cfg, layer, seed), axes=1)  # [Hkv, d]
     q = _rng(seed, _T_QS, layer, request).standard_normal((ns, hq, d), dtype=np.float32)
     q += (GAMMA * dirn[np.arange(hq) // G][None]).astype(np.float32)
     ks = _rng(seed, _T_KS, layer, request).standard_normal((ns, hkv, d), dtype=np.float32)
