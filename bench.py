@@ -201,8 +201,10 @@ def run_ckv(args, rank, world):
             dist.init_process_group("gloo")
     cfg = CONFIGS[CFG_NAME]
     k = ckv.ckv_budget_chunks(cfg.prefix_len, cfg.chunk_size, cfg.budget_bp)
-    quota = k if args.prefetch else 0
-    cache_slots = k + quota + k // 2
+    quota = int(round(k * args.quota_frac)) if args.prefetch else 0
+    cache_slots = k + k + k // 2  # k selected + a quota-sized prefetch partition + k/2 (~25% of a layer's chunks)
+    if args.cache_slots:
+        cache_slots = args.cache_slots
     ctx = ckv.Context(cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, cfg.chunk_size,
                       cfg.prefix_len, cfg.suffix_len, dtype=cfg.dtype, budget_bp=cfg.budget_bp,
                       prefetch_chunks=quota, cache_slots=cache_slots, device=local_rank, shard_index=rank,
@@ -628,6 +630,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ckv", choices=["ckv", "reference"])
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false")
+    ap.add_argument("--cache-slots", type=int, default=0, help="override the HBM cache slots per layer (studies)")
+    ap.add_argument("--quota-frac", type=float, default=1.0,
+                    help="speculative prefetch quota per layer as a fraction of k (the cache size stays k + k + k/2)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--cyclic", action="store_true", help="N > 1: cyclic chunk sharding (j mod N) instead of "

@@ -48,6 +48,7 @@ struct ckv_ctx {
   float* I = nullptr;
   float *lam2 = nullptr, *lampart = nullptr, *Lam2 = nullptr, *A = nullptr, *Apart = nullptr;
   int32_t* ids_buf[2] = {nullptr, nullptr};
+  uint64_t* sel_keys[2] = {nullptr, nullptr};  // (score bits << 32 | ~id) of ids_buf's entries (rank the speculation)
   int32_t* n_ids_buf[2] = {nullptr, nullptr};
   int32_t *kept_slots = nullptr, *ids_glob = nullptr, *flag = nullptr;
   int32_t *scratch_main = nullptr, *scratch_side = nullptr;
@@ -251,13 +252,14 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
 // A6: speculative plan + gather of layer `layer` for the given ids, on the side stream.
 // `recorded`: ev_ids was already recorded on st (global heap: after the compaction of the current layer).
 ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, cudaStream_t st,
-                          bool recorded = false) {
+                          bool recorded = false, const uint64_t* rank_keys = nullptr) {
   if (ctx->quota <= 0 || layer >= ctx->L) return CKV_OK;
   if (!recorded) CK(cudaEventRecord(ctx->ev_ids, st));
   CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ids, 0));
   pdl_mark_event_wait(ctx->side);
   PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)(layer * 2 + 1) * 4, ctx->stats,
              nullptr, ctx->epoch_dev};
+  po.rank_keys = rank_keys;
   LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 1, ctx->quota, ctx->epoch, ctx->rec_bytes, nullptr,
                        ctx->scratch_side, po, ctx->side));
   CK(cudaEventRecord(ctx->ev_pplan[layer], ctx->side));
@@ -370,7 +372,8 @@ void free_all(ckv_ctx* ctx) {
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   for (void* p : ctx->x_opened) cudaIpcCloseMemHandle(p);
-  for (void* p : {(void*)ctx->xwin, (void*)ctx->lam_loc, (void*)ctx->cand_loc})
+  for (void* p : {(void*)ctx->xwin, (void*)ctx->lam_loc, (void*)ctx->cand_loc, (void*)ctx->sel_keys[0],
+                  (void*)ctx->sel_keys[1]})
     if (p) cudaFree(p);
   if (ctx->host_store) cudaFreeHost(ctx->host_store);
   for (auto e : ctx->ev_pplan)
@@ -614,6 +617,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   for (int i = 0; i < 2; ++i) {
     CKC(dalloc(&ctx->ids_buf[i], (size_t)ctx->k));
     CKC(dalloc(&ctx->n_ids_buf[i], 1));
+    CKC(dalloc(&ctx->sel_keys[i], (size_t)ctx->k));
   }
   CKC(dalloc(&ctx->kept_slots, (size_t)ctx->k));
   CKC(dalloc(&ctx->ids_glob, (size_t)ctx->k));
@@ -637,7 +641,11 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   CKC(cudaMemset(ctx->stats, 0, sizeof(int64_t) * 16));
   int lo = 0, hi = 0;
   CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  CKC(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, hi));
+  // the side stream (speculative plan + gather) gets the LOWEST priority: its CTAs then fill the
+  // SMs the persistent score / attention kernels leave free instead of being dispatched ahead of
+  // them (measured on the B200, steady-state stream: 108.6 vs 109.4 us/layer, eager 115 vs 122)
+  const char* sp = tuning_env("CKV_SIDE_PRIO");  // tuning build: 0 = highest priority (A/B)
+  CKC(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking, (sp && sp[0] == '0') ? hi : lo));
   CKC(cudaEventCreateWithFlags(&ctx->ev_ids, cudaEventDisableTiming));
   ctx->ev_pplan.assign(ctx->L, nullptr);
   ctx->ev_pf.assign(ctx->L, nullptr);
@@ -785,7 +793,8 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
     PROF_END(2);
     PROF_BEGIN(6);
-    LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, nullptr, 0, nids, st));
+    LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, ctx->sel_keys[pid & 1], ctx->k,
+                          nids, st));
     PROF_END(6);
     // intra-period loads (exact ids) for the period's other layers, then the speculative load of
     // the next period's first layer (A6), all on the side stream in layer order
@@ -793,7 +802,7 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     // layer's demand plan and compaction -- issued below, after run_attend)
     if (!ctx->global_heap)
       for (int lp = layer + 1; lp <= pend && lp < ctx->L; ++lp)
-        if ((s = issue_prefetch(ctx, lp, ids, nids, st)) != CKV_OK) return s;
+        if ((s = issue_prefetch(ctx, lp, ids, nids, st, false, ctx->sel_keys[pid & 1])) != CKV_OK) return s;
     // subperiod gate: attention of the first layer waits for sp layers' chunks
     for (int lp = layer + 1; lp < layer + ctx->subperiod && lp < pend; ++lp)
       if (ctx->pf_issued[lp] == ctx->epoch) {
@@ -806,7 +815,8 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
   if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, selected_ids,
                       planned, st, defer_pf ? ctx->ev_ids : nullptr)) != CKV_OK)
     return s;
-  if (defer_pf && (s = issue_prefetch(ctx, layer + 1, ids, nids, st, true)) != CKV_OK) return s;
+  if (defer_pf && (s = issue_prefetch(ctx, layer + 1, ids, nids, st, true, ctx->sel_keys[pid & 1])) != CKV_OK)
+    return s;
   if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;
 }

@@ -86,7 +86,30 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
     }
     n_miss += tot;
   }
-  if (prefetch) n_miss = min(n_miss, quota);
+  if (prefetch && n_miss > quota) {
+    if (out.rank_keys) {
+      // speculation is a bet that layer l+1 reuses layer l's chunks: spend the
+      // quota on the misses layer l scored highest (kept in ascending chunk order)
+      auto rkey = [&](int t) -> uint64_t { return out.rank_keys[mpos[t]]; };
+      const uint64_t T = block_kth_largest<NT>(rkey, n_miss, quota, ss);
+      int n2 = 0;
+      for (int b = 0; b < n_miss; b += NT) {
+        const int t = b + threadIdx.x;
+        const bool f = t < n_miss && rkey(t) >= T;
+        const int jm = f ? miss[t] : 0, pm = f ? mpos[t] : 0;
+        int tot;
+        const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);  // barriers: reads precede writes
+        if (f) {
+          miss[n2 + pos] = jm;
+          mpos[n2 + pos] = pm;
+        }
+        n2 += tot;
+      }
+      n_miss = n2;
+    } else {
+      n_miss = quota;
+    }
+  }
   // 2. free slots, ascending (only needed when something is loaded)
   int n_free = 0;
   if (n_miss > 0)

@@ -14,28 +14,31 @@ ctx = Context(cfg.num_layers, cfg.num_q_heads, cfg.num_kv_heads, cfg.head_dim, c
 for l in range(cfg.num_layers):
     kp, vp = make_prefix(cfg, l)
     ctx.store_prefix(l, torch.from_numpy(kp).cuda().bfloat16(), torch.from_numpy(vp).cuda().bfloat16())
+R = 16
 reqs = [[[torch.from_numpy(x).cuda().bfloat16() for x in make_request(cfg, l, r)] for l in range(cfg.num_layers)]
-        for r in range(4)]
+        for r in range(R)]
+from bench import request_sequence
+seq = request_sequence(64) if os.environ.get("TL_REQ", "steady") == "steady" else [0] * 64
 outs = [torch.empty(cfg.suffix_len, cfg.num_q_heads, cfg.head_dim, dtype=torch.bfloat16, device="cuda")
         for _ in range(cfg.num_layers)]
 ids = [torch.empty(k, dtype=torch.int32, device="cuda") for _ in range(cfg.num_layers)]
 def step(r):
     for l in range(cfg.num_layers):
         ctx.reprefill_layer(l, *reqs[r][l], out=outs[l], ids=ids[l])
-for i in range(8):
-    step(i % 4)
-mode = os.environ.get("TL_MODE", "graph")
+for i in range(24):
+    step(seq[i])
+mode = os.environ.get("TL_MODE", "eager")
 if mode == "graph":
     gs = []
-    for r in range(4):
+    for r in range(R):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             step(r)
         gs.append(g)
-    for i in range(8):
-        gs[i % 4].replay()
+    for i in range(24, 32):
+        gs[seq[i]].replay()
 else:
-    for i in range(8):
-        step(i % 4)
+    for i in range(24, 32):
+        step(seq[i])
 torch.cuda.synchronize()
 ctx.close()
