@@ -162,6 +162,9 @@ LayerGeom geom(const ckv_ctx* ctx, int ns) {
 int simt_score_nsplit(const ckv_ctx* ctx, int ns) {
   const int rowblocks = (ctx->G * ns + 63) / 64;
   int s = (4 * 296 + rowblocks * ctx->Hkv - 1) / (rowblocks * ctx->Hkv);
+  // every split reloads its 64-row Q tile: give each at least 2 key sub-tiles (128 keys) of work
+  const int by_keys = (ctx->n_loc + 127) / 128;
+  s = s > by_keys ? by_keys : s;
   s = s < 1 ? 1 : s;
   return s > ctx->m_loc ? ctx->m_loc : s;
 }

@@ -148,6 +148,13 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __re
       }
       // record offset of this piece: swizzled [Hkv][K|V][half] pieces, or V-only [Hkv][half]
       const int64_t off = g.rec_swz == 2 ? ((int64_t)kvh * 2 + (part - 2)) * piece : (int64_t)kvh * 4 * piece + part * piece;
+      // record rows are swizzled by (row in chunk) & 7; in the tile a row sits at key + p, so for
+      // c % 8 != 0 (chunk sizes 1, 2, 4) each 16-byte unit is re-swizzled on the way
+      const int rs = key & 7;  // 0 whenever c % 8 == 0: units copy as they are
+      auto dunit = [&](int idx) {  // destination unit of source unit idx (row idx / 8, unit idx % 8)
+        const int p8 = idx >> 3, us = idx & 7;
+        return rs == 0 ? idx : p8 * 8 + ((us ^ (p8 & 7)) ^ ((rs + p8) & 7));
+      };
       if (slot >= 0) {
         const uint4* src = reinterpret_cast<const uint4*>(pool + (int64_t)slot * rec_bytes + off);
         const int nu = (int)(piece / 16);
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __re
             if (u0 + lane + 32 * q < nu) v[q] = __ldcg(src + u0 + lane + 32 * q);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (u0 + lane + 32 * q < nu) dst[u0 + lane + 32 * q] = v[q];
+            if (u0 + lane + 32 * q < nu) dst[dunit(u0 + lane + 32 * q)] = v[q];
         }
       } else {
         const uint4* src = reinterpret_cast<const uint4*>(host_layer + (int64_t)kept_ids[i] * rec_bytes + off);
@@ -172,7 +179,7 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __re
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             if (u0 + lane + 32 * q < nu) {
-              dst[u0 + lane + 32 * q] = v[q];
+              dst[dunit(u0 + lane + 32 * q)] = v[q];
               cdst[u0 + lane + 32 * q] = v[q];
             }
         }
@@ -527,8 +534,10 @@ const int kReg = register_kernels({(const void*)compact_kv_kernel, (const void*)
 }  // namespace
 
 bool attn_tc_supported(const LayerGeom& g) {
-  // chunk blocks (c rows, 8-row swizzle atoms) must tile 128 keys
-  return g.d == D && (g.rec_swz == 1 || g.rec_swz == 2) && g.c >= 8 && g.c <= BN && (BN % g.c) == 0;
+  // chunk blocks must tile the 128-key tiles (c | 128)
+  // (any c dividing 128: c % 8 != 0 re-swizzles the record rows in the compaction; V-only needs c % 8 == 0)
+  return g.d == D && (g.rec_swz == 1 || (g.rec_swz == 2 && g.c % 8 == 0)) && g.c >= 1 && g.c <= BN &&
+         (BN % g.c) == 0;
 }
 
 int attn_tc_nsplit(const LayerGeom& g, int k_cap, int include_suffix) {

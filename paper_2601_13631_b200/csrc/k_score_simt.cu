@@ -73,6 +73,40 @@ __global__ void __launch_bounds__(NT) score_simt_kernel(LayerGeom g, const T* __
 #pragma unroll
       for (int j = 0; j < 4; ++j) S[(ty * 4 + i) * (KB + 1) + tx * 4 + j] = acc[i][j];
     __syncthreads();
+    if (KB % g.c == 0) {
+      // chunks align to the 64-key sub-tiles (c | 64; kb is a multiple of c): every thread takes
+      // whole (row, chunk) items -- max, exponentials and sum of the chunk's c logits -- and the
+      // row threads fold the sub-tile's chunk values into the split's row partial
+      float* Lc = Kt;  // [KB / c][RB] chunk values of this sub-tile (K tile no longer needed)
+      const int cpt = KB / g.c;
+      for (int it = tid; it < RB * cpt; it += NT) {
+        const int rr = it % RB, cc = it / RB, kk0 = cc * g.c;
+        const int kend = min(g.c, key1 - kb - kk0);
+        float l2 = -INFINITY;
+        if (kend > 0 && row0 + rr < g.R) {
+          const float* srow = S + rr * (KB + 1) + kk0;
+          float m = srow[0];
+          for (int t = 1; t < kend; ++t) m = fmaxf(m, srow[t]);
+          m *= scale;
+          float sum = 0.f;
+          for (int t = 0; t < kend; ++t) sum += fast_exp2(fmaf(srow[t], scale, -m));
+          l2 = m + fast_log2(sum);
+          lam2[((size_t)kvh * g.m_loc + (kb + kk0) / g.c) * g.R + row0 + rr] = l2;
+        }
+        Lc[cc * RB + rr] = l2;
+      }
+      __syncthreads();
+      if (tid < RB && my_row < g.R) {
+        for (int cc = 0; cc < cpt; ++cc) {
+          const float l2 = Lc[cc * RB + tid];
+          if (l2 == -INFINITY) continue;
+          const float nm = fmaxf(pm, l2);
+          ps = ps * fast_exp2(pm - nm) + fast_exp2(l2 - nm);
+          pm = nm;
+        }
+      }
+      continue;
+    }
     if (tid < RB && my_row < g.R) {
       const int kend = min(KB, key1 - kb);
       for (int kk = 0; kk < kend; ++kk) {

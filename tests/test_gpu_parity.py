@@ -167,7 +167,8 @@ def test_score_kernels_agree_simt_vs_default():
     check_layer(ra["ids"], ra["out"], ra["A"], ra["qs"], ra["ks"], ra["vs"], *prefix[0], cfg, k)
 
 
-@pytest.mark.parametrize("c,ns,k", [(16, 130, 21), (8, 1, 5), (32, 40, 9), (64, 200, 3), (16, 256, 64)])
+@pytest.mark.parametrize("c,ns,k", [(16, 130, 21), (8, 1, 5), (32, 40, 9), (64, 200, 3), (16, 256, 64),
+                                    (4, 40, 37), (2, 17, 61), (1, 9, 100), (4, 130, 250)])
 def test_tensor_core_paths_vs_oracle_shapes(c, ns, k):
     """tcgen05 score + attention across chunk sizes, 1..2 suffix tiles, k not a multiple of 128/c."""
     from paper_2601_13631_b200 import CKV_FLAG_SIMT_ATTN
