@@ -30,8 +30,12 @@ constexpr int kColSplit = kEpiWarps / 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kKBytes = BN * D * 2;  // 65536
 constexpr uint32_t kQBytes = BM * D * 2;  // 32768
-constexpr int kQStages = 3;  // TMA latency of a Q tile (~2 us) spans more than one unit's MMAs
-constexpr size_t kSmem = 2 * kKBytes + kQStages * kQBytes + 1024 /*align*/ + 256 /*barriers*/;
+// Ring depths: the default (several row tiles per KV head) streams a new Q tile per unit through
+// 3 stages (TMA latency of a Q tile, ~2 us, spans more than one unit's MMAs) and keeps 2 K tiles;
+// with one row tile per KV head (G * n_s <= 128, e.g. the n_s = 8 HBM probe) Q is loaded once per
+// KV head and every unit needs a new 64 KB K tile, so the smem goes to a 3-deep K ring instead.
+template <int KS, int QS>
+constexpr size_t smem_bytes() { return KS * kKBytes + QS * kQBytes + 1024 /*align*/ + 256 /*barriers*/; }
 
 struct TcParams {
   LayerGeom g;
@@ -42,6 +46,8 @@ struct TcParams {
   int MT;       // row tiles per kv head
   int R_pad;
   int q_direct;  // 1: Q tiles straight from q [ns][Hq][128] by a 3-D map (n_s % 128 == 0), no pack
+  int perm;      // 1 (one row tile per KV head, R <= 128): packed row of rho = (rho % 4) * 32 + rho / 4, so
+                 // the valid rows spread over all four TMEM lane quadrants (= all four SM sub-partitions)
   int n_units;  // Hkv * NKT * MT
   float scale;  // log2(e) / sqrt(d)
   int epi_sleep;  // epilogue warps wait for their accumulator with a suspend-time hint
@@ -215,21 +221,21 @@ __device__ __forceinline__ void trace_ev(const TcParams& p, int e, int i) {
 #endif
 }
 
-template <int C, int NP>
+template <int C, int NP, int KS, int QS>
 __global__ void __launch_bounds__(kThreads, 1)
     score_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* kbuf0 = smem;
-  uint8_t* qbuf0 = smem + 2 * kKBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kKBytes + kQStages * kQBytes);
-  uint64_t* k_full = bars + 0;
-  uint64_t* k_empty = bars + 2;
-  uint64_t* acc_full = bars + 4;
-  uint64_t* acc_empty = bars + 6;
-  uint64_t* q_full = bars + 8;              // [kQStages]
-  uint64_t* q_empty = bars + 8 + kQStages;  // [kQStages]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8 + 2 * kQStages);
+  uint8_t* qbuf0 = smem + KS * kKBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + KS * kKBytes + QS * kQBytes);
+  uint64_t* k_full = bars + 0;             // [KS]
+  uint64_t* k_empty = bars + KS;           // [KS]
+  uint64_t* acc_full = bars + 2 * KS;      // [2]
+  uint64_t* acc_empty = bars + 2 * KS + 2; // [2]
+  uint64_t* q_full = bars + 2 * KS + 4;    // [QS]
+  uint64_t* q_empty = q_full + QS;         // [QS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + QS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef CKV_TUNING
@@ -246,13 +252,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int u1 = (int)((int64_t)(blockIdx.x + 1) * p.n_units / gridDim.x);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < KS; ++i) {
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&acc_full[i], 1);
       ptx::mbar_init(&acc_empty[i], kEpiWarps / 2);  // one epilogue group per buffer
     }
-    for (int i = 0; i < kQStages; ++i) {
+    for (int i = 0; i < QS; ++i) {
       ptx::mbar_init(&q_full[i], 1);
       ptx::mbar_init(&q_empty[i], 1);
     }
@@ -268,13 +276,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tmK);
       ptx::tma_prefetch_desc(&tmQ);
-      int kcount = 0, qcount = 0, cur = -1;
+      int kcount = 0, qcount = 0, cur = -1, qcur = -1;
       UnitIter it(u0, p.MT, p.NKT);
       for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT)) {
         const int pr = it.pr, mt = it.mt(p.MT), kvh = it.kvh, kt = it.kt;
         if (pr != cur) {
-          const int kb = kcount & 1;
-          ptx::mbar_wait_sleep(&k_empty[kb], ((kcount >> 1) & 1) ^ 1);
+          const int kb = kcount % KS;
+          ptx::mbar_wait_sleep(&k_empty[kb], ((kcount / KS) & 1) ^ 1);
           ptx::mbar_expect_tx(&k_full[kb], kKBytes);
           const int y = kvh * p.g.n_pad + kt * BN;
           uint8_t* dst = kbuf0 + kb * kKBytes;
@@ -283,8 +291,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           cur = pr;
           ++kcount;
         }
-        const int qs = qcount % kQStages;
-        ptx::mbar_wait_sleep(&q_empty[qs], ((qcount / kQStages) & 1) ^ 1);
+        const int qid = kvh * p.MT + mt;
+        if (qid == qcur) continue;  // same Q tile as the previous unit (one row tile per KV head)
+        qcur = qid;
+        const int qs = qcount % QS;
+        ptx::mbar_wait_sleep(&q_empty[qs], ((qcount / QS) & 1) ^ 1);
         if (qcount == 0) pdl_wait();  // Q is the previous kernel's output (the probe keys are not)
         ptx::mbar_expect_tx(&q_full[qs], kQBytes);
         uint8_t* dq = qbuf0 + qs * kQBytes;
@@ -303,18 +314,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
-      int kcount = 0, qcount = 0, acount = 0, cur = -1, kb = 0;
+      int kcount = 0, qcount = 0, acount = 0, cur = -1, kb = 0, qcur = -1, qs = 0;
       UnitIter it(u0, p.MT, p.NKT);
       for (int u = u0; u < u1; ++u, it.next(p.MT, p.NKT)) {
         const int pr = it.pr;
         if (pr != cur) {
-          kb = kcount & 1;
-          ptx::mbar_wait_sleep(&k_full[kb], (kcount >> 1) & 1);
+          kb = kcount % KS;
+          ptx::mbar_wait_sleep(&k_full[kb], (kcount / KS) & 1);
           ++kcount;
           cur = pr;
         }
-        const int qs = qcount % kQStages;
-        ptx::mbar_wait_sleep(&q_full[qs], (qcount / kQStages) & 1);
+        const int qid = it.kvh * p.MT + it.mt(p.MT);
+        if (qid != qcur) {  // a new Q tile (the producer loads one only when the tile changes)
+          qcur = qid;
+          qs = qcount % QS;
+          ptx::mbar_wait_sleep(&q_full[qs], (qcount / QS) & 1);
+          ++qcount;
+        }
         trace_ev(p, 0, acount);  // Q (and K) of the unit landed
         const int ab = acount & 1;
         ptx::mbar_wait_sleep(&acc_empty[ab], ((acount >> 1) & 1) ^ 1);
@@ -330,11 +346,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::mma_bf16(d_tmem, ptx::umma_desc_sw128(qa + off_q), ptx::umma_desc_sw128(ka + off_k), idesc,
                         k > 0 ? 1u : 0u);
         }
-        ptx::mma_commit(&q_empty[qs]);
+        // release the Q stage when the next unit uses another Q tile (or this is the CTA's last)
+        UnitIter nx = it;
+        nx.next(p.MT, p.NKT);
+        if (u + 1 == u1 || nx.kvh * p.MT + nx.mt(p.MT) != qid) ptx::mma_commit(&q_empty[qs]);
         ptx::mma_commit(&acc_full[ab]);
         const bool last_of_pair = (u + 1 == u1) || it.last_of_pair(p.MT);
         if (last_of_pair) ptx::mma_commit(&k_empty[kb]);
-        ++qcount;
         ++acount;
       }
     }
@@ -366,13 +384,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::mbar_wait(&acc_full[ab], (acount >> 1) & 1);
       ptx::tc_fence_after();
       if (lane == 0 && e < 8 && (e & 3) == 0) trace_ev(p, 2, acount);  // group's first warp: MMA done
-      if (mt * BM + quad * 32 >= p.g.R) {  // warp-uniform: this lane quadrant is all padding rows
+      if (p.perm ? quad >= p.g.R : mt * BM + quad * 32 >= p.g.R) {  // warp-uniform: quadrant all padding
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
         continue;
       }
-      const int rho = mt * BM + row_in_tile;
+      const int rho = p.perm ? lane * 4 + quad : mt * BM + row_in_tile;
       const bool row_ok = rho < p.g.R;
 #pragma unroll 1
       for (int pass = 0; pass < 2; ++pass) {
@@ -425,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // GQA row packing: qpack[kvh][rho][x] = q[r][kvh*G + g][x], rho = g*ns + r, zero rows past R.
-__global__ void pack_q_kernel(LayerGeom g, int R_pad, const __nv_bfloat16* __restrict__ q,
+__global__ void pack_q_kernel(LayerGeom g, int R_pad, int perm, const __nv_bfloat16* __restrict__ q,
                               __nv_bfloat16* __restrict__ qpack) {
   pdl_wait();
   pdl_trigger();
@@ -433,7 +451,8 @@ __global__ void pack_q_kernel(LayerGeom g, int R_pad, const __nv_bfloat16* __res
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int x8 = (int)(i % (D / 8));
     const int64_t row = i / (D / 8);
-    const int kvh = (int)(row / R_pad), rho = (int)(row % R_pad);
+    const int kvh = (int)(row / R_pad), slot = (int)(row % R_pad);
+    const int rho = perm ? (slot & 31) * 4 + (slot >> 5) : slot;  // inverse of slot = (rho % 4) * 32 + rho / 4
     uint4 val = make_uint4(0, 0, 0, 0);
     if (rho < g.R) {
       const int gq = rho / g.ns, r = rho % g.ns;
@@ -454,16 +473,23 @@ int num_sms() {
   return n;
 }
 
-template <int C, int NP>
-cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
+template <int C, int NP, int KS, int QS>
+cudaError_t launch_cpq(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
+  constexpr size_t kSmem = smem_bytes<KS, QS>();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<C, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    cudaError_t e = cudaFuncSetAttribute(score_tc_kernel<C, NP, KS, QS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (cudaError_t e_ = launch_kernel(score_tc_kernel<C, NP>, grid, kThreads, kSmem, st, tmK, tmQ, p)) return e_;
+  if (cudaError_t e_ = launch_kernel(score_tc_kernel<C, NP, KS, QS>, grid, kThreads, kSmem, st, tmK, tmQ, p)) return e_;
   return cudaGetLastError();
+}
+template <int C, int NP>
+cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcParams& p, int grid, cudaStream_t st) {
+  if (p.MT == 1) return launch_cpq<C, NP, 3, 1>(tmK, tmQ, p, grid, st);  // one row tile per KV head
+  return launch_cpq<C, NP, 2, 3>(tmK, tmQ, p, grid, st);
 }
 
 // pairs of every 8 (i.e. exponentials of every 16) evaluated by the FFMA2 polynomial instead of
@@ -496,7 +522,7 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
   return launch_cp<C, kPolyPairs>(tmK, tmQ, p, grid, st);
 }
 
-#define CKV_SC(C) (const void*)score_tc_kernel<C, kPolyPairs>
+#define CKV_SC(C) (const void*)score_tc_kernel<C, kPolyPairs, 2, 3>, (const void*)score_tc_kernel<C, kPolyPairs, 3, 1>
 const int kReg = register_kernels({CKV_SC(1), CKV_SC(2), CKV_SC(4), CKV_SC(8), CKV_SC(16), CKV_SC(32), CKV_SC(64),
                                    (const void*)pack_q_kernel});
 #undef CKV_SC
@@ -509,7 +535,7 @@ int score_tc_nsplit(const LayerGeom& g) {
   return kColSplit * ((g.n_loc + BN - 1) / BN);
 }
 
-int score_tc_packs_q(const LayerGeom& g) { return (g.ns % BM) != 0; }
+int score_tc_packs_q(const LayerGeom& g) { return (g.ns % BM) != 0 || g.R <= BM; }
 
 size_t score_tc_qpack_elems(int Hkv, int R_max) { return (size_t)Hkv * ((R_max + BM - 1) / BM) * BM * D; }
 
@@ -540,9 +566,10 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   }
 #endif
   auto* qpack = static_cast<__nv_bfloat16*>(qpack_ws);
-  p.q_direct = (g.ns % BM) == 0 ? 1 : 0;
+  p.perm = p.MT == 1 ? 1 : 0;
+  p.q_direct = ((g.ns % BM) == 0 && !p.perm) ? 1 : 0;
   if (!p.q_direct)
-    if (cudaError_t e_ = launch_kernel(pack_q_kernel, 256, 256, 0, st, g, p.R_pad, q, qpack)) return e_;
+    if (cudaError_t e_ = launch_kernel(pack_q_kernel, 256, 256, 0, st, g, p.R_pad, p.perm, q, qpack)) return e_;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap tmK, tmQ;

@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from synth import CONFIGS, make_request
 from tests.gpu_util import make_ctx, to_dev
-cfg = CONFIGS["c3_7b"].replace(num_layers=1)
+cfg = CONFIGS[os.environ.get("TRACE_CFG", "c3_7b")].replace(num_layers=1)
 ctx, _ = make_ctx(cfg)
 q, k_, v_ = (to_dev(x, torch.bfloat16) for x in make_request(cfg, 0, 0))
 for rep in range(3):
