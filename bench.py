@@ -145,6 +145,22 @@ def oracle_layer_seconds(cfg, k, layer=0, request=0):
     return time.perf_counter() - t
 
 
+def oracle_single_thread_layer_seconds(cfg, k):
+    """the oracle with one BLAS thread, timed on one KV head's share of layer 0
+    (the same arithmetic per KV head, the selection over that head's scores) x Hkv."""
+    import oracle as O
+    from synth import make_prefix, make_request
+    from threadpoolctl import threadpool_limits
+    kp, vp = make_prefix(cfg, 0)
+    qs, ks, vs = make_request(cfg, 0, 0)
+    G = cfg.group
+    with threadpool_limits(limits=1):
+        t = time.perf_counter()
+        O.reprefill_layer(qs[:, :G], ks[:, :1], vs[:, :1], kp[:, :1], vp[:, :1], cfg.chunk_size, k, G)
+        dt = time.perf_counter() - t
+    return dt * cfg.num_kv_heads
+
+
 def run_reference(args, rank, world):
     """--impl reference: the fp64 oracle on the host cores, each step one layer of the workload."""
     from synth import CONFIGS
@@ -525,8 +541,11 @@ def run_ckv(args, rank, world):
     cpu = None
     if world == 1 and not args.no_cpu:
         t = oracle_layer_seconds(cfg, k)
+        t1 = oracle_single_thread_layer_seconds(cfg, k)
         cpu = {"value": bpl / t / 1e9, "unit": "GB/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": f"1 layer (layer 0, request 0) of {CFG_NAME}, fp64 NumPy, {t:.2f} s"}
+               "sample": f"1 layer (layer 0, request 0) of {CFG_NAME}, fp64 NumPy, {t:.2f} s",
+               "single_thread": {"s_per_layer": t1, "value": bpl / t1 / 1e9,
+                                 "sample": "one KV head of layer 0 with one BLAS thread, x Hkv"}}
     gate = None
     gp = os.path.join(ROOT, "profiles", "r2_gate_rate_c3.json")
     if os.path.exists(gp):

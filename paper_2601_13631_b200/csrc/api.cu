@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ckv.h"
 #include "common.cuh"
 
@@ -88,6 +90,13 @@ struct ckv_ctx {
 };
 
 namespace {
+
+// NVTX range around each public entry point (an nsys / ncu timeline shows the library's host calls;
+// without an attached tool the header-only NVTX v3 calls are no-ops)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 ckv_status fail(ckv_ctx* ctx, ckv_status s, const char* fmt, ...) {
   if (ctx) {
@@ -489,6 +498,7 @@ int32_t ckv_budget_chunks(int64_t n, int32_t c, int32_t budget_bp) {
 }
 
 ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
+  NvtxRange nvtx_("ckv_create");
   if (!cfg || !out) return CKV_EINVAL;
   *out = nullptr;
   ckv_ctx* ctx = new (std::nothrow) ckv_ctx();
@@ -691,6 +701,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
 
 ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const void* v, int64_t n_tokens,
                             void* stream) {
+  NvtxRange nvtx_("ckv_store_prefix");
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
   if (!k || !v) return fail(ctx, CKV_EINVAL, "null k/v");
@@ -757,6 +768,7 @@ ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const vo
 ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const void* k_suf, const void* v_suf,
                                int32_t n_suffix, void* out, int32_t* selected_ids, float* chunk_scores,
                                void* stream) {
+  NvtxRange nvtx_("ckv_reprefill_layer");
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
   ckv_status s = check_layer_call(ctx, layer, n_suffix);
@@ -826,6 +838,7 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
 
 ckv_status ckv_shard_score(ckv_ctx* ctx, int32_t layer, const void* q, const void* k_suf, int32_t n_suffix,
                            float* lam_local, void* stream) {
+  NvtxRange nvtx_("ckv_shard_score");
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
   ckv_status s = check_layer_call(ctx, layer, n_suffix);
@@ -868,6 +881,7 @@ ckv_status ckv_shard_select(ckv_ctx* ctx, int32_t layer, const void* q, const vo
 ckv_status ckv_shard_attend(ckv_ctx* ctx, int32_t layer, const uint64_t* cand_all, const void* q, const void* k_suf,
                             const void* v_suf, int32_t n_suffix, float* o_part, float* lse_part,
                             int32_t* selected_ids, void* stream) {
+  NvtxRange nvtx_("ckv_shard_attend");
   if (!ctx) return CKV_EINVAL;
   ctx->err.clear();
   ckv_status s = check_layer_call(ctx, layer, n_suffix);

@@ -67,10 +67,44 @@ def logical(a):
                 assert torch.equal(res[g][0], res[0][0]), ("out differs across ranks", g)
             diags.append(check_layer(res[0][1].cpu().numpy(), res[0][0].float().cpu().numpy(), None, qs, ks, vs, kp,
                                      vp, cfg, k, norm=a.norm))
+    graph_ok = None
+    if a.graph:
+        # every rank's whole request captured in one CUDA graph per rank (the exchange is kernel
+        # nodes only); the graphs replay concurrently on the ranks' streams and must reproduce
+        # the eager outputs bit for bit
+        req = a.requests - 1
+        outs = [[torch.empty(cfg.suffix_len, cfg.num_q_heads, cfg.head_dim, dtype=ctxs[0].torch_dtype,
+                             device="cuda") for _ in range(cfg.num_layers)] for _ in range(W)]
+        idsb = [[torch.empty(k, dtype=torch.int32, device="cuda") for _ in range(cfg.num_layers)] for _ in range(W)]
+        inp = [[to_dev(x, ctxs[0].torch_dtype) for x in make_request(cfg, l, req)] for l in range(cfg.num_layers)]
+        torch.cuda.synchronize()
+        graphs = []
+        for g, c in enumerate(ctxs):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=streams[g]):
+                for l in range(cfg.num_layers):
+                    c.reprefill_layer(l, *inp[l], out=outs[g][l], ids=idsb[g][l], stream=streams[g])
+            graphs.append(gr)
+        torch.cuda.synchronize()
+        for rep in range(2):
+            for g in range(W):
+                with torch.cuda.stream(streams[g]):
+                    graphs[g].replay()
+            torch.cuda.synchronize()
+        graph_ok = True
+        for l in range(cfg.num_layers):
+            for g in range(W):
+                assert torch.equal(outs[g][l], outs[0][l]) and torch.equal(idsb[g][l], idsb[0][l])
+            kp, vp = prefix[l]
+            qs, ks, vs = make_request(cfg, l, req)
+            d = check_layer(idsb[0][l].cpu().numpy(), outs[0][l].float().cpu().numpy(), None, qs, ks, vs, kp, vp,
+                            cfg, k, norm=a.norm)
+            diags.append(d)
     for c in ctxs:
         c.close()
     return {"mode": "logical", "W": W, "cyclic": a.cyclic, "vonly": a.vonly, "dtype": a.dtype, "layers": len(diags),
-            "strict": sum(d["strict"] for d in diags), "max_out_rel": max(d["out_rel"] for d in diags)}
+            "strict": sum(d["strict"] for d in diags), "max_out_rel": max(d["out_rel"] for d in diags),
+            "graph": graph_ok}
 
 
 def multiprocess(a):
@@ -125,6 +159,7 @@ def main():
     ap.add_argument("--ns", type=int, default=40)
     ap.add_argument("--layers", type=int, default=2)
     ap.add_argument("--requests", type=int, default=2)
+    ap.add_argument("--graph", action="store_true", help="logical mode: also replay per-rank CUDA graphs")
     a = ap.parse_args()
     r = logical(a) if a.mode == "logical" else multiprocess(a)
     if r.get("rank", 0) == 0:

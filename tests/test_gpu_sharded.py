@@ -50,6 +50,13 @@ def test_fused_exchange_logical_ranks(W, extra):
     assert r["layers"] > 0 and r["max_out_rel"] < (1e-4 if "fp32" in extra else 2e-2), r
 
 
+def test_fused_exchange_in_cuda_graphs():
+    # the whole sharded request of every rank captured in one CUDA graph per rank, replayed
+    # concurrently: the exchange's put / wait kernels are ordinary graph nodes
+    r = _run(["-m", "tests.sharded_worker", "logical", "--W", "3", "--graph", "--cyclic"])
+    assert r["graph"] is True and r["max_out_rel"] < 2e-2, r
+
+
 @pytest.mark.parametrize("impl,extra", [("fused", []), ("fused", ["--cyclic", "--prefetch"]), ("collective", []),
                                         ("collective", ["--cyclic"])])
 def test_two_processes_one_gpu(impl, extra):
