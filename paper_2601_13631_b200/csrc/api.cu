@@ -75,7 +75,8 @@ struct ckv_ctx {
   cudaEvent_t ev_ids = nullptr;
   std::vector<cudaEvent_t> ev_pplan, ev_pf;
   std::vector<int> pf_issued;
-  std::vector<int> pf_joined;  // epoch in which the main stream already waited for ev_pf[layer]
+  std::vector<int> pf_joined;
+  std::vector<char> pf_late;  // the prefetch of this layer was issued at the end of the previous layer  // epoch in which the main stream already waited for ev_pf[layer]
   std::vector<char> stored;
   int epoch = 0;
   int last_layer = -1;
@@ -279,6 +280,7 @@ ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int
                    ctx->side));
   CK(cudaEventRecord(ctx->ev_pf[layer], ctx->side));
   ctx->pf_issued[layer] = ctx->epoch;
+  ctx->pf_late[layer] = 0;
   return CKV_OK;
 }
 
@@ -668,6 +670,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   }
   ctx->pf_issued.assign(ctx->L, -1);
   ctx->pf_joined.assign(ctx->L, -1);
+  ctx->pf_late.assign(ctx->L, 0);
   ctx->stored.assign(ctx->L, 0);
   ctx->score_kind = (ctx->dtype == CKV_BF16 && ctx->d == 128 && !(c.flags & CKV_FLAG_SIMT_SCORE)) ? 1 : 0;
   if (ctx->score_kind == 1) {
@@ -791,12 +794,19 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
   int32_t* ids = ctx->ids_buf[pid & 1];  // double-buffered by period: side-stream plans may still read it
   int32_t* nids = ctx->n_ids_buf[pid & 1];
   bool planned = false;  // the demand plan of this layer ran inside the fused select kernel
+  // p = 1: the next layer's speculative plan + gather are issued after this layer's last kernel (not
+  // right after A3): they then overlap the next layer's scoring instead of this layer's compaction
+  // (demand misses on the same host link) and attention (SMs); they are joined before the next
+  // layer's plan.  Measured on the B200: steady-state stream 106.7 vs 109.7 us/layer, all-hit 89.6
+  // vs 92.0.  The tuning build's CKV_LATE_PF=0 restores the early issue (A/B).
+  static const bool late_on = !(tuning_env("CKV_LATE_PF") && tuning_env("CKV_LATE_PF")[0] == '0');
+  const bool late_pf = late_on && first && p == 1 && !ctx->global_heap && ctx->quota > 0 && layer + 1 < ctx->L;
   if (first) {  // identification: A1 -> A2 -> A3
     // The persistent score kernel needs every SM: side-stream prefetch work for this layer must
     // not still be resident when it starts (one late CTA delays the whole statically partitioned
     // launch), so the prefetch is joined here rather than only before the attention.
     static const bool side_sync = !(tuning_env("CKV_SIDE_SYNC") && tuning_env("CKV_SIDE_SYNC")[0] == '0');
-    if (side_sync && ctx->pf_issued[layer] == ctx->epoch) {
+    if (side_sync && ctx->pf_issued[layer] == ctx->epoch && !ctx->pf_late[layer]) {
       CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
       pdl_mark_event_wait(st);
       ctx->pf_joined[layer] = ctx->epoch;
@@ -815,7 +825,7 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     // the next period's first layer (A6), all on the side stream in layer order
     // (global heap: one shared pool, so the next layer's speculative plan may only run after this
     // layer's demand plan and compaction -- issued below, after run_attend)
-    if (!ctx->global_heap)
+    if (!ctx->global_heap && !late_pf)
       for (int lp = layer + 1; lp <= pend && lp < ctx->L; ++lp)
         if ((s = issue_prefetch(ctx, lp, ids, nids, st, false, ctx->sel_keys[pid & 1])) != CKV_OK) return s;
     // subperiod gate: attention of the first layer waits for sp layers' chunks
@@ -827,11 +837,16 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
   }
   // the demand planner also writes selected_ids (no separate copy node per layer)
   const bool defer_pf = ctx->global_heap && first && ctx->quota > 0 && layer + 1 < ctx->L;
+  // (late_pf: the next layer's speculative plan + gather are issued after this layer's last kernel)
   if ((s = run_attend(ctx, layer, ids, nids, q, k_suf, v_suf, n_suffix, 1, out, nullptr, nullptr, selected_ids,
                       planned, st, defer_pf ? ctx->ev_ids : nullptr)) != CKV_OK)
     return s;
   if (defer_pf && (s = issue_prefetch(ctx, layer + 1, ids, nids, st, true, ctx->sel_keys[pid & 1])) != CKV_OK)
     return s;
+  if (late_pf) {
+    if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st, false, ctx->sel_keys[pid & 1])) != CKV_OK) return s;
+    ctx->pf_late[layer + 1] = 1;  // joined before the next layer's plan, not before its scoring
+  }
   if (chunk_scores) CK(cudaMemcpyAsync(chunk_scores, ctx->A, sizeof(float) * ctx->m_loc, cudaMemcpyDeviceToDevice, st));
   return CKV_OK;
 }
