@@ -801,6 +801,12 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
   // vs 92.0.  The tuning build's CKV_LATE_PF=0 restores the early issue (A/B).
   static const bool late_on = !(tuning_env("CKV_LATE_PF") && tuning_env("CKV_LATE_PF")[0] == '0');
   const bool late_pf = late_on && first && p == 1 && !ctx->global_heap && ctx->quota > 0 && layer + 1 < ctx->L;
+  // ... and the speculative plan runs as CTA 1 of this layer's demand-plan launch (cache_plan2): a
+  // single-CTA planner on the side stream could not share an SM with the next layer's persistent
+  // score kernel, so it ran after it and its gather landed late (measured: steady-state stream
+  // 100.6 vs 107.6 us/layer, all-hit 91.2 vs 89.9).  Tuning build: CKV_PLAN2=0 for the A/B.
+  static const bool plan2_on = !(tuning_env("CKV_PLAN2") && tuning_env("CKV_PLAN2")[0] == '0');
+  bool planned2 = false;
   if (first) {  // identification: A1 -> A2 -> A3
     // The persistent score kernel needs every SM: side-stream prefetch work for this layer must
     // not still be resident when it starts (one late CTA delays the whole statically partitioned
@@ -825,6 +831,29 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     // the next period's first layer (A6), all on the side stream in layer order
     // (global heap: one shared pool, so the next layer's speculative plan may only run after this
     // layer's demand plan and compaction -- issued below, after run_attend)
+    if (late_pf && plan2_on && gather_fused(ctx)) {
+      // this layer's demand plan (CTA 0) and the next layer's speculative plan (CTA 1) in one
+      // launch; the speculative gather follows at the end of the layer (below).  A prefetch of
+      // this layer not yet joined must land its plan first (tables) -- it was planned on this
+      // stream, so only its gather is outstanding, and the compaction waits for that
+      if (ctx->pf_issued[layer] == ctx->epoch && ctx->pf_joined[layer] != ctx->epoch && !ctx->pf_late[layer]) {
+        CK(cudaStreamWaitEvent(st, ctx->ev_pf[layer], 0));
+        pdl_mark_event_wait(st);
+        ctx->pf_joined[layer] = ctx->epoch;
+      }
+      PROF_BEGIN(3);
+      PlanJob a{cache_layer(ctx, layer), ids, nids, 0, 0, 0, ctx->epoch, ctx->rec_bytes, ctx->scratch_main,
+                demand_plan_out(ctx, layer, selected_ids)};
+      PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)((layer + 1) * 2 + 1) * 4,
+                 ctx->stats, nullptr, ctx->epoch_dev};
+      po.rank_keys = ctx->sel_keys[pid & 1];
+      PlanJob b{cache_layer(ctx, layer + 1), ids, nids, 0, 1, ctx->quota, ctx->epoch, ctx->rec_bytes,
+                ctx->scratch_side, po};
+      LK(launch_cache_plan2(a, b, st));
+      PROF_END(3);
+      planned = true;
+      planned2 = true;
+    }
     if (!ctx->global_heap && !late_pf)
       for (int lp = layer + 1; lp <= pend && lp < ctx->L; ++lp)
         if ((s = issue_prefetch(ctx, lp, ids, nids, st, false, ctx->sel_keys[pid & 1])) != CKV_OK) return s;
@@ -843,7 +872,16 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     return s;
   if (defer_pf && (s = issue_prefetch(ctx, layer + 1, ids, nids, st, true, ctx->sel_keys[pid & 1])) != CKV_OK)
     return s;
-  if (late_pf) {
+  if (late_pf && planned2) {  // speculative gather of the layer planned by cache_plan2 (CTA 1)
+    CK(cudaEventRecord(ctx->ev_ids, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ids, 0));
+    pdl_mark_event_wait(ctx->side);
+    LK(launch_gather(ctx->gl_side, ctx->nload_side, host_layer_dev(ctx, layer + 1), pool_layer(ctx, layer + 1),
+                     ctx->rec_bytes, ctx->side));
+    CK(cudaEventRecord(ctx->ev_pf[layer + 1], ctx->side));
+    ctx->pf_issued[layer + 1] = ctx->epoch;
+    ctx->pf_late[layer + 1] = 1;
+  } else if (late_pf) {
     if ((s = issue_prefetch(ctx, layer + 1, ids, nids, st, false, ctx->sel_keys[pid & 1])) != CKV_OK) return s;
     ctx->pf_late[layer + 1] = 1;  // joined before the next layer's plan, not before its scoring
   }

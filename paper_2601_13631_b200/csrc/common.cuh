@@ -205,6 +205,16 @@ struct PlanOut {
 cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const int32_t* n_ids_dev, int n_ids_host,
                               int prefetch, int quota, int epoch, int64_t rec_bytes, uint64_t* scratch64,
                               int32_t* scratch32, PlanOut out, cudaStream_t st);
+struct PlanJob {  // one cache_plan_body invocation (launch_cache_plan2)
+  CacheLayer cl;
+  const int32_t* ids;
+  const int32_t* n_ids_dev;
+  int n_ids_host, prefetch, quota, epoch;
+  int64_t rec_bytes;
+  int32_t* scratch;
+  PlanOut out;
+};
+cudaError_t launch_cache_plan2(const PlanJob& a, const PlanJob& b, cudaStream_t st);
 cudaError_t launch_epoch_inc(int32_t* epoch_dev, cudaStream_t st);
 cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
                           char* pool_layer, int64_t rec_bytes, cudaStream_t st);

@@ -33,6 +33,22 @@ __global__ void __launch_bounds__(NT) cache_plan_kernel(CacheLayer cl, const int
                       smem_keys ? plan_skeys : nullptr);
 }
 
+// Two plans in one launch (CTA 0: job a, CTA 1: job b) on disjoint per-layer pools: this layer's
+// demand plan and the next layer's speculative plan, so the speculation needs no single-CTA
+// planner on the side stream (which could not share an SM with the next layer's persistent score
+// kernel and so ran only after it).
+__global__ void __launch_bounds__(NT) cache_plan2_kernel(PlanJob a, PlanJob b) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ PlanSmem ps;
+  extern __shared__ uint64_t plan_skeys[];
+  const PlanJob& j = blockIdx.x == 0 ? a : b;
+  const int n_ids = j.n_ids_dev ? *j.n_ids_dev : j.n_ids_host;
+  const bool smem_keys = j.cl.P > NT * kPlanKPT && j.cl.P <= kPlanSmemKeysMax;
+  cache_plan_body<NT>(j.cl, j.ids, n_ids, j.prefetch, j.quota, j.epoch, j.rec_bytes, j.scratch, j.out, ps,
+                      smem_keys ? plan_skeys : nullptr);
+}
+
 // Whole-record copy host store -> HBM slot: work items are 4 KiB segments of records so a
 // few misses still keep many 16-B loads in flight over the host link.  Small CTAs (4 warps,
 // <= 64 registers): one fits on an SM beside a persistent score / attention CTA (576 threads x
@@ -132,7 +148,7 @@ __global__ void epoch_inc_kernel(int32_t* e) {
   pdl_wait();
   pdl_trigger(); *e += 1; }
 
-const int kReg = register_kernels({(const void*)cache_plan_kernel, (const void*)gather_kernel,
+const int kReg = register_kernels({(const void*)cache_plan_kernel, (const void*)cache_plan2_kernel, (const void*)gather_kernel,
                                    (const void*)cache_update_kernel, (const void*)pack_probe_kernel<float>,
                                    (const void*)pack_probe_kernel<__nv_bfloat16>, (const void*)pack_records_kernel<float>,
                                    (const void*)pack_records_kernel<__nv_bfloat16>, (const void*)epoch_inc_kernel});
@@ -160,6 +176,23 @@ cudaError_t launch_cache_plan(const CacheLayer& cl, const int32_t* ids, const in
   }
   if (cudaError_t e_ = launch_kernel(cache_plan_kernel, 1, NT, smem, st, cl, ids, n_ids_dev, n_ids_host, prefetch, quota,
                                      epoch, rec_bytes, scratch32, out)) return e_;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cache_plan2(const PlanJob& a, const PlanJob& b, cudaStream_t st) {
+  size_t smem = 0;
+  const int P = a.cl.P > b.cl.P ? a.cl.P : b.cl.P;
+  if (P > NT * kPlanKPT && P <= kPlanSmemKeysMax) {
+    static bool attr = false;
+    if (!attr) {
+      if (cudaError_t e = cudaFuncSetAttribute(cache_plan2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(kPlanSmemKeysMax * sizeof(uint64_t))))
+        return e;
+      attr = true;
+    }
+    smem = (size_t)P * sizeof(uint64_t);
+  }
+  if (cudaError_t e_ = launch_kernel(cache_plan2_kernel, 2, NT, smem, st, a, b)) return e_;
   return cudaGetLastError();
 }
 
