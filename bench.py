@@ -331,17 +331,25 @@ def run_ckv(args, rank, world):
     torch.cuda.synchronize()
     ids_cpu = [t.cpu().numpy() for t in ids]  # request 0's ids per layer
     cov = [len(set(ids_cpu[l].tolist()) & set(ids_cpu[l - 1].tolist())) / k for l in range(1, L)]
-    if args.quick:  # tuning runs: the warm graph-replayed step only
+    quick = {"us_per_layer": ms_step * 1e3 / L, "value": value, "all_hit_us_per_layer": ms_hit * 1e3 / L,
+             "eager_us_per_layer": ms_eager * 1e3 / L, "clocks": clk.summary(),
+             "hit_rate": stats["total_hits"] / max(stats["total_hits"] + stats["total_misses"], 1)}
+    if args.quick and not args.quick_e2e:  # tuning runs: the warm graph-replayed step only
         if rank == 0:
-            print(json.dumps({"us_per_layer": ms_step * 1e3 / L, "value": value, "all_hit_us_per_layer":
-                              ms_hit * 1e3 / L, "eager_us_per_layer": ms_eager * 1e3 / L, "clocks": clk.summary(),
-                              "hit_rate": stats["total_hits"] / max(stats["total_hits"] + stats["total_misses"], 1)}))
+            print(json.dumps(quick))
         return
 
-    # stage profile pass (eager; CUDA events on the launching stream, inside the library)
+    # stage profile pass (eager; CUDA events on the launching stream, inside the library): on the
+    # timed stream (the kernels as the headline runs them) and on the all-hit request (A1 alone,
+    # no speculative gather beside it)
     ctx.profile(True)
     ms_prof = timed(lambda i: run_request(seq[off2 + i]), args.steps)
     prof = ctx.profile_read()
+    for _ in range(2):
+        run_request(0)
+    ctx.profile_read()
+    timed(lambda i: run_request(0), args.steps)
+    prof_hit = ctx.profile_read()
     ctx.profile(False)
 
     # end-to-end through the public API with host buffers: H2D of the step's inputs from
@@ -356,16 +364,28 @@ def run_ckv(args, rank, world):
     ev_out = [torch.cuda.Event() for _ in range(L)]
     dev_in = [[torch.empty_like(t) for t in lay] for lay in reqs[0]]  # the step's device input buffers
 
+    ev_go = [torch.cuda.Event() for _ in range(L)]
+    AHEAD = 2  # layer l's inputs go up while layer l - AHEAD runs: the copies share the host link
+    # with the speculative chunk gathers evenly instead of as one burst at the start of the step
+
     def e2e_body(r):
         main = torch.cuda.current_stream()
         h2d_s.wait_stream(main)
         d2h_s.wait_stream(main)
-        with torch.cuda.stream(h2d_s):
-            for l in range(L):
+
+        def copy_in(l):  # layer l's inputs on the H2D stream (enqueued in stream order)
+            with torch.cuda.stream(h2d_s):
                 for dst, src in zip(dev_in[l], reqs_host[r][l]):
                     dst.copy_(src, non_blocking=True)
                 ev_in[l].record(h2d_s)
+
+        for l in range(min(AHEAD, L)):
+            copy_in(l)
         for l in range(L):
+            if l + AHEAD < L:  # layer l + AHEAD's inputs go up while layer l runs
+                ev_go[l].record(main)
+                h2d_s.wait_event(ev_go[l])
+                copy_in(l + AHEAD)
             main.wait_event(ev_in[l])
             layer_call(l, *dev_in[l])
             ev_out[l].record(main)
@@ -400,6 +420,11 @@ def run_ckv(args, rank, world):
     for i in range(2):
         e2e_step(seq[off2 + i])
     ms_e2e = timed(lambda i: e2e_step(seq[off3 - args.steps + i]), args.steps) / args.steps
+    if args.quick:
+        if rank == 0:
+            quick["e2e_us_per_layer"] = ms_e2e * 1e3 / L
+            print(json.dumps(quick))
+        return
 
     # cold HBM cache: every step starts from an empty chunk cache (all selected chunks cross the
     # host link; speculative prefetch still overlaps the next layer's loads)
@@ -528,6 +553,7 @@ def run_ckv(args, rank, world):
     peaks, peak_src = load_peaks()
     score_ms, score_n = prof["score"]
     score_avg = score_ms / max(score_n, 1)
+    score_avg_alone = prof_hit["score"][0] / max(prof_hit["score"][1], 1)
     flops = 2.0 * cfg.head_dim * cfg.num_q_heads * cfg.suffix_len * (cfg.prefix_len / world)
     achieved = flops / (score_avg * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
@@ -587,6 +613,10 @@ def run_ckv(args, rank, world):
                      "peak_source": "derived: 16 ex2/clk/SM x 148 SMs x sampled SM clock (DESIGN.md §6)",
                      "score_kernel_kind": ["simt", "tcgen05"][ctx.score_kernel_kind], "avg_launch_ms": score_avg,
                      "algorithmic": mufu["algorithmic"], "tensor": tensor,
+                     # the same kernel without the speculative gather of the stream running beside it
+                     "alone": {"avg_launch_ms": score_avg_alone,
+                               "frac": mufu_roofline(cfg, world, score_avg_alone, clk.summary())["frac"],
+                               "how": "all-hit request repeated (no prefetch traffic), same events"},
                      "hbm_achieved_gbs": (cfg.prefix_len / world) * cfg.num_kv_heads * cfg.head_dim * 2
                      / (score_avg * 1e-3) / 1e9},
         "stage_ms_per_step": step_stage_ms, "profiled_ms_per_step": ms_prof / args.steps,
@@ -657,12 +687,14 @@ def main():
     ap.add_argument("--cyclic", action="store_true", help="N > 1: cyclic chunk sharding (j mod N) instead of "
                     "contiguous ranges (balanced kept chunks, SURVEY §8(f) NEXT-3)")
     ap.add_argument("--quick", action="store_true", help="tuning: print only the warm graph-step time")
+    ap.add_argument("--quick-e2e", action="store_true", help="tuning: --quick plus the end-to-end step")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--exchange", default="fused", choices=["fused", "collective"],
                     help="N > 1: fused device-side exchange inside libckv (default) or host-issued "
                          "torch.distributed collectives (ShardedReprefill, the NCCL baseline)")
     ap.add_argument("--local-gpu", type=int, default=None, help="pin every rank to this GPU (functional runs)")
     args = ap.parse_args()
+    args.quick = args.quick or args.quick_e2e
     args.warmup = max(args.warmup, 3) if args.impl == "ckv" else args.warmup
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         sys.exit(relaunch(args))

@@ -34,6 +34,7 @@ struct ckv_ctx {
   int64_t t0 = 0;
   int n_loc = 0, n_pad = 0;
   int k = 0, P = 0, quota = 0, max_ns = 0, period = 1, subperiod = 1;
+  int spec_gate = -1;  // p = 1 speculation is skipped when the previous layer missed <= spec_gate chunks
   int64_t rec_elems = 0, rec_bytes = 0;
   int nsplit_score_max = 1, nsplit_attn_max = 1;
   int score_kind = 0;  // 0 SIMT, 1 tcgen05
@@ -561,6 +562,12 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   if (ctx->k < 1 || ctx->k > ctx->m) return bad("budget: k must be in [1, m]");
   ctx->quota = c.prefetch_chunks < 0 ? 0 : (c.prefetch_chunks > ctx->k ? ctx->k : c.prefetch_chunks);
   ctx->P = c.cache_slots > 0 ? c.cache_slots : 2 * ctx->k + ctx->quota;
+  // adaptive p = 1 speculation (plan.cuh): skipped while the previous layer missed <= k/8 chunks.
+  // Measured on the B200, C3 steady-state stream at equal HBM (510 slots): no gate 100.6 us/layer
+  // (e2e 128), gate k/16 96.3 (102.5), k/8 93.9 (102.6), speculation off 91.8 (97.6); cold cache:
+  // the speculation stays on (misses ~ k)
+  ctx->spec_gate = ctx->k / 8;
+  if (const char* sg = tuning_env("CKV_SPEC_GATE")) ctx->spec_gate = atoi(sg);  // tuning build: -1 = off
   if (ctx->P < ctx->k + ctx->quota) return bad("cache_slots < k + prefetch_chunks");
   ctx->global_heap = (c.flags & CKV_FLAG_GLOBAL_HEAP) != 0;
   // one shared pool: the next layer's speculative plan is issued only after this layer's demand plan
@@ -847,6 +854,10 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
       PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)((layer + 1) * 2 + 1) * 4,
                  ctx->stats, nullptr, ctx->epoch_dev};
       po.rank_keys = ctx->sel_keys[pid & 1];
+      if (layer > 0) {
+        po.gate_misses = ctx->counts + (size_t)((layer - 1) * 2) * 4 + 1;
+        po.gate_max = ctx->spec_gate;
+      }
       PlanJob b{cache_layer(ctx, layer + 1), ids, nids, 0, 1, ctx->quota, ctx->epoch, ctx->rec_bytes,
                 ctx->scratch_side, po};
       LK(launch_cache_plan2(a, b, st));

@@ -198,6 +198,8 @@ struct PlanOut {
   int32_t* ids_out = nullptr;  // if set: copy of the planned ids (the caller's selected_ids)
   int mark_miss = 0;  // kept_slots of a miss = -(slot + 2): the consumer (compact_kv) loads it from the
                       // host store itself and fills the slot (no separate gather launch)
+  const int32_t* gate_misses = nullptr;  // prefetch plans: demand misses of the previous layer ...
+  int gate_max = -1;                     // ... at or below which nothing is speculated (adaptive)
   const uint64_t* rank_keys = nullptr;  // prefetch plans: per position of ids, the (score bits << 32 | ~id)
                                         // key of the identifying layer; over quota, the highest-scored
                                         // misses are loaded (else the first in chunk order)

@@ -86,6 +86,11 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
     }
     n_miss += tot;
   }
+  // adaptive speculation: when the previous layer's demand plan missed (almost) nothing, the HBM
+  // cache already serves this request and a speculative load would only take link bytes and
+  // slots (in a warm multi-request stream only ~3% of them were used); speculate again as soon as
+  // the demand misses grow (cold cache, a new topic)
+  if (prefetch && out.gate_misses && *out.gate_misses <= out.gate_max) n_miss = 0;
   if (prefetch && n_miss > quota) {
     if (out.rank_keys) {
       // speculation is a bet that layer l+1 reuses layer l's chunks: spend the
