@@ -520,7 +520,14 @@ def run_ckv(args, rank, world):
         ctx.reset_stats()
         ms_p = timed(lambda i: pgraphs[seq[off2 + i]].replay(), args.steps) / args.steps
         pst = ctx.get_stats()
+        pcold = []
+        for _ in range(3):  # empty cache: every Period's chunks cross the host link
+            ctx.reset_cache()
+            torch.cuda.synchronize()
+            pcold.append(timed(lambda _: pgraphs[0].replay(), 1))
         period_line = {"period": 8, "subperiod": 4, "ms_per_step": ms_p, "us_per_layer": ms_p * 1e3 / L,
+                       "cold_us_per_layer": sum(pcold) / len(pcold) * 1e3 / L,
+                       "exposed_gather_us_per_layer": sum(pcold) / len(pcold) * 1e3 / L - ms_p * 1e3 / L,
                        "value": bpl * L / (ms_p * 1e-3) / 1e9, "unit": "GB/s",
                        "hit_rate": pst["total_hits"] / max(pst["total_hits"] + pst["total_misses"], 1),
                        "link_bytes_per_layer": (pst["total_link_bytes_delta"] + pst["total_link_bytes_spec"])
@@ -541,6 +548,39 @@ def run_ckv(args, rank, world):
         link_ms.append(e0.elapsed_time(e1))
     link_peak = (256 << 20) / (min(link_ms) * 1e-3) / 1e9
     del hbuf, dbuf
+    # the A5 gather engine alone: one layer's k random chunks demand-loaded into an empty cache
+    # (ckv_load_chunks) vs a pinned cudaMemcpy of the same bytes (>= 80% of the link)
+    gprobe = None
+    if world == 1:
+        rec = 2 * cfg.num_kv_heads * cfg.chunk_size * cfg.head_dim * 2
+        gids = torch.from_numpy(np.sort(np.random.default_rng(7).choice(cfg.num_chunks, k, replace=False))
+                                .astype(np.int32)).to(dev)
+        gt = []
+        for _ in range(5):
+            ctx.reset_cache()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ctx.load_chunks(0, gids)
+            e1.record()
+            torch.cuda.synchronize()
+            gt.append(e0.elapsed_time(e1))
+        hb = torch.empty(k * rec, dtype=torch.uint8).pin_memory()
+        db = torch.empty(k * rec, dtype=torch.uint8, device=dev)
+        mt = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            db.copy_(hb, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            mt.append(e0.elapsed_time(e1))
+        gb = k * rec / (min(gt) * 1e-3) / 1e9
+        mb = k * rec / (min(mt) * 1e-3) / 1e9
+        gprobe = {"chunks": k, "bytes": k * rec, "gather_gbs": gb, "memcpy_same_bytes_gbs": mb,
+                  "frac_of_memcpy": gb / mb, "frac_of_link_peak": gb / link_peak}
+        del hb, db
+        ctx.reset_cache()
     h2d = sum(t.numel() * t.element_size() for lay in reqs_host[0] for t in lay)
     d2h = L * (outs[0].numel() * outs[0].element_size() + k * 4)
 
@@ -630,6 +670,7 @@ def run_ckv(args, rank, world):
         "selection": {"coverage_prev_mean": float(np.mean(cov)), "coverage_prev_min": float(np.min(cov)),
                       "gap_gate": gate},
         "paper_period": period_line,
+        "gather_probe": gprobe,
         "cold_cache": {"ms_per_step": sum(cold_ms) / len(cold_ms), "us_per_layer": sum(cold_ms) / len(cold_ms) * 1e3 / L,
                        "hit_rate": hit_rate(cold_stats),
                        "link_bytes_per_layer": (cold_stats["total_link_bytes_delta"] + cold_stats["total_link_bytes_spec"])
