@@ -5,7 +5,7 @@
 
 Workload (config.workload): Qwen2.5-7B shape, 28 layers, 28 Q / 4 KV heads, d = 128,
 32K-token prefix, chunk 16, 128-token suffix, 10% budget (k = 204), bf16, inter-layer
-speculative prefetch on (quota k), HBM chunk cache of k + quota + k/2 slots per layer
+speculative prefetch on (quota k/4, adaptive), HBM chunk cache of k + k + k/2 slots per layer
 (~25% of the 2048 chunks of a layer).  Requests: a steady-state stream over 16 distinct
 requests sharing the prefix (Zipf(1) popularity, seed 42; 16 untimed draws warm the cache),
 so selected chunks that are not resident cross the host link inside the timed region
@@ -721,7 +721,7 @@ def main():
     ap.add_argument("--impl", default="ckv", choices=["ckv", "reference"])
     ap.add_argument("--no-prefetch", dest="prefetch", action="store_false")
     ap.add_argument("--cache-slots", type=int, default=0, help="override the HBM cache slots per layer (studies)")
-    ap.add_argument("--quota-frac", type=float, default=1.0,
+    ap.add_argument("--quota-frac", type=float, default=0.25,
                     help="speculative prefetch quota per layer as a fraction of k (the cache size stays k + k + k/2)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false")

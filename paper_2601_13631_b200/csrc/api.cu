@@ -265,8 +265,9 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
 
 // A6: speculative plan + gather of layer `layer` for the given ids, on the side stream.
 // `recorded`: ev_ids was already recorded on st (global heap: after the compaction of the current layer).
+// quota: chunks this plan may load (exact intra-period loads pass k; speculation the ctx's quota)
 ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t* n_ids_dev, cudaStream_t st,
-                          bool recorded = false, const uint64_t* rank_keys = nullptr) {
+                          bool recorded = false, const uint64_t* rank_keys = nullptr, int quota = -1) {
   if (ctx->quota <= 0 || layer >= ctx->L) return CKV_OK;
   if (!recorded) CK(cudaEventRecord(ctx->ev_ids, st));
   CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ids, 0));
@@ -274,8 +275,8 @@ ckv_status issue_prefetch(ckv_ctx* ctx, int layer, const int32_t* ids, const int
   PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)(layer * 2 + 1) * 4, ctx->stats,
              nullptr, ctx->epoch_dev};
   po.rank_keys = rank_keys;
-  LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 1, ctx->quota, ctx->epoch, ctx->rec_bytes, nullptr,
-                       ctx->scratch_side, po, ctx->side));
+  LK(launch_cache_plan(cache_layer(ctx, layer), ids, n_ids_dev, 0, 1, quota > 0 ? quota : ctx->quota, ctx->epoch,
+                       ctx->rec_bytes, nullptr, ctx->scratch_side, po, ctx->side));
   CK(cudaEventRecord(ctx->ev_pplan[layer], ctx->side));
   LK(launch_gather(ctx->gl_side, ctx->nload_side, host_layer_dev(ctx, layer), pool_layer(ctx, layer), ctx->rec_bytes,
                    ctx->side));
@@ -867,7 +868,11 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     }
     if (!ctx->global_heap && !late_pf)
       for (int lp = layer + 1; lp <= pend && lp < ctx->L; ++lp)
-        if ((s = issue_prefetch(ctx, lp, ids, nids, st, false, ctx->sel_keys[pid & 1])) != CKV_OK) return s;
+        // layers inside the period reuse ids exactly (load all k); the next period's first layer is
+        // speculative (the quota, highest-scored first)
+        if ((s = issue_prefetch(ctx, lp, ids, nids, st, false, ctx->sel_keys[pid & 1], lp < pend ? ctx->k : -1)) !=
+            CKV_OK)
+          return s;
     // subperiod gate: attention of the first layer waits for sp layers' chunks
     for (int lp = layer + 1; lp < layer + ctx->subperiod && lp < pend; ++lp)
       if (ctx->pf_issued[lp] == ctx->epoch) {
