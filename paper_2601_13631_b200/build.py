@@ -6,6 +6,8 @@ Each csrc/*.cu is compiled to an object in parallel, then linked with the static
 CUDA runtime (no libcuda link dependency: the driver API is reached through
 cudaGetDriverEntryPoint), so the library loads on a machine without a GPU.
 
+--variant NAME builds the current sources into libckv_NAME.so (A/B of source variants:
+CKV_LIBRARY=variant:NAME in scripts/).
 --tuning builds libckv_tuning.so with -DCKV_TUNING: the same kernels plus the environment
 knobs the A/B scripts use (CKV_PDL, CKV_SCORE_POLY, CKV_ATTN_SPLITS, traces ...).  The
 product libckv.so reads no environment variable.  Scripts select the tuning library with
@@ -60,8 +62,11 @@ def _compile(src, build_dir=BUILD, extra=()):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False, tuning: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, tuning: bool = False, variant: str = "") -> str:
     build_dir, lib_path = (BUILD_TUNING, LIB_TUNING) if tuning else (BUILD, LIB)
+    if variant:  # A/B: the current sources as libckv_<variant>.so (CKV_LIBRARY=variant:<variant>)
+        build_dir = os.path.join(HERE, "_build_var_" + variant)
+        lib_path = os.path.join(HERE, "libckv_" + variant + ".so")
     extra = ("-DCKV_TUNING",) if tuning else ()
     os.makedirs(build_dir, exist_ok=True)
     srcs = _sources()
@@ -83,4 +88,5 @@ def build(force: bool = False, verbose: bool = False, tuning: bool = False) -> s
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, tuning="--tuning" in sys.argv))
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, tuning="--tuning" in sys.argv, variant=var))

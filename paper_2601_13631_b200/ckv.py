@@ -13,9 +13,12 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libckv.so")
-# scripts/ A/B runs only: CKV_LIBRARY=tuning loads the knob-enabled build (build.py --tuning)
+# scripts/ A/B runs only: CKV_LIBRARY=tuning loads the knob-enabled build (build.py --tuning);
+# CKV_LIBRARY=variant:<name> loads libckv_<name>.so (a source variant built by build.py --variant)
 if os.environ.get("CKV_LIBRARY") == "tuning":
     LIB_PATH = os.path.join(_HERE, "libckv_tuning.so")
+elif os.environ.get("CKV_LIBRARY", "").startswith("variant:"):
+    LIB_PATH = os.path.join(_HERE, "libckv_" + os.environ["CKV_LIBRARY"][8:] + ".so")
 
 CKV_BF16, CKV_FP32 = 0, 1
 CKV_NORM_PREFIX, CKV_NORM_FULLROW = 0, 1

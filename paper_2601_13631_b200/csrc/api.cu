@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -20,6 +21,8 @@
 
 namespace ckv {
 void timeline_dump();  // debug (CKV_TIMELINE=1), defined at the end of this file
+void dtl_init();       // tuning build: device timeline (CKV_DTL=1)
+void dtl_dump();
 }
 
 using namespace ckv;
@@ -606,6 +609,7 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
   } while (0)
   CKC(cudaSetDevice(c.device));
   CKC(preload_kernels());  // no lazy module load later on the hot path (see common.cuh)
+  dtl_init();               // tuning build: device timeline (CKV_DTL=1)
   const int R_max = ctx->G * ctx->max_ns;
   ctx->nsplit_score_max = ctx->m_loc < 4096 ? ctx->m_loc : 4096;
   {
@@ -1245,6 +1249,7 @@ const char* ckv_last_error(const ckv_ctx* ctx) { return ctx ? ctx->err.c_str() :
 
 void ckv_destroy(ckv_ctx* ctx) {
   ckv::timeline_dump();
+  ckv::dtl_dump();
   if (!ctx) return;
   free_all(ctx);
   delete ctx;
@@ -1327,6 +1332,64 @@ void timeline_dump() {
     prev = ms;
   }
 }
+#ifdef CKV_TUNING
+static std::vector<DtlSetter>& dtl_setters() {
+  static std::vector<DtlSetter> v;
+  return v;
+}
+int register_dtl(DtlSetter f) {
+  dtl_setters().push_back(f);
+  return 0;
+}
+static unsigned long long* g_dtl_buf = nullptr;
+static unsigned int* g_dtl_cnt = nullptr;
+static std::vector<std::pair<unsigned long long, std::string>> g_dtl_names;  // (grid | block << 32, kernel)
+void dtl_init() {
+  if (!(tuning_env("CKV_DTL") && tuning_env("CKV_DTL")[0] == '1') || g_dtl_buf) return;
+  cudaMalloc(&g_dtl_buf, 8192 * 2 * sizeof(unsigned long long));
+  cudaMalloc(&g_dtl_cnt, sizeof(unsigned int));
+  cudaMemset(g_dtl_cnt, 0, sizeof(unsigned int));
+  for (DtlSetter f : dtl_setters()) f(g_dtl_buf, g_dtl_cnt);
+}
+void dtl_name(const void* kern, dim3 grid, dim3 block) {
+  if (!g_dtl_buf) return;
+  const unsigned long long key = grid.x | ((unsigned long long)block.x << 32);
+  for (auto& e : g_dtl_names)
+    if (e.first == key) return;
+  const char* name = nullptr;
+  cudaFuncGetName(&name, kern);
+  std::string nm = name ? name : "?";
+  const size_t k = nm.find("kernel");
+  if (k != std::string::npos) nm = nm.substr(0, k + 6);
+  const size_t b = nm.rfind("_N_");
+  if (b != std::string::npos) nm = nm.substr(b + 3);
+  const size_t u = nm.find("_cu_");
+  if (u != std::string::npos) nm = nm.substr(u + 4);
+  g_dtl_names.push_back({key, nm});
+}
+void dtl_dump() {
+  if (!g_dtl_buf) return;
+  cudaDeviceSynchronize();
+  unsigned int n = 0;
+  cudaMemcpy(&n, g_dtl_cnt, sizeof n, cudaMemcpyDeviceToHost);
+  if (n > 8192) n = 8192;
+  std::vector<unsigned long long> h(2 * (size_t)n);
+  cudaMemcpy(h.data(), g_dtl_buf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  std::vector<std::pair<unsigned long long, unsigned long long>> r;
+  for (unsigned i = 0; i < n; ++i) r.push_back({h[2 * i], h[2 * i + 1]});
+  std::sort(r.begin(), r.end());
+  for (auto& e : r) {
+    const char* nm = "?";
+    for (auto& k : g_dtl_names)
+      if (k.first == e.second) nm = k.second.c_str();
+    fprintf(stderr, "[dtl] %llu %u %u %s\n", e.first, (unsigned)(e.second & 0xffffffffu), (unsigned)(e.second >> 32), nm);
+  }
+}
+#else
+void dtl_init() {}
+void dtl_name(const void*, dim3, dim3) {}
+void dtl_dump() {}
+#endif
 bool pdl_enabled() {
   static int v = -1;
   if (v < 0) {

@@ -22,7 +22,33 @@ namespace ckv {
 // kernel chains -- plan, gather, attention -- read stale data: measured on B200.)  Only
 // constant inputs (q, k_suf, v_suf, the probe keys), TMEM / shared-memory setup and tensor-map
 // prefetches may precede pdl_wait().
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifdef CKV_TUNING
+// Device timeline (tuning build, CKV_DTL=1): CTA 0 / thread 0 of every kernel records the time its
+// pdl_wait() returned (= its predecessor completed) with its grid / block size; the per-TU
+// pointers are set by ckv_create (dtl_setters), ckv_destroy prints the records in time order.
+static __device__ unsigned long long* g_dtl = nullptr;
+static __device__ unsigned int* g_dtl_n = nullptr;
+using DtlSetter = cudaError_t (*)(unsigned long long*, unsigned int*);
+int register_dtl(DtlSetter f);
+static cudaError_t dtl_set_tu(unsigned long long* b, unsigned int* n) {
+  cudaError_t e = cudaMemcpyToSymbol(g_dtl, &b, sizeof b);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyToSymbol(g_dtl_n, &n, sizeof n);
+}
+static const int kDtlReg = register_dtl(dtl_set_tu);
+#endif
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef CKV_TUNING
+  if (g_dtl && threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned i = atomicAdd(g_dtl_n, 1u) & 8191u;
+    g_dtl[2 * i] = t;
+    g_dtl[2 * i + 1] = gridDim.x | ((unsigned long long)blockDim.x << 32);
+  }
+#endif
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();  // tuning build: CKV_PDL=0 disables the launch attribute (A/B measurements)
 // A kernel that follows a cross-stream event wait is launched without the attribute (the
@@ -30,6 +56,7 @@ bool pdl_enabled();  // tuning build: CKV_PDL=0 disables the launch attribute (A
 void pdl_mark_event_wait(cudaStream_t st);
 bool pdl_take_event_wait(cudaStream_t st);  // true (and cleared) if st was marked
 void timeline_mark(const void* kern, cudaStream_t st);
+void dtl_name(const void* kern, dim3 grid, dim3 block);  // tuning build: names for the device timeline
 // Every kernel of the library is registered at load time (static initialisers, no CUDA call) and
 // loaded by ckv_create (cudaFuncGetAttributes): with CUDA's lazy module loading, the first launch
 // of a kernel can block the host until the device is idle, which deadlocks a host thread that
@@ -65,6 +92,7 @@ inline cudaError_t launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, 
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<Args&&>(args)...);
   timeline_mark(reinterpret_cast<const void*>(kern), st);
+  dtl_name(reinterpret_cast<const void*>(kern), grid, block);
   return e;
 }
 

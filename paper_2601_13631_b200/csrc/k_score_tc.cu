@@ -52,6 +52,7 @@ struct TcParams {
   float scale;  // log2(e) / sqrt(d)
   int epi_sleep;  // epilogue warps wait for their accumulator with a suspend-time hint
   unsigned long long* trace;  // tuning build (CKV_SCORE_TRACE=1): %globaltimer events of CTA 0, else null
+  int dbg;  // tuning build (CKV_SCORE_DBG): 1 = no epilogue math, 2 = no MMAs, 3 = no stores (results invalid)
 };
 
 // ---- packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two fp32 lanes per instruction) ----
@@ -176,6 +177,9 @@ __device__ __forceinline__ void epilogue_unit(const TcParams& p, float (&v)[64],
     tot = t2[0];
   }
   if (!row_ok) return;
+#ifdef CKV_TUNING
+  if (p.dbg == 3 && tot != -1.f) return;  // all the math, no stores (tot is never -1)
+#endif
 #pragma unroll
   for (int i = 0; i < NC; ++i) {
     if (MASK && key0 / C + i >= p.g.m_loc) break;
@@ -339,6 +343,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t d_tmem = tmem_base + ab * BN;
         const uint32_t qa = ptx::smem_u32(qbuf0 + qs * kQBytes);
         const uint32_t ka = ptx::smem_u32(kbuf0 + kb * kKBytes);
+#ifdef CKV_TUNING
+        if (p.dbg != 2)
+#endif
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off_q = (k >> 2) * (kQBytes / 2) + (k & 3) * 32;
@@ -415,6 +422,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) ptx::mbar_arrive(&acc_empty[ab]);
           if (lane == 0 && e < 8 && (e & 3) == 0) trace_ev(p, 3, acount);
         }
+#ifdef CKV_TUNING
+        if (p.dbg == 1) {
+          if (row_ok && v[0] + v[63] == 12345.f) p.lam2[0] = v[1];  // keep the loads alive
+          continue;
+        }
+#endif
         const int key0 = kt * BN + cq * (BN / kColSplit);
         float* lamrow = p.lam2 + ((size_t)kvh * p.g.m_loc + key0 / C) * p.g.R + rho;
         float* lp = p.lampart + ((size_t)kvh * p.nsplit + kt * kColSplit + cq) * p.g.R + rho;
@@ -439,8 +452,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<512>(tmem_base);
+#ifdef CKV_TUNING
+    if (p.trace && lane == 0) {  // after the dealloc (slot 352 + CTA)
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      p.trace[5 * 32 + 352 + blockIdx.x] = t;
+    }
+#endif
   }
 }
+
+#ifdef CKV_TUNING
+__global__ void stamp_kernel(unsigned long long* t) {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  *t = v;
+}
+// calibration: a 576-thread CTA per SM that records its start / end like the score kernel
+__global__ void __launch_bounds__(kThreads, 1) null_kernel(unsigned long long* t) {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  __syncthreads();
+  if (threadIdx.x == 0) t[blockIdx.x] = v;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+  if (threadIdx.x == 0) t[160 + blockIdx.x] = v;
+}
+#endif
 
 // GQA row packing: qpack[kvh][rho][x] = q[r][kvh*G + g][x], rho = g*ns + r, zero rows past R.
 __global__ void pack_q_kernel(LayerGeom g, int R_pad, int perm, const __nv_bfloat16* __restrict__ q,
@@ -554,14 +591,16 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   p.scale = kLog2e / sqrtf((float)g.d);
   p.trace = nullptr;
   p.epi_sleep = 1;
+  p.dbg = 0;
 #ifdef CKV_TUNING
+  if (const char* es = tuning_env("CKV_SCORE_DBG")) p.dbg = atoi(es);
   if (const char* es = tuning_env("CKV_SCORE_EPI_SLEEP")) p.epi_sleep = atoi(es);
 #endif
 #ifdef CKV_TUNING
   static unsigned long long* trace_buf = nullptr;
   if (tuning_env("CKV_SCORE_TRACE")) {
-    if (!trace_buf) cudaMalloc(&trace_buf, (5 * 32 + 320) * sizeof(unsigned long long));
-    cudaMemsetAsync(trace_buf, 0, (5 * 32 + 320) * sizeof(unsigned long long), st);
+    if (!trace_buf) cudaMalloc(&trace_buf, (5 * 32 + 352 + 160) * sizeof(unsigned long long));
+    cudaMemsetAsync(trace_buf, 0, (5 * 32 + 352 + 160) * sizeof(unsigned long long), st);
     p.trace = trace_buf;
   }
 #endif
@@ -581,6 +620,16 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
   }
   const int grid = p.n_units < num_sms() ? p.n_units : num_sms();
   cudaError_t el;
+#ifdef CKV_TUNING
+  cudaEvent_t tev0 = nullptr, tev1 = nullptr;
+  if (p.trace) {
+    cudaEventCreate(&tev0);
+    cudaEventCreate(&tev1);
+    cudaStreamSynchronize(st);
+    cudaEventRecord(tev0, st);
+    stamp_kernel<<<1, 1, 0, st>>>(p.trace + 5 * 32 + 318);
+  }
+#endif
   switch (g.c) {
     case 1: el = launch_c<1>(tmK, tmQ, p, grid, st); break;
     case 2: el = launch_c<2>(tmK, tmQ, p, grid, st); break;
@@ -594,17 +643,33 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
 #ifdef CKV_TUNING
   if (p.trace && el == cudaSuccess) {  // synchronous dump of CTA 0's events (us since its first)
     unsigned long long h[5][32], cta[320];
+    stamp_kernel<<<1, 1, 0, st>>>(p.trace + 5 * 32 + 319);
+    cudaEventRecord(tev1, st);
     cudaStreamSynchronize(st);
+    float tev_ms = 0.f;
+    cudaEventElapsedTime(&tev_ms, tev0, tev1);
+    fprintf(stderr, "[score trace] launch event time %.2f us (stream idle before)\n", tev_ms * 1e3);
+    cudaEventDestroy(tev0);
+    cudaEventDestroy(tev1);
     cudaMemcpy(h, p.trace, sizeof h, cudaMemcpyDeviceToHost);
     cudaMemcpy(cta, p.trace + 5 * 32, sizeof cta, cudaMemcpyDeviceToHost);
     {
-      unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+      unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0, dmax = 0;
+      {
+        unsigned long long dl[160];
+        cudaMemcpy(dl, p.trace + 5 * 32 + 352, sizeof dl, cudaMemcpyDeviceToHost);
+        for (int b = 0; b < grid; ++b) dmax = dl[b] > dmax ? dl[b] : dmax;
+      }
       for (int b = 0; b < grid; ++b) {
         s0 = cta[b] < s0 ? cta[b] : s0;
         s1 = cta[b] > s1 ? cta[b] : s1;
         e0 = cta[160 + b] < e0 ? cta[160 + b] : e0;
         e1 = cta[160 + b] > e1 ? cta[160 + b] : e1;
       }
+      fprintf(stderr, "[score trace] stamp before -> first CTA start %.2f us; last CTA end -> stamp after %.2f us; "
+              "last dealloc -> stamp after %.2f us\n",
+              ((long long)s0 - (long long)cta[318]) * 1e-3, ((long long)cta[319] - (long long)e1) * 1e-3,
+              ((long long)cta[319] - (long long)dmax) * 1e-3);
       fprintf(stderr, "[score trace] CTA start spread %.2f us, end %.2f..%.2f us after first start; CTA0 start %.2f end %.2f\n",
               (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, (e1 - s0) * 1e-3, (cta[0] - s0) * 1e-3, (cta[160] - s0) * 1e-3);
     }
@@ -612,6 +677,23 @@ cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __
     for (auto& r : h)
       for (unsigned long long t : r)
         if (t && t < t0) t0 = t;
+    {
+      unsigned long long* cal = nullptr;
+      cudaMalloc(&cal, 320 * sizeof(unsigned long long));
+      stamp_kernel<<<1, 1, 0, st>>>(cal + 318);
+      null_kernel<<<grid, kThreads, 0, st>>>(cal);
+      stamp_kernel<<<1, 1, 0, st>>>(cal + 319);
+      unsigned long long hc[320];
+      cudaMemcpy(hc, cal, sizeof hc, cudaMemcpyDeviceToHost);
+      unsigned long long c0 = ~0ull, c1 = 0;
+      for (int b = 0; b < grid; ++b) {
+        c0 = hc[b] < c0 ? hc[b] : c0;
+        c1 = hc[160 + b] > c1 ? hc[160 + b] : c1;
+      }
+      fprintf(stderr, "[score trace] calibration null kernel: stamp -> start %.2f us, end -> stamp %.2f us\n",
+              ((long long)c0 - (long long)hc[318]) * 1e-3, ((long long)hc[319] - (long long)c1) * 1e-3);
+      cudaFree(cal);
+    }
     const char* nm[5] = {"q_land", "acc_free", "mma_done", "release", "epi_done"};
     for (int ev = 0; ev < 5; ++ev) {
       fprintf(stderr, "[score trace] %-8s", nm[ev]);
