@@ -55,6 +55,9 @@ struct ckv_ctx {
   float *lam2 = nullptr, *lampart = nullptr, *Lam2 = nullptr, *A = nullptr, *Apart = nullptr;
   int32_t* ids_buf[2] = {nullptr, nullptr};
   uint64_t* sel_keys[2] = {nullptr, nullptr};  // (score bits << 32 | ~id) of ids_buf's entries (rank the speculation)
+  int32_t *ids_b = nullptr, *n_b = nullptr;    // topk_plan2's CTA 1: its private copy of the top-k
+  int lam2_layer = -1;  // layer whose row normalisers Lam2 holds (the attention's softmax reference)
+  uint64_t* cand_b = nullptr;
   int32_t* n_ids_buf[2] = {nullptr, nullptr};
   int32_t *kept_slots = nullptr, *ids_glob = nullptr, *flag = nullptr;
   int32_t *scratch_main = nullptr, *scratch_side = nullptr;
@@ -263,6 +266,7 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
                                      static_cast<const __nv_bfloat16*>(ks), lam_local_out ? 0 : ctx->fullrow, nullptr,
                                      1, ctx->Lam2, lam_local_out, st));
   PROF_END(1);
+  ctx->lam2_layer = layer;  // Lam2 bounds every prefix logit of this layer's rows (local or global LSE)
   return CKV_OK;
 }
 
@@ -348,7 +352,7 @@ ckv_status run_attend(ckv_ctx* ctx, int layer, const int32_t* ids, const int32_t
                          reinterpret_cast<const __nv_bfloat16*>(pool_layer(ctx, layer)), ctx->kept_slots, ids,
                          n_ids_dev, ctx->k, include_suffix, nsplit, ctx->o_part, ctx->lse_part, ctx->dense_kv,
                          host_layer_dev(ctx, layer), static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)),
-                         after_slots, st);
+                         after_slots, ctx->lam2_layer == layer ? ctx->Lam2 : nullptr, st);
       if (e == cudaSuccess) after_slots = nullptr;  // recorded between the compaction and the attention
       if (e == cudaSuccess) ctx->launches += 1;  // + the dense K/V compaction kernel
     }
@@ -392,7 +396,7 @@ void free_all(ckv_ctx* ctx) {
     if (p) cudaFree(p);
   for (void* p : ctx->x_opened) cudaIpcCloseMemHandle(p);
   for (void* p : {(void*)ctx->xwin, (void*)ctx->lam_loc, (void*)ctx->cand_loc, (void*)ctx->sel_keys[0],
-                  (void*)ctx->sel_keys[1]})
+                  (void*)ctx->sel_keys[1], (void*)ctx->ids_b, (void*)ctx->n_b, (void*)ctx->cand_b})
     if (p) cudaFree(p);
   if (ctx->host_store) cudaFreeHost(ctx->host_store);
   for (auto e : ctx->ev_pplan)
@@ -645,6 +649,11 @@ ckv_status ckv_create(const ckv_config* cfg, ckv_ctx** out) {
     CKC(dalloc(&ctx->ids_buf[i], (size_t)ctx->k));
     CKC(dalloc(&ctx->n_ids_buf[i], 1));
     CKC(dalloc(&ctx->sel_keys[i], (size_t)ctx->k));
+    if (i == 0) {
+      CKC(dalloc(&ctx->ids_b, (size_t)ctx->k));
+      CKC(dalloc(&ctx->n_b, 1));
+      CKC(dalloc(&ctx->cand_b, (size_t)ctx->k));
+    }
   }
   CKC(dalloc(&ctx->kept_slots, (size_t)ctx->k));
   CKC(dalloc(&ctx->ids_glob, (size_t)ctx->k));
@@ -835,10 +844,15 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     PROF_BEGIN(2);
     LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
     PROF_END(2);
-    PROF_BEGIN(6);
-    LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, ctx->sel_keys[pid & 1], ctx->k,
-                          nids, st));
-    PROF_END(6);
+    // p = 1 with the speculative plan fused (below): the top-k runs inside that launch too
+    static const bool topk_fuse_on = !(tuning_env("CKV_TOPK_PLAN") && tuning_env("CKV_TOPK_PLAN")[0] == '0');
+    const bool fuse_sel = late_pf && plan2_on && gather_fused(ctx) && topk_fuse_on && ctx->m_loc <= 8192;
+    if (!fuse_sel) {
+      PROF_BEGIN(6);
+      LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, 0, 1, ids, ctx->sel_keys[pid & 1],
+                            ctx->k, nids, st));
+      PROF_END(6);
+    }
     // intra-period loads (exact ids) for the period's other layers, then the speculative load of
     // the next period's first layer (A6), all on the side stream in layer order
     // (global heap: one shared pool, so the next layer's speculative plan may only run after this
@@ -858,14 +872,20 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
                 demand_plan_out(ctx, layer, selected_ids)};
       PlanOut po{ctx->gl_side, ctx->nload_side, nullptr, nullptr, ctx->counts + (size_t)((layer + 1) * 2 + 1) * 4,
                  ctx->stats, nullptr, ctx->epoch_dev};
-      po.rank_keys = ctx->sel_keys[pid & 1];
+      po.rank_keys = fuse_sel ? ctx->cand_b : ctx->sel_keys[pid & 1];
       if (layer > 0) {
         po.gate_misses = ctx->counts + (size_t)((layer - 1) * 2) * 4 + 1;
         po.gate_max = ctx->spec_gate;
       }
-      PlanJob b{cache_layer(ctx, layer + 1), ids, nids, 0, 1, ctx->quota, ctx->epoch, ctx->rec_bytes,
-                ctx->scratch_side, po};
-      LK(launch_cache_plan2(a, b, st));
+      PlanJob b{cache_layer(ctx, layer + 1), fuse_sel ? ctx->ids_b : ids, fuse_sel ? ctx->n_b : nids, 0, 1, ctx->quota,
+                ctx->epoch, ctx->rec_bytes, ctx->scratch_side, po};
+      if (fuse_sel) {
+        TopkJob t{ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, ids, ctx->sel_keys[pid & 1], nids,
+                  ctx->ids_b, ctx->cand_b, ctx->n_b};
+        LK(launch_topk_plan2(t, a, b, st));
+      } else {
+        LK(launch_cache_plan2(a, b, st));
+      }
       PROF_END(3);
       planned = true;
       planned2 = true;
@@ -944,6 +964,7 @@ ckv_status ckv_shard_select(ckv_ctx* ctx, int32_t layer, const void* q, const vo
     LK(launch_row_lse<__nv_bfloat16>(g, nullptr, 0, static_cast<const __nv_bfloat16*>(q),
                                      static_cast<const __nv_bfloat16*>(k_suf), ctx->fullrow, lam_all, ctx->W,
                                      ctx->Lam2, nullptr, st));
+  ctx->lam2_layer = layer;
   LK(launch_chunk_sum(g, ctx->lam2, ctx->Lam2, ctx->Apart, st));
   LK(launch_topk_scores(ctx->A, ctx->Apart, ctx->Hkv, ctx->m_loc, ctx->k, ctx->j0, ctx->cyc_W > 0 ? ctx->cyc_W : 1,
                         nullptr, cand, ctx->k, nullptr, st));

@@ -245,6 +245,22 @@ struct PlanJob {  // one cache_plan_body invocation (launch_cache_plan2)
   PlanOut out;
 };
 cudaError_t launch_cache_plan2(const PlanJob& a, const PlanJob& b, cudaStream_t st);
+// A3 top-k of the local chunk scores fused with the two plans of launch_cache_plan2: both CTAs run
+// the same top-k (deterministic); CTA 0 writes A, ids, n_ids, rank keys (cand) and plans job a on
+// them; CTA 1 writes its copy to ids_b / cand_b / n_b and plans job b on those (job b's ids,
+// n_ids_dev and out.rank_keys must point there).  m <= 8192, else cudaErrorNotSupported.
+struct TopkJob {
+  float* A;
+  const float* Apart;
+  int nparts, m, k;
+  int32_t* ids;
+  uint64_t* cand;
+  int32_t* n_out;
+  int32_t* ids_b;
+  uint64_t* cand_b;
+  int32_t* n_b;
+};
+cudaError_t launch_topk_plan2(const TopkJob& t, const PlanJob& a, const PlanJob& b, cudaStream_t st);
 cudaError_t launch_epoch_inc(int32_t* epoch_dev, cudaStream_t st);
 cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,
                           char* pool_layer, int64_t rec_bytes, cudaStream_t st);
@@ -273,7 +289,8 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
                            const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
                            int nsplit, float* o_part, float* lse_part, void* dense_ws, const char* host_layer,
-                           const __nv_bfloat16* probe_layer, cudaEvent_t after_compact, cudaStream_t st);
+                           const __nv_bfloat16* probe_layer, cudaEvent_t after_compact, const float* lam_ref,
+                           cudaStream_t st);
 template <typename T>
 cudaError_t launch_attn_combine(const LayerGeom& g, const float* o_part, const float* lse_part, int nsplit,
                                 T* out, float* o_f32, float* lse_nat, cudaStream_t st, const XPartDst* xd = nullptr);

@@ -21,9 +21,14 @@
 //               pipelined one tile behind S.  tcgen05 MMAs execute in issue order, so S(j+2)
 //               (same TMEM buffer) follows PV(j).
 //   warps 2..17 softmax: one row per thread, four warps per TMEM lane quadrant (32 key
-//               columns and 32 O columns each); row max exchanged through shared memory; lazy O
-//               rescale (only when the running max grows by > 8 in log2 units); P = 2^(s - m)
-//               as bf16 into TMEM.  They also load each item's Q rows from q into TMEM.
+//               columns and 32 O columns each); P = 2^(s - m) as bf16 into TMEM (each warp writes
+//               its 16 P columns over the first half of its own 32 S columns, so no warp waits
+//               for another before overwriting S).  The reference m of a row is its prefix LSE
+//               Lambda2 from A2 when the layer was scored (lam_ref): every prefix logit is <= it
+//               (an LSE bounds the max), so prefix tiles need no row max, no cross-warp exchange
+//               and no rescale; the suffix tile (or a layer without lam_ref) computes the row max
+//               through shared memory with a lazy O rescale (only when the running max grows by
+//               > 8 in log2 units).  They also load each item's Q rows from q into TMEM.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -61,6 +66,7 @@ struct AttnParams {
   float scale;
   float* o_part;
   float* lse_part;
+  const float* lam_ref;  // Lambda2 [Hkv][R] of this layer (log2 units, >= every prefix logit) or null
   unsigned long long* trace;  // debug: %globaltimer events of CTA 0 (CKV_ATTN_TRACE=1), else null
 };
 
@@ -212,7 +218,9 @@ __device__ __forceinline__ void issue_pv(uint32_t tmem, uint8_t* kvbuf0, uint64_
   const uint32_t va0 = ptx::smem_u32(kvbuf0 + stage * kKVBytes + 2 * kPartBytes);
   const int ksteps = (nkeys + 15) / 16;  // key steps past the tile's valid keys are skipped
   for (int k = 0; k < ksteps; ++k)
-    ptx::mma_bf16_ts(tmem + kColO, tmem + sbuf * BN + k * 8, ptx::umma_desc_sw128_mn(va0 + k * 16 * 128, kPartBytes),
+    // P of keys [16k, 16k + 16): written by softmax warp k / 2 at its S columns 32 (k / 2) + 8 (k % 2)
+    ptx::mma_bf16_ts(tmem + kColO, tmem + sbuf * BN + (k >> 1) * 32 + (k & 1) * 8,
+                     ptx::umma_desc_sw128_mn(va0 + k * 16 * 128, kPartBytes),
                      idesc_o, k > 0 || jj > 0 ? 1u : 0u);
   ptx::mma_commit(pv_done);
   ptx::mma_commit(&kv_empty[stage]);
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
     const int rit = quad * 32 + lane;  // row in tile
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t bar_id = 1 + quad;  // named barrier of the quadrant's NWQ warps
-    int icount = 0, scount = 0, pcount = 0;
+    int icount = 0, scount = 0, pcount = 0, nx = 0;  // nx: row-max exchanges (red_m parity)
     int n_kept = -1, n_valid_prefix = 0;
     const float sc = p.scale;
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++icount) {
@@ -387,6 +395,13 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
       }
       const Tiles tl = item_tiles(p, sp, n_kept);
       float m_ref = -INFINITY, l = 0.f;
+      // prefix LSE as the reference (uniform over the quadrant's 4 warps: they share these rows)
+      bool ref_ok = false;
+      if (p.lam_ref) {
+        const float lr = row_ok ? p.lam_ref[(size_t)kvh * p.g.R + rho] : 0.f;
+        ref_ok = __all_sync(0xffffffffu, lr > -INFINITY && lr < INFINITY);
+        if (ref_ok) m_ref = lr;
+      }
       int j = 0;
       for (int t = tl.t0; t < tl.t1; ++t) {
         if (!tile_present(p, tl, t)) continue;
@@ -405,28 +420,31 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           for (int i = 0; i < CPW; ++i)
             if (b0 + i >= lim) x[i] = -INFINITY;
         }
-        float mx[CPW / 2];
+        float f = 1.f;
+        bool resc = false;
+        if (!(ref_ok && pre)) {  // row max needed: suffix tile, or no prefix-LSE reference
+          float mx[CPW / 2];
 #pragma unroll
-        for (int i = 0; i < CPW / 2; ++i) mx[i] = fmaxf(x[i], x[i + CPW / 2]);
+          for (int i = 0; i < CPW / 2; ++i) mx[i] = fmaxf(x[i], x[i + CPW / 2]);
 #pragma unroll
-        for (int n = CPW / 4; n >= 1; n >>= 1)
+          for (int n = CPW / 4; n >= 1; n >>= 1)
 #pragma unroll
-          for (int i = 0; i < n; ++i) mx[i] = fmaxf(mx[i], mx[i + n]);
-        // red_m is double-buffered by tile parity: a warp can only overwrite a buffer two tiles
-        // later, after the next barrier, which every reader of this tile's values has passed
-        float* rm = red_m[j & 1];
-        rm[h * 128 + rit] = mx[0];
-        // after this barrier every warp of the quadrant holds its S columns in registers, so
-        // P may be written over the S buffer
-        ptx::named_bar_sync(bar_id, 32 * NWQ);
-        float tmax = rm[rit];
+            for (int i = 0; i < n; ++i) mx[i] = fmaxf(mx[i], mx[i + n]);
+          // red_m is double-buffered by tile parity: a warp can only overwrite a buffer two
+          // exchanges later, after the next barrier, which every reader of these values has passed
+          float* rm = red_m[nx & 1];
+          ++nx;
+          rm[h * 128 + rit] = mx[0];
+          ptx::named_bar_sync(bar_id, 32 * NWQ);
+          float tmax = rm[rit];
 #pragma unroll
-        for (int w = 1; w < NWQ; ++w) tmax = fmaxf(tmax, rm[w * 128 + rit]);
-        tmax *= sc;
-        const float m_new = fmaxf(m_ref, tmax);
-        const bool resc = (j > 0) && (m_ref != -INFINITY) && (m_new > m_ref + kRescaleThresh);
-        const float f = resc ? fast_exp2(m_ref - m_new) : 1.f;
-        if (j == 0 || m_ref == -INFINITY || resc) m_ref = m_new;
+          for (int w = 1; w < NWQ; ++w) tmax = fmaxf(tmax, rm[w * 128 + rit]);
+          tmax *= sc;
+          const float m_new = fmaxf(m_ref, tmax);
+          resc = (j > 0) && (m_ref != -INFINITY) && (m_new > m_ref + kRescaleThresh);
+          f = resc ? fast_exp2(m_ref - m_new) : 1.f;
+          if (j == 0 || m_ref == -INFINITY || resc) m_ref = m_new;
+        }
         const float msub = (m_ref == -INFINITY) ? 0.f : m_ref;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t pk[CPW / 2];
@@ -453,8 +471,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const __grid_const
           ptx::tmem_st32(ta, o);
         }
         l = l * f + lsum;
-        // P(j) over S(j): keys [h*32, h*32+32) -> columns [h*16, h*16+16) of the S buffer
-        ptx::tmem_st16_nowait(tmem + sb * BN + h * (CPW / 2) + lane_off, pk);
+        // P(j) over S(j): keys [h*32, h*32+32) -> columns [h*32, h*32+16) of the S buffer (this
+        // warp's own S columns, already in its registers)
+        ptx::tmem_st16_nowait(tmem + sb * BN + h * CPW + lane_off, pk);
         ptx::tmem_wait_st();
         ptx::tc_fence_before();
         __syncwarp();
@@ -564,7 +583,8 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
                            const __nv_bfloat16* v_suf, const __nv_bfloat16* pool_layer, const int32_t* kept_slots,
                            const int32_t* kept_ids, const int32_t* n_kept_dev, int k_cap, int include_suffix,
                            int nsplit, float* o_part, float* lse_part, void* dense_ws, const char* host_layer,
-                           const __nv_bfloat16* probe_layer, cudaEvent_t after_compact, cudaStream_t st) {
+                           const __nv_bfloat16* probe_layer, cudaEvent_t after_compact, const float* lam_ref,
+                           cudaStream_t st) {
   if (!attn_tc_supported(g) || !dense_ws) return cudaErrorNotSupported;
   AttnParams p;
   p.g = g;
@@ -582,6 +602,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   p.scale = kLog2e / sqrtf((float)g.d);
   p.o_part = o_part;
   p.lse_part = lse_part;
+  p.lam_ref = lam_ref;
   const int64_t rec_bytes = (int64_t)(g.rec_swz == 2 ? 1 : 2) * g.Hkv * g.c * D * 2;
   const int64_t n_warps = (int64_t)g.Hkv * k_cap * 4 + (include_suffix ? (int64_t)g.Hkv * g.ns * 2 : 0);
   const int cblocks = (int)std::min<int64_t>((n_warps + 7) / 8, 8 * sm_count());

@@ -49,6 +49,26 @@ __global__ void __launch_bounds__(NT) cache_plan2_kernel(PlanJob a, PlanJob b) {
                       smem_keys ? plan_skeys : nullptr);
 }
 
+// A3 + the two plans above in one launch: the top-k is single-CTA work, so both CTAs compute it
+// (same keys, same result) instead of a separate one-CTA launch whose completion the plans would
+// wait for -- one kernel boundary less on the layer's serial chain.
+template <int KPT>
+__global__ void __launch_bounds__(NT) topk_plan2_kernel(TopkJob t, PlanJob a, PlanJob b) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ PlanSmem ps;
+  extern __shared__ uint64_t plan_skeys[];
+  const bool c0 = blockIdx.x == 0;
+  topk_body<NT, KPT>(c0 ? t.A : nullptr, t.Apart, t.nparts, t.m, t.k, 0, 1, c0 ? t.ids : t.ids_b, c0 ? t.cand : t.cand_b,
+                     t.k, c0 ? t.n_out : t.n_b, ps.ss);
+  __syncthreads();  // this CTA's ids / n / keys (and CTA 0's A, read by the fused A9) are written
+  const PlanJob& j = c0 ? a : b;
+  const int n_ids = j.n_ids_dev ? *j.n_ids_dev : j.n_ids_host;
+  const bool smem_keys = j.cl.P > NT * kPlanKPT && j.cl.P <= kPlanSmemKeysMax;
+  cache_plan_body<NT>(j.cl, j.ids, n_ids, j.prefetch, j.quota, j.epoch, j.rec_bytes, j.scratch, j.out, ps,
+                      smem_keys ? plan_skeys : nullptr);
+}
+
 // Whole-record copy host store -> HBM slot: work items are 4 KiB segments of records so a
 // few misses still keep many 16-B loads in flight over the host link.  Small CTAs (4 warps,
 // <= 64 registers): one fits on an SM beside a persistent score / attention CTA (576 threads x
@@ -148,6 +168,8 @@ __global__ void epoch_inc_kernel(int32_t* e) {
   pdl_wait();
   pdl_trigger(); *e += 1; }
 
+const int kReg2 = register_kernels({(const void*)topk_plan2_kernel<1>, (const void*)topk_plan2_kernel<2>,
+                                    (const void*)topk_plan2_kernel<4>, (const void*)topk_plan2_kernel<8>});
 const int kReg = register_kernels({(const void*)cache_plan_kernel, (const void*)cache_plan2_kernel, (const void*)gather_kernel,
                                    (const void*)cache_update_kernel, (const void*)pack_probe_kernel<float>,
                                    (const void*)pack_probe_kernel<__nv_bfloat16>, (const void*)pack_records_kernel<float>,
@@ -194,6 +216,30 @@ cudaError_t launch_cache_plan2(const PlanJob& a, const PlanJob& b, cudaStream_t 
   }
   if (cudaError_t e_ = launch_kernel(cache_plan2_kernel, 2, NT, smem, st, a, b)) return e_;
   return cudaGetLastError();
+}
+
+cudaError_t launch_topk_plan2(const TopkJob& t, const PlanJob& a, const PlanJob& b, cudaStream_t st) {
+  size_t smem = 0;
+  const int P = a.cl.P > b.cl.P ? a.cl.P : b.cl.P;
+  const bool big = P > NT * kPlanKPT && P <= kPlanSmemKeysMax;
+  if (big) smem = (size_t)P * sizeof(uint64_t);
+  static bool attr = false;
+  if (big && !attr) {
+    for (auto kern : {topk_plan2_kernel<1>, topk_plan2_kernel<2>, topk_plan2_kernel<4>, topk_plan2_kernel<8>})
+      if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)(kPlanSmemKeysMax * sizeof(uint64_t))))
+        return e;
+    attr = true;
+  }
+  auto go = [&](void (*kern)(TopkJob, PlanJob, PlanJob)) -> cudaError_t {
+    if (cudaError_t e_ = launch_kernel(kern, 2, NT, smem, st, t, a, b)) return e_;
+    return cudaGetLastError();
+  };
+  if (t.m <= NT) return go(topk_plan2_kernel<1>);
+  if (t.m <= 2 * NT) return go(topk_plan2_kernel<2>);
+  if (t.m <= 4 * NT) return go(topk_plan2_kernel<4>);
+  if (t.m <= 8 * NT) return go(topk_plan2_kernel<8>);
+  return cudaErrorNotSupported;
 }
 
 cudaError_t launch_gather(const int32_t* gather_list, const int32_t* n_load, const char* host_layer_dev,

@@ -293,7 +293,7 @@ __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart
       if (Apart) {  // A_j = sum over KV heads of the chunk-sum partials, fixed order
         a = 0.f;
         for (int h = 0; h < nparts; ++h) a += __ldcg(Apart + (size_t)h * m + j);
-        A[j] = a;
+        if (A) A[j] = a;  // (null: a private copy of the select, topk_plan2_kernel's CTA 1)
       } else {
         a = A[j];
       }
