@@ -57,6 +57,7 @@ struct ckv_ctx {
   uint64_t* sel_keys[2] = {nullptr, nullptr};  // (score bits << 32 | ~id) of ids_buf's entries (rank the speculation)
   int32_t *ids_b = nullptr, *n_b = nullptr;    // topk_plan2's CTA 1: its private copy of the top-k
   int lam2_layer = -1;  // layer whose row normalisers Lam2 holds (the attention's softmax reference)
+  int spec_next = -1;   // layer whose speculative gather (gl_side) its score kernel runs (p = 1, tcgen05)
   uint64_t* cand_b = nullptr;
   int32_t* n_ids_buf[2] = {nullptr, nullptr};
   int32_t *kept_slots = nullptr, *ids_glob = nullptr, *flag = nullptr;
@@ -235,9 +236,18 @@ ckv_status run_score(ckv_ctx* ctx, int layer, const void* q, const void* ks, int
   PROF_BEGIN(0);
   if (ctx->score_kind == 1) {
     nsplit = score_tc_nsplit(g);
+    SpecGather spec;
+    if (ctx->spec_next == layer) {  // planned by the previous layer (CTA 1 of its top-k / plan launch)
+      spec.list = ctx->gl_side;
+      spec.n_load = ctx->nload_side;
+      spec.host_layer = host_layer_dev(ctx, layer);
+      spec.pool_layer = pool_layer(ctx, layer);
+      spec.rec_bytes = ctx->rec_bytes;
+    }
+    ctx->spec_next = -1;
     e = launch_score_tc(g, static_cast<const __nv_bfloat16*>(q),
                         static_cast<const __nv_bfloat16*>(probe_layer(ctx, layer)), ctx->lam2, ctx->lampart, nsplit,
-                        ctx->tmap_cache, st);
+                        ctx->tmap_cache, spec, st);
     if (e == cudaSuccess) {
       ctx->launches += score_tc_packs_q(g);  // + the Q pack kernel
     }
@@ -806,6 +816,7 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     return reprefill_sharded(ctx, layer, q, k_suf, v_suf, n_suffix, out, selected_ids, chunk_scores, st);
   if (layer == 0) {
     ++ctx->epoch;
+    ctx->spec_next = -1;
     LK(launch_epoch_inc(ctx->epoch_dev, st));
   }
   const int p = ctx->period;
@@ -912,7 +923,15 @@ ckv_status ckv_reprefill_layer(ckv_ctx* ctx, int32_t layer, const void* q, const
     return s;
   if (defer_pf && (s = issue_prefetch(ctx, layer + 1, ids, nids, st, true, ctx->sel_keys[pid & 1])) != CKV_OK)
     return s;
-  if (late_pf && planned2) {  // speculative gather of the layer planned by cache_plan2 (CTA 1)
+  static const bool inscore_on = !(tuning_env("CKV_SPEC_INSCORE") && tuning_env("CKV_SPEC_INSCORE")[0] == '0');
+  if (late_pf && planned2 && inscore_on && ctx->score_kind == 1) {
+    // the speculative gather of the next layer (planned by CTA 1 above) runs in that layer's score
+    // kernel (its gather warp): stream order completes it before that layer's plan -- nothing to join
+    ctx->spec_next = layer + 1;
+    ctx->pf_issued[layer + 1] = ctx->epoch;
+    ctx->pf_joined[layer + 1] = ctx->epoch;
+    ctx->pf_late[layer + 1] = 1;
+  } else if (late_pf && planned2) {  // speculative gather of the layer planned by cache_plan2 (CTA 1)
     CK(cudaEventRecord(ctx->ev_ids, st));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_ids, 0));
     pdl_mark_event_wait(ctx->side);

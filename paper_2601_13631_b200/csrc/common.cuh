@@ -169,8 +169,17 @@ template <typename T>
 cudaError_t launch_score_simt(const LayerGeom& g, const T* q, const T* probe_layer, float* lam2,
                               float* lampart, int nsplit, cudaStream_t st);
 // A1 tcgen05 (bf16 only, d == 128); returns cudaErrorNotSupported if the shape is outside it
+// A6 speculative gather run by the score kernel's gather warp: (chunk, slot) pairs, count on device
+struct SpecGather {
+  const int32_t* list = nullptr;
+  const int32_t* n_load = nullptr;
+  const char* host_layer = nullptr;
+  char* pool_layer = nullptr;
+  int64_t rec_bytes = 0;
+};
 cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* probe_layer,
-                            float* lam2, float* lampart, int nsplit, void* qpack_ws, cudaStream_t st);
+                            float* lam2, float* lampart, int nsplit, void* qpack_ws, const SpecGather& spec,
+                            cudaStream_t st);
 int score_tc_nsplit(const LayerGeom& g);   // 0 if the shape is outside the tcgen05 kernel
 size_t score_tc_qpack_elems(int Hkv, int R_max);
 int score_tc_packs_q(const LayerGeom& g);  // 1 if the launch includes the Q pack kernel (n_s % 128 != 0)

@@ -10,6 +10,10 @@
 //               from a GQA-packed Q [Hkv][R_pad][128]; 128-byte swizzle.
 //   warp 1      TMEM allocator + single-thread MMA issuer: D[128 x 256] fp32 in TMEM
 //               (two accumulators = all 512 columns), 8 x tcgen05.mma kind::f16 (K = 16 each).
+//   warp 18     speculative gather (A6): the whole-chunk records the previous layer's plan chose
+//               for this layer, host store -> HBM slots, one 4 KiB segment per warp iteration
+//               (the link transfer overlaps this layer's scoring on the SMs it already holds, so
+//               it needs no side stream, no event join and no SM of its own); idle otherwise.
 //   warps 2..17 epilogue: tcgen05.ld 32 columns at a time, one suffix row per thread (TMEM lane),
 //               four warps per lane quadrant (64 columns each); per-chunk LSE in registers,
 //               coalesced lam2 stores ([kvh][chunk][row] layout).
@@ -27,7 +31,9 @@ namespace {
 constexpr int BM = 128, BN = 256, D = 128;
 constexpr int kEpiWarps = 16;  // 4 per TMEM lane quadrant, 64 key columns each
 constexpr int kColSplit = kEpiWarps / 4;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr int kGatherWarp = 2 + kEpiWarps;
+constexpr int kThreads = 96 + 32 * kEpiWarps;
+constexpr int kGatherSeg = 4096;  // bytes per gather work item (as gather_kernel, k_cache.cu)
 constexpr uint32_t kKBytes = BN * D * 2;  // 65536
 constexpr uint32_t kQBytes = BM * D * 2;  // 32768
 // Ring depths: the default (several row tiles per KV head) streams a new Q tile per unit through
@@ -52,6 +58,7 @@ struct TcParams {
   float scale;  // log2(e) / sqrt(d)
   int epi_sleep;  // epilogue warps wait for their accumulator with a suspend-time hint
   unsigned long long* trace;  // tuning build (CKV_SCORE_TRACE=1): %globaltimer events of CTA 0, else null
+  SpecGather spec;  // A6 speculative gather of this layer (list null: none)
   int dbg;  // tuning build (CKV_SCORE_DBG): 1 = no epilogue math, 2 = no MMAs, 3 = no stores (results invalid)
 };
 
@@ -363,6 +370,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++acount;
       }
     }
+  } else if (warp == kGatherWarp) {
+    if (p.spec.list) {
+      pdl_wait();  // the list and count come from the previous layer's plan
+      const int n = *p.spec.n_load;
+      const int64_t rb = p.spec.rec_bytes;
+      const int nseg = (int)((rb + kGatherSeg - 1) / kGatherSeg);
+      for (int it = blockIdx.x; it < n * nseg; it += gridDim.x) {
+        const int e = it / nseg, sg = it - e * nseg;
+        const int j = p.spec.list[2 * e], s = p.spec.list[2 * e + 1];
+        const int64_t off = (int64_t)sg * kGatherSeg;
+        const int cnt = (int)(min((int64_t)kGatherSeg, rb - off) / 16);
+        const int4* src = reinterpret_cast<const int4*>(p.spec.host_layer + (int64_t)j * rb + off);
+        int4* dst = reinterpret_cast<int4*>(p.spec.pool_layer + (int64_t)s * rb + off);
+        int4 v[kGatherSeg / 16 / 32];
+#pragma unroll
+        for (int u = 0; u < kGatherSeg / 16 / 32; ++u)
+          if (lane + 32 * u < cnt) v[u] = __ldg(src + lane + 32 * u);
+#pragma unroll
+        for (int u = 0; u < kGatherSeg / 16 / 32; ++u)
+          if (lane + 32 * u < cnt) dst[lane + 32 * u] = v[u];
+      }
+    }
   } else {
     pdl_wait();
     pdl_trigger();  // after this CTA's own dependency is resolved (see common.cuh)
@@ -577,12 +606,13 @@ int score_tc_packs_q(const LayerGeom& g) { return (g.ns % BM) != 0 || g.R <= BM;
 size_t score_tc_qpack_elems(int Hkv, int R_max) { return (size_t)Hkv * ((R_max + BM - 1) / BM) * BM * D; }
 
 cudaError_t launch_score_tc(const LayerGeom& g, const __nv_bfloat16* q, const __nv_bfloat16* probe_layer, float* lam2,
-                            float* lampart, int nsplit, void* qpack_ws, cudaStream_t st) {
+                            float* lampart, int nsplit, void* qpack_ws, const SpecGather& spec, cudaStream_t st) {
   if (score_tc_nsplit(g) == 0 || nsplit != score_tc_nsplit(g) || !qpack_ws) return cudaErrorNotSupported;
   TcParams p;
   p.g = g;
   p.lam2 = lam2;
   p.lampart = lampart;
+  p.spec = spec;
   p.nsplit = nsplit;
   p.NKT = nsplit / kColSplit;
   p.MT = (g.R + BM - 1) / BM;
