@@ -49,6 +49,20 @@ __device__ __forceinline__ void pdl_wait() {
   }
 #endif
 }
+// tuning build: a device-timeline mark (tag, CTA) by thread 0 of the calling CTA (CKV_DTL=1)
+__device__ __forceinline__ void dtl_mark(int tag) {
+#ifdef CKV_TUNING
+  if (g_dtl && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned i = atomicAdd(g_dtl_n, 1u) & 8191u;
+    g_dtl[2 * i] = t;
+    g_dtl[2 * i + 1] = 0xF0000000u | ((unsigned)tag << 8) | (blockIdx.x & 0xFF);
+  }
+#else
+  (void)tag;
+#endif
+}
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 bool pdl_enabled();  // tuning build: CKV_PDL=0 disables the launch attribute (A/B measurements)
 // A kernel that follows a cross-stream event wait is launched without the attribute (the

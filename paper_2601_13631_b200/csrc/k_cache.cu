@@ -59,14 +59,18 @@ __global__ void __launch_bounds__(NT) topk_plan2_kernel(TopkJob t, PlanJob a, Pl
   __shared__ PlanSmem ps;
   extern __shared__ uint64_t plan_skeys[];
   const bool c0 = blockIdx.x == 0;
+  dtl_mark(1);
   topk_body<NT, KPT>(c0 ? t.A : nullptr, t.Apart, t.nparts, t.m, t.k, 0, 1, c0 ? t.ids : t.ids_b, c0 ? t.cand : t.cand_b,
                      t.k, c0 ? t.n_out : t.n_b, ps.ss);
-  __syncthreads();  // this CTA's ids / n / keys (and CTA 0's A, read by the fused A9) are written
+  __syncthreads();
+  dtl_mark(2);  // this CTA's ids / n / keys (and CTA 0's A, read by the fused A9) are written
   const PlanJob& j = c0 ? a : b;
   const int n_ids = j.n_ids_dev ? *j.n_ids_dev : j.n_ids_host;
   const bool smem_keys = j.cl.P > NT * kPlanKPT && j.cl.P <= kPlanSmemKeysMax;
   cache_plan_body<NT>(j.cl, j.ids, n_ids, j.prefetch, j.quota, j.epoch, j.rec_bytes, j.scratch, j.out, ps,
                       smem_keys ? plan_skeys : nullptr);
+  __syncthreads();
+  dtl_mark(3);
 }
 
 // Whole-record copy host store -> HBM slot: work items are 4 KiB segments of records so a

@@ -300,8 +300,10 @@ __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart
       key[u] = ((uint64_t)__float_as_uint(a) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(j * id_mul + id_offset));
     }
   }
+  dtl_mark(4);
   const int kk = min(k, m);
   const uint64_t T = block_kth_largest_regs1<NT, KPT>(key, m, kk, ss);
+  dtl_mark(5);
   // ascending compaction
   const int base = block_compact_regs1<NT, KPT>(key, m, T, ss, [&](int pos, int j, uint64_t kv) {
     if (ids) ids[pos] = j * id_mul + id_offset;

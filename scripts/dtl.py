@@ -13,6 +13,20 @@ if os.environ.get("DTL_CHILD") != "1":
     if not recs:
         print(r.stdout[-2000:], r.stderr[-4000:])
         sys.exit(1)
+    marks = [x for x in recs if x[1] >= 0xF0000000]
+    recs = [x for x in recs if x[1] < 0xF0000000]
+    if marks:  # in-kernel marks (dtl_mark): mean time between consecutive marks of one CTA
+        by_cta = collections.defaultdict(list)
+        for t, gw, _, _ in marks:
+            by_cta[gw & 0xFF].append((t, (gw >> 8) & 0xFFFF))
+        seg = collections.defaultdict(list)
+        for c, v in by_cta.items():
+            v.sort()
+            for (t0, a), (t1, b) in zip(v, v[1:]):
+                if b != 1:
+                    seg[(c, a, b)].append((t1 - t0) * 1e-3)
+        for (c, a, b), v in sorted(seg.items()):
+            print(f"mark CTA {c}: {a} -> {b}: n={len(v)} mean={sum(v)/len(v):6.2f} us")
     tail = recs[-int(os.environ.get("DTL_LAST", "1400")):]
     side = {"gather_kernel"}
     main = [x for x in tail if x[3] not in side]
