@@ -273,7 +273,7 @@ def run_ckv(args, rank, world):
 
     # the request stream: WARM_CACHE untimed draws bring the HBM chunk cache to its steady state
     # ("warm up"), then the W warm-up and K timed steps follow the same stream
-    seq = request_sequence(WARM_CACHE + args.warmup + 2 * args.steps)
+    seq = request_sequence(WARM_CACHE + args.warmup + 2 * args.steps + 4)  # + the untimed e2e warm-ups
     for r in seq[:WARM_CACHE]:
         run_request(r)
     off = WARM_CACHE

@@ -52,23 +52,57 @@ __global__ void __launch_bounds__(NT) cache_plan2_kernel(PlanJob a, PlanJob b) {
 // A3 + the two plans above in one launch: the top-k is single-CTA work, so both CTAs compute it
 // (same keys, same result) instead of a separate one-CTA launch whose completion the plans would
 // wait for -- one kernel boundary less on the layer's serial chain.
+// Shared-memory layout of the table copies: ids [k], A, slot_of, I, F [m], owner, pf_epoch [P] (4-byte words).
+inline size_t tables_smem_bytes(int k, int m, int P) { return 4 * ((size_t)k + 4 * (size_t)m + 2 * (size_t)P); }
+
 template <int KPT>
-__global__ void __launch_bounds__(NT) topk_plan2_kernel(TopkJob t, PlanJob a, PlanJob b) {
+__global__ void __launch_bounds__(NT) topk_plan2_kernel(TopkJob t, PlanJob a, PlanJob b, int use_tables) {
   pdl_wait();
   pdl_trigger();
   __shared__ PlanSmem ps;
   extern __shared__ uint64_t plan_skeys[];
   const bool c0 = blockIdx.x == 0;
-  dtl_mark(1);
-  topk_body<NT, KPT>(c0 ? t.A : nullptr, t.Apart, t.nparts, t.m, t.k, 0, 1, c0 ? t.ids : t.ids_b, c0 ? t.cand : t.cand_b,
-                     t.k, c0 ? t.n_out : t.n_b, ps.ss);
-  __syncthreads();
-  dtl_mark(2);  // this CTA's ids / n / keys (and CTA 0's A, read by the fused A9) are written
   const PlanJob& j = c0 ? a : b;
-  const int n_ids = j.n_ids_dev ? *j.n_ids_dev : j.n_ids_host;
-  const bool smem_keys = j.cl.P > NT * kPlanKPT && j.cl.P <= kPlanSmemKeysMax;
+  dtl_mark(1);
+  PlanTables tc;
+  float* As = nullptr;
+  int32_t* ids_s = nullptr;
+  if (use_tables) {  // this CTA's layer tables -> shared memory, asynchronously, while the top-k runs
+    int32_t* w = reinterpret_cast<int32_t*>(plan_skeys);
+    ids_s = w;
+    As = reinterpret_cast<float*>(w + t.k);
+    int32_t* sl = w + t.k + t.m;
+    float* sI = reinterpret_cast<float*>(sl + t.m);
+    int32_t* sF = sl + 2 * t.m;
+    int32_t* so = sl + 3 * t.m;
+    int32_t* sp = so + j.cl.P;
+    for (int i = threadIdx.x; i < t.m; i += NT) {
+      cp_async4(sl + i, j.cl.slot_of + i);
+      cp_async4(sI + i, j.cl.I + i);
+      cp_async4(sF + i, j.cl.F + i);
+    }
+    for (int i = threadIdx.x; i < j.cl.P; i += NT) {
+      cp_async4(so + i, j.cl.owner + i);
+      cp_async4(sp + i, j.cl.pf_epoch + i);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    tc.ids = ids_s;
+    tc.A = As;
+    tc.slot_of = sl;
+    tc.I = sI;
+    tc.F = sF;
+    tc.owner = so;
+    tc.pf_epoch = sp;
+  }
+  topk_body<NT, KPT>(c0 ? t.A : nullptr, t.Apart, t.nparts, t.m, t.k, 0, 1, c0 ? t.ids : t.ids_b, c0 ? t.cand : t.cand_b,
+                     t.k, c0 ? t.n_out : t.n_b, ps.ss, As, ids_s);
+  if (use_tables) asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();  // this CTA's ids / n / keys (and CTA 0's A, read by the fused A9) are written
+  dtl_mark(2);
+  const int n_ids = use_tables ? min(t.k, t.m) : (j.n_ids_dev ? *j.n_ids_dev : j.n_ids_host);
+  const bool smem_keys = !use_tables && j.cl.P > NT * kPlanKPT && j.cl.P <= kPlanSmemKeysMax;
   cache_plan_body<NT>(j.cl, j.ids, n_ids, j.prefetch, j.quota, j.epoch, j.rec_bytes, j.scratch, j.out, ps,
-                      smem_keys ? plan_skeys : nullptr);
+                      smem_keys ? plan_skeys : nullptr, tc);
   __syncthreads();
   dtl_mark(3);
 }
@@ -227,16 +261,22 @@ cudaError_t launch_topk_plan2(const TopkJob& t, const PlanJob& a, const PlanJob&
   const int P = a.cl.P > b.cl.P ? a.cl.P : b.cl.P;
   const bool big = P > NT * kPlanKPT && P <= kPlanSmemKeysMax;
   if (big) smem = (size_t)P * sizeof(uint64_t);
+  // table copies in shared memory: per-layer pools only (the demand and the speculative plan each
+  // see one layer's [m_loc] tables) with register-resident victim keys (P <= NT * kPlanKPT)
+  static const bool tables_on = !(tuning_env("CKV_PLAN_TABLES") && tuning_env("CKV_PLAN_TABLES")[0] == '0');
+  const size_t tb = tables_smem_bytes(t.k, t.m, P);
+  const int use_tables =
+      (tables_on && !big && a.cl.m_loc == t.m && b.cl.m_loc == t.m && tb <= 200 * 1024) ? 1 : 0;
+  if (use_tables) smem = tb;
   static bool attr = false;
-  if (big && !attr) {
+  if (!attr) {
     for (auto kern : {topk_plan2_kernel<1>, topk_plan2_kernel<2>, topk_plan2_kernel<4>, topk_plan2_kernel<8>})
-      if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)(kPlanSmemKeysMax * sizeof(uint64_t))))
+      if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
         return e;
     attr = true;
   }
-  auto go = [&](void (*kern)(TopkJob, PlanJob, PlanJob)) -> cudaError_t {
-    if (cudaError_t e_ = launch_kernel(kern, 2, NT, smem, st, t, a, b)) return e_;
+  auto go = [&](void (*kern)(TopkJob, PlanJob, PlanJob, int)) -> cudaError_t {
+    if (cudaError_t e_ = launch_kernel(kern, 2, NT, smem, st, t, a, b, use_tables)) return e_;
     return cudaGetLastError();
   };
   if (t.m <= NT) return go(topk_plan2_kernel<1>);

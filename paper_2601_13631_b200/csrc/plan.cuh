@@ -27,6 +27,24 @@ __device__ __forceinline__ bool bsearch_ids(const int32_t* ids, int n, int j) {
 constexpr int kPlanKPT = 4;  // victim keys per thread held in registers (P <= 4 * NT)
 constexpr int kPlanSmemKeysMax = 24 * 1024;  // larger pools: keys in dynamic shared memory (192 KB)
 
+// Shared-memory copies of one layer's cache tables (the fused top-k / plan kernel, k_cache.cu):
+// copied with cp.async while the top-k runs, so the planner's lookups (hit / miss, spec-used, A9
+// read-modify-write, free slots, victim candidates) cost no dependent global round trip.  Any
+// pointer may be null (read global memory); the planner's writes always go to global memory.
+struct PlanTables {
+  const int32_t* ids = nullptr;       // [n_ids] the plan's ids (this CTA's top-k output)
+  const float* A = nullptr;           // [m_loc] chunk scores (the fused A9's I += A)
+  const int32_t* slot_of = nullptr;   // [m_loc]
+  const float* I = nullptr;           // [m_loc]
+  const int32_t* F = nullptr;         // [m_loc]
+  const int32_t* owner = nullptr;     // [P]
+  const int32_t* pf_epoch = nullptr;  // [P]
+};
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
 struct PlanSmem {
   SelectSmem ss;
   int hits, spec_used;
@@ -37,7 +55,8 @@ struct PlanSmem {
 template <int NT>
 __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict__ ids, int n_ids, int prefetch,
                                 int quota, int epoch, int64_t rec_bytes, int32_t* __restrict__ scratch,
-                                const PlanOut& out, PlanSmem& ps, uint64_t* skeys = nullptr) {
+                                const PlanOut& out, PlanSmem& ps, uint64_t* skeys = nullptr,
+                                const PlanTables& tc = PlanTables()) {
   SelectSmem& ss = ps.ss;
   int& s_hits = ps.hits;
   int& s_spec_used = ps.spec_used;
@@ -62,19 +81,19 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
     bool is_miss = false;
     int j = -1;
     if (t < n_ids) {
-      j = ids[t];
-      const int s = cl.slot_of[j];
+      j = tc.ids ? tc.ids[t] : ids[t];
+      const int s = tc.slot_of ? tc.slot_of[j] : cl.slot_of[j];
       is_miss = s < 0;
       if (!is_miss) {
         atomicAdd(&s_hits, 1);
         if (use_bits) atomicOr(&ps.req_bits[s >> 5], 1u << (s & 31));
-        if (!prefetch && cl.pf_epoch[s] == epoch) atomicAdd(&s_spec_used, 1);
+        if (!prefetch && (tc.pf_epoch ? tc.pf_epoch[s] : cl.pf_epoch[s]) == epoch) atomicAdd(&s_spec_used, 1);
       }
       if (out.kept_slots) out.kept_slots[t] = s;  // misses: -1 until step 4 assigns a slot
       if (out.ids_out) out.ids_out[t] = j;
       if (out.upd_A) {
-        cl.I[j] += out.upd_A[j];
-        cl.F[j] += 1;
+        cl.I[j] = (tc.I ? tc.I[j] : cl.I[j]) + (tc.A ? tc.A[j] : out.upd_A[j]);
+        cl.F[j] = (tc.F ? tc.F[j] : cl.F[j]) + 1;
         cl.T[j] = epoch;
       }
     }
@@ -120,7 +139,7 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
   if (n_miss > 0)
     for (int b = 0; b < cl.P; b += NT) {
       const int s = b + threadIdx.x;
-      const bool f = s < cl.P && cl.owner[s] < 0;
+      const bool f = s < cl.P && (tc.owner ? tc.owner[s] : cl.owner[s]) < 0;
       int tot;
       const int pos = block_excl_scan<NT>(f ? 1 : 0, tot, ss);
       if (f) freel[n_free + pos] = s;
@@ -131,7 +150,7 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
   int n_vict = 0;
   if (need > 0) {
     auto key = [&](int s) -> uint64_t {
-      const int e = cl.owner[s];  // table index layer * m_loc + j
+      const int e = tc.owner ? tc.owner[s] : cl.owner[s];  // table index layer * m_loc + j
       if (e < 0) return 0ull;
       if (use_bits) {  // requested by this plan = the slot of a hit (marked in step 1)
         if (ps.req_bits[s >> 5] & (1u << (s & 31))) return 0ull;
@@ -139,7 +158,7 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
         const int jl = e - cl.lbase;
         if (jl >= 0 && jl < cl.m_loc && bsearch_ids(ids, n_ids, jl)) return 0ull;
       }
-      if (!prefetch && cl.pf_epoch[s] == epoch) return 0ull;
+      if (!prefetch && (tc.pf_epoch ? tc.pf_epoch[s] : cl.pf_epoch[s]) == epoch) return 0ull;
       // Eq. 2 by default; the ablation policies of PAPER.md:610-613.  Ties by
       // (S, layer, j) = (S, e)
       const float S = cl.policy == 0 ? cl.I0[e] * (float)cl.F0[e] : cl.policy == 1 ? (float)cl.F0[e] : (float)cl.T0[e];
@@ -227,7 +246,7 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
     __syncthreads();
     for (int t = threadIdx.x; t < n_vict; t += NT) {
       const int s = vict[t];
-      const int e = cl.owner[s];
+      const int e = tc.owner ? tc.owner[s] : cl.owner[s];
       if (out.victims) out.victims[t] = e;
       cl.slot_of0[e] = -1;
       cl.owner[s] = -1;

@@ -282,7 +282,7 @@ __device__ int block_compact_regs1(const uint64_t (&keys)[KPT], int n, uint64_t 
 template <int NT, int KPT>
 __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart, int nparts, int m, int k,
                           int id_offset, int id_mul, int32_t* __restrict__ ids, uint64_t* __restrict__ cand, int n_cand_out,
-                          int32_t* __restrict__ n_out, SelectSmem& ss) {
+                          int32_t* __restrict__ n_out, SelectSmem& ss, float* As = nullptr, int32_t* ids_s = nullptr) {
   uint64_t key[KPT];
 #pragma unroll
   for (int u = 0; u < KPT; ++u) {
@@ -294,6 +294,7 @@ __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart
         a = 0.f;
         for (int h = 0; h < nparts; ++h) a += __ldcg(Apart + (size_t)h * m + j);
         if (A) A[j] = a;  // (null: a private copy of the select, topk_plan2_kernel's CTA 1)
+        if (As) As[j] = a;  // shared-memory copy for a planner in the same CTA
       } else {
         a = A[j];
       }
@@ -307,6 +308,7 @@ __device__ void topk_body(float* __restrict__ A, const float* __restrict__ Apart
   // ascending compaction
   const int base = block_compact_regs1<NT, KPT>(key, m, T, ss, [&](int pos, int j, uint64_t kv) {
     if (ids) ids[pos] = j * id_mul + id_offset;
+    if (ids_s) ids_s[pos] = j * id_mul + id_offset;
     if (cand) cand[pos] = kv;
   });
   if (cand)
