@@ -106,7 +106,7 @@ __device__ __forceinline__ bool tile_present(const AttnParams& p, const Tiles& t
 // slot s, so the layer has no separate gather launch on its critical path.
 // V-only store (rec_swz 2): the K pieces come from the HBM probe array ([Hkv][n_pad][128], rows of
 // the chunk's local tokens), swizzled on the way; the records (slots, host) hold V alone.
-__global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __restrict__ pool,
+__global__ void __launch_bounds__(256, 3) compact_kv_kernel(LayerGeom g, char* __restrict__ pool,
                                                          const char* __restrict__ host_layer,
                                                          const __nv_bfloat16* __restrict__ probe,
                                                          const int32_t* __restrict__ kept_ids,
@@ -177,13 +177,13 @@ __global__ void __launch_bounds__(256) compact_kv_kernel(LayerGeom g, char* __re
         const uint4* src = reinterpret_cast<const uint4*>(host_layer + (int64_t)kept_ids[i] * rec_bytes + off);
         uint4* cdst = reinterpret_cast<uint4*>(pool + (int64_t)(-slot - 2) * rec_bytes + off);
         const int nu = (int)(piece / 16);
-        for (int u0 = 0; u0 < nu; u0 += 32 * 8) {  // 8 host loads in flight per lane
-          uint4 v[8];
+        for (int u0 = 0; u0 < nu; u0 += 32 * 4) {  // 4 host loads in flight per lane (whole 2 KB piece)
+          uint4 v[4];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
+          for (int q = 0; q < 4; ++q)
             if (u0 + lane + 32 * q < nu) v[q] = __ldg(src + u0 + lane + 32 * q);
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
+          for (int q = 0; q < 4; ++q)
             if (u0 + lane + 32 * q < nu) {
               dst[dunit(u0 + lane + 32 * q)] = v[q];
               cdst[u0 + lane + 32 * q] = v[q];
@@ -605,7 +605,7 @@ cudaError_t launch_attn_tc(const LayerGeom& g, const __nv_bfloat16* q, const __n
   p.lam_ref = lam_ref;
   const int64_t rec_bytes = (int64_t)(g.rec_swz == 2 ? 1 : 2) * g.Hkv * g.c * D * 2;
   const int64_t n_warps = (int64_t)g.Hkv * k_cap * 4 + (include_suffix ? (int64_t)g.Hkv * g.ns * 2 : 0);
-  const int cblocks = (int)std::min<int64_t>((n_warps + 7) / 8, 8 * sm_count());
+  const int cblocks = (int)std::min<int64_t>((n_warps + 7) / 8, 3 * sm_count());  // one resident wave (3 CTAs / SM)
   if (cudaError_t e_ = launch_kernel(compact_kv_kernel, cblocks, 256, 0, st, g,
                                      reinterpret_cast<char*>(const_cast<__nv_bfloat16*>(pool_layer)), host_layer,
                                      probe_layer,
