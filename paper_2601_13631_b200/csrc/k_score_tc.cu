@@ -560,7 +560,7 @@ cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPa
 
 // pairs of every 8 (i.e. exponentials of every 16) evaluated by the FFMA2 polynomial instead of
 // MUFU.EX2; the tuning build's CKV_SCORE_POLY overrides it for A/B sweeps
-constexpr int kPolyPairs = 3;
+constexpr int kPolyPairs = 2;
 int poly_pairs() {
   static int np = -1;
   if (np < 0) {
@@ -577,7 +577,7 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
   switch (poly_pairs()) {
     case 0: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
     case 1: return launch_cp<C, 1>(tmK, tmQ, p, grid, st);
-    case 2: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
+    case 3: return launch_cp<C, 3>(tmK, tmQ, p, grid, st);
     case 4: return launch_cp<C, 4>(tmK, tmQ, p, grid, st);
     case 5: return launch_cp<C, 5>(tmK, tmQ, p, grid, st);
     case 6: return launch_cp<C, 6>(tmK, tmQ, p, grid, st);
