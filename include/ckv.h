@@ -12,7 +12,9 @@
  *          PAPER.md:424-455, Eq. 2) and gather the misses as whole chunks from the
  *          pinned, chunk-contiguous host store;
  *   A6     speculatively prefetch the next layer's chunks from this layer's ids
- *          on a side stream (inter-period prefetch at p = 1);
+ *          (inter-period prefetch at p = 1): planned with this
+ *          layer's plan, copied by a warp of the next layer's score kernel (bf16,
+ *          tcgen05 path) or on a side stream (periods, fp32 / SIMT path);
  *   A7/A8  exact softmax attention of the suffix queries over the kept chunks plus
  *          the causal suffix, split-K with an LSE combine;
  *   A9     cache-score update I_j += A_j, F_j += 1.
@@ -150,9 +152,12 @@ ckv_status ckv_store_prefix(ckv_ctx* ctx, int32_t layer, const void* k, const vo
  *  out    device [n_suffix, Hq, d]  attention output, cfg.dtype
  *  selected_ids  device int32 [k]   selected chunk ids, ascending (global ids)
  *  chunk_scores  device float [m] or NULL: A_j (Eq. 1) for parity/debug
- * Layer 0 starts a new request; layers must be called in order.  With period p = 1 every
- * layer runs A1-A9; if prefetch_chunks > 0 and layer + 1 < L the call also enqueues the
- * speculative prefetch of layer + 1 (this layer's ids) on the side stream.  With p > 1 only the
+ * Layer 0 starts a new request; layers must be called in order, and the calls of one request on
+ * one stream (or stream-ordered by the caller: a call reads what the previous one enqueued,
+ * e.g. the speculative copy list).  With period p = 1 every
+ * layer runs A1-A9; if prefetch_chunks > 0 and layer + 1 < L the call also plans the
+ * speculative prefetch of layer + 1 (this layer's ids); its copy runs inside the next call's
+ * score kernel (tcgen05 path) or on the side stream.  With p > 1 only the
  * first layer of a period identifies chunks; it then enqueues the loads of the period's other
  * layers (exact ids) and the speculative load of the next period's first layer; the other
  * layers reuse the ids (selected_ids / chunk_scores report the period's).

@@ -559,8 +559,12 @@ cudaError_t launch_cp(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPa
 }
 
 // pairs of every 8 (i.e. exponentials of every 16) evaluated by the FFMA2 polynomial instead of
-// MUFU.EX2; the tuning build's CKV_SCORE_POLY overrides it for A/B sweeps
+// MUFU.EX2; the tuning build's CKV_SCORE_POLY overrides it for A/B sweeps.  Measured on B200: 2 at
+// c = 16 (C3: 87.1 vs 87.9 us/layer with 3), 3 for c <= 8 (C5 c = 4: 497 vs 525 us of A1 with 2 --
+// its 16 lg2 per 64-key pass already load the MUFU pipe)
 constexpr int kPolyPairs = 2;
+template <int C>
+constexpr int poly_pairs_c() { return C <= 8 ? 3 : kPolyPairs; }
 int poly_pairs() {
   static int np = -1;
   if (np < 0) {
@@ -577,6 +581,7 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
   switch (poly_pairs()) {
     case 0: return launch_cp<C, 0>(tmK, tmQ, p, grid, st);
     case 1: return launch_cp<C, 1>(tmK, tmQ, p, grid, st);
+    case 2: return launch_cp<C, 2>(tmK, tmQ, p, grid, st);
     case 3: return launch_cp<C, 3>(tmK, tmQ, p, grid, st);
     case 4: return launch_cp<C, 4>(tmK, tmQ, p, grid, st);
     case 5: return launch_cp<C, 5>(tmK, tmQ, p, grid, st);
@@ -585,10 +590,10 @@ cudaError_t launch_c(const CUtensorMap& tmK, const CUtensorMap& tmQ, const TcPar
   }
 #endif
   (void)poly_pairs;
-  return launch_cp<C, kPolyPairs>(tmK, tmQ, p, grid, st);
+  return launch_cp<C, poly_pairs_c<C>()>(tmK, tmQ, p, grid, st);
 }
 
-#define CKV_SC(C) (const void*)score_tc_kernel<C, kPolyPairs, 2, 3>, (const void*)score_tc_kernel<C, kPolyPairs, 3, 1>
+#define CKV_SC(C) (const void*)score_tc_kernel<C, poly_pairs_c<C>(), 2, 3>, (const void*)score_tc_kernel<C, poly_pairs_c<C>(), 3, 1>
 const int kReg = register_kernels({CKV_SC(1), CKV_SC(2), CKV_SC(4), CKV_SC(8), CKV_SC(16), CKV_SC(32), CKV_SC(64),
                                    (const void*)pack_q_kernel});
 #undef CKV_SC

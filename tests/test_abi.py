@@ -70,5 +70,6 @@ def test_config_validation_needs_no_gpu():
 def test_product_library_has_no_tuning_knobs():
     # timing-only modes and env knobs live in the tuning build only (build.py --tuning)
     data = open(ckv.LIB_PATH, "rb").read()
-    for knob in (b"CKV_KNOCKOUT", b"CKV_SCORE_POLY", b"CKV_PDL_SKIP", b"CKV_ATTN_TRACE", b"CKV_TIMELINE"):
+    for knob in (b"CKV_KNOCKOUT", b"CKV_SCORE_POLY", b"CKV_PDL_SKIP", b"CKV_ATTN_TRACE", b"CKV_TIMELINE", b"CKV_DTL",
+                 b"CKV_SCORE_DBG", b"CKV_TOPK_PLAN", b"CKV_SPEC_INSCORE", b"CKV_PLAN_TABLES"):
         assert knob not in data, knob
