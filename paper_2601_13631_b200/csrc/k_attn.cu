@@ -202,6 +202,15 @@ __global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_par
   if (row >= nrow) return;
   const int kvh = row / g.R, rho = row % g.R;
   const int gq = rho / g.ns, r = rho % g.ns, h = kvh * g.G + gq;
+  // d = 128, <= 8 splits: the partial O loads are issued first, so their L2 round trip overlaps
+  // the LSE loads and the weight reduction (empty splits' partials are loaded but never used)
+  const bool d128 = g.d == 128 && nsplit <= 8;
+  float4 v[8];
+  if (d128) {
+#pragma unroll
+    for (int sp = 0; sp < 8; ++sp)
+      if (sp < nsplit) v[sp] = __ldcg(reinterpret_cast<const float4*>(o_part + (sp * nrow + row) * g.d + lane * 4));
+  }
   // lane s < nsplit holds split s's lse (nsplit <= 64: two rounds)
   float l0 = (lane < nsplit) ? lse_part[lane * nrow + row] : -INFINITY;
   float l1 = (lane + 32 < nsplit) ? lse_part[(lane + 32) * nrow + row] : -INFINITY;
@@ -226,10 +235,11 @@ __global__ void attn_combine_kernel(LayerGeom g, const float* __restrict__ o_par
   if ((g.d & 127) == 0 && nsplit <= 8) {
     // all split loads issued before the weighted sum (independent 16-byte loads in flight)
     for (int x = lane * 4; x < g.d; x += 128) {
-      float4 v[8];
+      if (!d128) {
 #pragma unroll
-      for (int sp = 0; sp < 8; ++sp)
-        if (sp < nsplit) v[sp] = __ldcg(reinterpret_cast<const float4*>(o_part + (sp * nrow + row) * g.d + x));
+        for (int sp = 0; sp < 8; ++sp)
+          if (sp < nsplit) v[sp] = __ldcg(reinterpret_cast<const float4*>(o_part + (sp * nrow + row) * g.d + x));
+      }
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int sp = 0; sp < 8; ++sp) {
