@@ -161,7 +161,13 @@ __device__ void cache_plan_body(const CacheLayer& cl, const int32_t* __restrict_
       if (!prefetch && (tc.pf_epoch ? tc.pf_epoch[s] : cl.pf_epoch[s]) == epoch) return 0ull;
       // Eq. 2 by default; the ablation policies of PAPER.md:610-613.  Ties by
       // (S, layer, j) = (S, e)
-      const float S = cl.policy == 0 ? cl.I0[e] * (float)cl.F0[e] : cl.policy == 1 ? (float)cl.F0[e] : (float)cl.T0[e];
+      // (I, F of this layer's residents from the shared-memory copies when present: per-layer pools
+      // hold this layer's chunks only, and the fused A9 touches requested chunks, never candidates)
+      const int jl = e - cl.lbase;
+      const bool tl = tc.I && jl >= 0 && jl < cl.m_loc;
+      const float I = tl ? tc.I[jl] : cl.I0[e];
+      const int F = tl ? tc.F[jl] : cl.F0[e];
+      const float S = cl.policy == 0 ? I * (float)F : cl.policy == 1 ? (float)F : (float)cl.T0[e];
       return ~(((uint64_t)__float_as_uint(S) << 32) | (uint64_t)(uint32_t)e);
     };
     if (cl.P <= NT * kPlanKPT) {
