@@ -236,6 +236,7 @@ __device__ uint64_t block_kth_largest_regs1(const uint64_t (&keys)[KPT], int n, 
     sel = __shfl_sync(0xffffffffu, sel, src);
     knew = __shfl_sync(0xffffffffu, knew, src);
     done = __shfl_sync(0xffffffffu, done, src);
+    dtl_mark(10 + p);  // tuning build: end of radix pass p
     prefix |= (uint64_t)sel << shift;
     mask |= (uint64_t)255u << shift;
     krem = knew;
