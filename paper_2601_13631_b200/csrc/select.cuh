@@ -196,11 +196,15 @@ __device__ uint64_t block_kth_largest_regs1(const uint64_t (&keys)[KPT], int n, 
     for (int u = 0; u < KPT; ++u) {
       const int i = threadIdx.x + NT * u;
       const bool in = i < n && (keys[u] & mask) == prefix;
-      const unsigned act = __ballot_sync(0xffffffffu, in);
-      if (in) {
-        const unsigned dig = (unsigned)(keys[u] >> shift) & 255u;
-        const unsigned peers = __match_any_sync(act, dig);
-        if (lane == __ffs(peers) - 1) atomicAdd(&h[dig], __popc(peers));
+      if (p == 0) {  // the top byte (sign + exponent bits): few distinct digits per warp -> aggregate
+        const unsigned act = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const unsigned dig = (unsigned)(keys[u] >> shift) & 255u;
+          const unsigned peers = __match_any_sync(act, dig);
+          if (lane == __ffs(peers) - 1) atomicAdd(&h[dig], __popc(peers));
+        }
+      } else if (in) {  // mantissa bytes: digits nearly distinct in a warp -> one atomic per key
+        atomicAdd(&h[(unsigned)(keys[u] >> shift) & 255u], 1);
       }
     }
     __syncthreads();
