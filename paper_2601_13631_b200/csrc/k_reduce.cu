@@ -171,13 +171,48 @@ __device__ __forceinline__ void chunk_sum_warp(const LayerGeom& g, const float* 
   if (lane == 0) Apart[warp] = s;
 }
 
+// lam2 comes from the score kernel, which is older than this kernel's stream predecessor (the row
+// normaliser) and so has completed when this kernel starts (programmatic launch: at most two
+// kernels of a stream overlap, common.cuh): its loads are issued BEFORE pdl_wait() and overlap the
+// row normaliser; only Lam2 needs the wait.  (R % 4 == 0, R <= 1024: 8 x 16 B per lane in flight.)
 __global__ void chunk_sum_kernel(LayerGeom g, const float* __restrict__ lam2, const float* __restrict__ Lam2,
                                  float* __restrict__ Apart) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const bool live = warp < g.m_loc * g.Hkv;
+  if (live && (g.R & 3) == 0 && g.R <= 1024) {
+    const int kvh = warp / g.m_loc, j = warp % g.m_loc;
+    const float* src = lam2 + ((size_t)kvh * g.m_loc + j) * g.R;
+    float4 a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = lane * 4 + 128 * i;
+      if (row < g.R) a[i] = __ldcg(reinterpret_cast<const float4*>(src + row));
+    }
+    pdl_wait();
+    pdl_trigger();
+    const float* L = Lam2 + (size_t)kvh * g.R;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int row = lane * 4 + 128 * i;
+      if (row < g.R) {
+        const float4 b = *reinterpret_cast<const float4*>(L + row);
+        acc[0] += fast_exp2(a[i].x - b.x);
+        acc[1] += fast_exp2(a[i].y - b.y);
+        acc[2] += fast_exp2(a[i].z - b.z);
+        acc[3] += fast_exp2(a[i].w - b.w);
+      }
+    }
+    float sum = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) Apart[warp] = sum;
+    return;
+  }
   pdl_wait();
   pdl_trigger();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (warp >= g.m_loc * g.Hkv) return;
-  chunk_sum_warp(g, lam2, Lam2, Apart, warp, threadIdx.x & 31);
+  if (!live) return;
+  chunk_sum_warp(g, lam2, Lam2, Apart, warp, lane);
 }
 
 const int kReg = register_kernels({(const void*)row_lse_kernel<float>, (const void*)row_lse_kernel<__nv_bfloat16>,
