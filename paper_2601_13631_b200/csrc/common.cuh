@@ -20,8 +20,9 @@ namespace ckv {
 // the completion of its predecessor, so at most two kernels of a stream overlap and every
 // kernel older than the predecessor has completed.  (Triggering before the wait let three-
 // kernel chains -- plan, gather, attention -- read stale data: measured on B200.)  Only
-// constant inputs (q, k_suf, v_suf, the probe keys), TMEM / shared-memory setup and tensor-map
-// prefetches may precede pdl_wait().
+// constant inputs (q, k_suf, v_suf, the probe keys), TMEM / shared-memory setup, tensor-map
+// prefetches and data whose last writer is older than the stream predecessor (chunk sums: the
+// score kernel's lam2; the fused select: the cache tables) may precede pdl_wait().
 #ifdef CKV_TUNING
 // Device timeline (tuning build, CKV_DTL=1): CTA 0 / thread 0 of every kernel records the time its
 // pdl_wait() returned (= its predecessor completed) with its grid / block size; the per-TU

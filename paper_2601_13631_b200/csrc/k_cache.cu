@@ -57,13 +57,10 @@ inline size_t tables_smem_bytes(int k, int m, int P) { return 4 * ((size_t)k + 4
 
 template <int KPT>
 __global__ void __launch_bounds__(NT) topk_plan2_kernel(TopkJob t, PlanJob a, PlanJob b, int use_tables) {
-  pdl_wait();
-  pdl_trigger();
   __shared__ PlanSmem ps;
   extern __shared__ uint64_t plan_skeys[];
   const bool c0 = blockIdx.x == 0;
   const PlanJob& j = c0 ? a : b;
-  dtl_mark(1);
   PlanTables tc;
   float* As = nullptr;
   int32_t* ids_s = nullptr;
@@ -86,6 +83,9 @@ __global__ void __launch_bounds__(NT) topk_plan2_kernel(TopkJob t, PlanJob a, Pl
       cp_async4(sp + i, j.cl.pf_epoch + i);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
+    // (issued before pdl_wait: the tables' last writers -- the previous request's plans and the
+    // speculative plan of this layer, CTA 1 of the previous layer's launch -- are older than this
+    // kernel's stream predecessor, the chunk sums, so they have completed)
     tc.ids = ids_s;
     tc.A = As;
     tc.slot_of = sl;
@@ -94,6 +94,9 @@ __global__ void __launch_bounds__(NT) topk_plan2_kernel(TopkJob t, PlanJob a, Pl
     tc.owner = so;
     tc.pf_epoch = sp;
   }
+  pdl_wait();
+  pdl_trigger();
+  dtl_mark(1);
   topk_body<NT, KPT>(c0 ? t.A : nullptr, t.Apart, t.nparts, t.m, t.k, 0, 1, c0 ? t.ids : t.ids_b, c0 ? t.cand : t.cand_b,
                      t.k, c0 ? t.n_out : t.n_b, ps.ss, As, ids_s);
   if (use_tables) asm volatile("cp.async.wait_all;" ::: "memory");
